@@ -1,0 +1,283 @@
+/*
+ * scion_b200.h — C ABI of the B200-native traversal backend for Scion BVH layouts.
+ *
+ * This is the drop-in boundary for ONE path of the reference (arxiv 2511.15028,
+ * `layoutc`): executing closest-hit ray/triangle and closest-point queries over
+ * a PhysicalTree whose node layout was chosen by a Scion layout specification.
+ *
+ * The reference ships no header for its exec layer (include/layoutc/ has no
+ * interp/harness/scene/emit header; src/interp.cpp, src/emit_c.cpp,
+ * src/build_physical.cpp, src/scene.cpp, src/logical.cpp, src/rng.cpp and
+ * src/harness.cpp are placeholders).  Every entry point below therefore cites the
+ * SPEC.md contract (and, where one exists, the reference header) it stands in for.
+ *
+ * Conventions
+ *   - every function returns int: 0 = SCION_OK, otherwise a scion_status code;
+ *     nothing throws across the boundary; scion_last_error() gives the message
+ *     of the calling thread's last failure.
+ *   - plain pointers and sizes only; no torch / STL types.
+ *   - "d_" pointers are device pointers on the tree's device, "h_" pointers are
+ *     host pointers.  Device launches are asynchronous on the given stream
+ *     (cudaStream_t passed as void*; NULL = the legacy default stream).
+ *   - a scion_dtree is immutable after creation: concurrent launches on
+ *     different streams are legal.
+ */
+#ifndef SCION_B200_H
+#define SCION_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCION_ABI_VERSION 1
+
+typedef enum scion_status {
+  SCION_OK = 0,
+  SCION_ERR_ARG = 1,       /* bad argument / unknown name (CLI exit code 2 class)  */
+  SCION_ERR_LAYOUT = 2,    /* layout spec rejected (PlanError class, plan.hpp:89)              */
+  SCION_ERR_BUILD = 3,     /* builder hard fault: count/emit disagreement, capacity */
+  SCION_ERR_CUDA = 4,      /* CUDA runtime failure                                              */
+  SCION_ERR_NO_DEVICE = 5, /* no CUDA device: the product path has NO CPU fallback              */
+  SCION_ERR_QUERY = 6      /* at least one query reported an error status        */
+} scion_status;
+
+/* per-query status word (overflow / OOB are query errors, never silent) */
+#define SCION_Q_OK 0u
+#define SCION_Q_STACK_OVERFLOW 1u
+
+/* layout families — /root/reference/proj/include/layoutc/corpus.hpp:11 (enum Family) */
+#define SCION_FAMILY_BVH2 0
+#define SCION_FAMILY_DOP14 1
+#define SCION_FAMILY_BVH8 2
+
+#define SCION_MISS_PRIM 0xFFFFFFFFu
+#define SCION_STACK_DEPTH 64 /* specialize.hpp:57 CompileOptions::stack_depth */
+
+/* ------------------------------------------------------------------------- */
+/* Query / result records                                                     */
+/* ------------------------------------------------------------------------- */
+
+/* Ray(origin, direction, tmax = inf) — corpus/lib/geometry.scion:4, padded to 32 B
+ * so that one ray is two 16-byte vector loads. */
+typedef struct scion_ray {
+  float ox, oy, oz, tmax;
+  float dx, dy, dz, pad;
+} scion_ray;
+
+/* closest_hit's `best: mut (f32, Triangle)` (corpus/alg/chrt.scion:2): the triangle
+ * is reported as its index in the tree-ordered primitives array.  Miss:
+ * t = +inf, prim = SCION_MISS_PRIM. */
+typedef struct scion_hit {
+  float t;
+  uint32_t prim;
+} scion_hit;
+
+/* closest_point's `best: mut (f32, Point)` (corpus/alg/cpq.scion:3) plus the chosen
+ * primitive (harness contract "identical chosen primitive").
+ * prim = SCION_MISS_PRIM when d2 was only ever tightened by the farthest-corner
+ * bound and no primitive improved it. */
+typedef struct scion_cp {
+  float d2;
+  float x, y, z;
+  uint32_t prim;
+} scion_cp;
+
+typedef struct scion_counters { /* interpreter cost counters */
+  uint32_t node_visits; /* node decodes (CPQ: incl. the two child peeks per interior) */
+  uint32_t prim_tests;  /* triangle tests */
+} scion_counters;
+
+/* ------------------------------------------------------------------------- */
+/* Logical tree interchange (what oracle and GPU both consume)                */
+/* ------------------------------------------------------------------------- */
+
+/* Binary LogicalTree node, nodes stored in preorder. */
+typedef struct scion_lnode {
+  float lo[3], hi[3];
+  int32_t left, right;  /* node indices, or -1/-1 for a Leaf */
+  uint32_t first_prim;  /* Leaf: first triangle in the tree-ordered array */
+  uint32_t nprims;      /* Leaf: count (>0); Interior: 0 */
+} scion_lnode;
+
+/* 8-wide LogicalTree interior (collapse_to_wide). Children are
+ * left-packed; unused slots are SENTINELs with an inverted box (lo=+inf, hi=-inf). */
+#define SCION_W_SENTINEL INT32_MIN
+typedef struct scion_wnode {
+  float lo[8][3], hi[8][3];
+  int32_t child[8]; /* >=0: interior index; <0 (and != SENTINEL): leaf id = ~child */
+} scion_wnode;
+
+typedef struct scion_wleaf {
+  uint32_t first_prim, nprims;
+} scion_wleaf;
+
+typedef struct scion_scene scion_scene; /* triangle soup                          */
+typedef struct scion_ltree scion_ltree; /* LogicalTree (binary, optional 8-wide)  */
+typedef struct scion_ptree scion_ptree; /* PhysicalTree on the host */
+typedef struct scion_dtree scion_dtree; /* PhysicalTree resident on one device    */
+
+const char* scion_last_error(void);
+int scion_abi_version(void);
+
+/* ------------------------------------------------------------------------- */
+/* Layout registry — replaces corpus_layouts()/find_corpus_layout(),          */
+/* /root/reference/proj/src/corpus.cpp:9-34, and plan_layout()/footprint(),   */
+/* /root/reference/proj/include/layoutc/plan.hpp:94, :110                     */
+/* ------------------------------------------------------------------------- */
+typedef struct scion_layout_info {
+  const char* name;        /* CLI-facing name, same strings as corpus.cpp:11-25 */
+  int family;              /* SCION_FAMILY_*                                    */
+  int arity;               /* 2 or 8                                            */
+  uint32_t node_stride;    /* node bytes = sum of segment strides (plan.cpp:327) */
+  uint32_t node_align;
+  uint32_t n_segments;
+  uint32_t ref_bits;       /* width of the primary reference component          */
+  uint32_t max_leaf;       /* capacity of the nprims field                      */
+  int has_cpq;             /* closest_point available (binary families only, corpus.cpp:83) */
+} scion_layout_info;
+
+int scion_layout_count(void);
+int scion_layout_info_at(int index, scion_layout_info* out);
+int scion_layout_find(const char* name, scion_layout_info* out);
+/* JSON dump of the MemoryPlan (buffers, segments, slots @bit offset:width), the
+ * counterpart of the `footprint` report. Caller frees with scion_free. */
+int scion_layout_plan_json(const char* name, char** out_json);
+/* emit_cuda: the CUDA sibling of emit_c — deterministic text. */
+int scion_layout_emit_cuda(const char* name, char** out_text);
+/* Compile a layout spec from source text (layout-language subset of the
+ * reference grammar, src/parser.cpp:790-955) and return plan JSON / CUDA text. */
+int scion_compile_layout_text(const char* scion_source, char** out_plan_json, char** out_cuda);
+void scion_free(void* p);
+
+/* ------------------------------------------------------------------------- */
+/* Scene tools — stand in for src/scene.cpp, src/logical.cpp */
+/* ------------------------------------------------------------------------- */
+int scion_scene_terrain(uint32_t grid, uint64_t seed, scion_scene** out);  /* 2*grid^2 triangles */
+int scion_scene_sphere(uint32_t grid, uint64_t seed, scion_scene** out);   /* 2*grid^2 triangles */
+int scion_scene_cloud(uint64_t npoints, uint64_t seed, scion_scene** out); /* degenerate triangles p0=p1=p2 */
+int scion_scene_from_triangles(const float* xyz9, uint64_t ntris, scion_scene** out);
+uint64_t scion_scene_ntris(const scion_scene* s);
+const float* scion_scene_triangles(const scion_scene* s); /* 9 floats per triangle */
+void scion_scene_bounds(const scion_scene* s, float lo[3], float hi[3]);
+void scion_scene_free(scion_scene* s);
+
+/* build_sah: binned SAH, `bins` bins, C_trav = C_isect = 1, ties ->
+ * lowest axis then lowest bin, coincident centroids -> index halves. Depth is capped at
+ * max_depth (<= 64) by switching to median splits.  build_median: SPEC.md:556-561. */
+int scion_build_sah(const scion_scene* s, uint32_t bins, uint32_t max_leaf, uint32_t max_depth,
+                    scion_ltree** out);
+int scion_build_median(const scion_scene* s, uint32_t max_leaf, scion_ltree** out);
+/* collapse_to_wide; idempotent, result cached inside the ltree. */
+int scion_ltree_collapse8(scion_ltree* t);
+
+uint64_t scion_ltree_nnodes(const scion_ltree* t);
+const scion_lnode* scion_ltree_nodes(const scion_ltree* t);
+uint64_t scion_ltree_nprims(const scion_ltree* t);
+const float* scion_ltree_triangles(const scion_ltree* t);     /* tree order, 9 floats each */
+const uint32_t* scion_ltree_prim_ids(const scion_ltree* t);   /* tree order -> scene index */
+const float* scion_ltree_dop_lo2(const scion_ltree* t);       /* 4 floats per node (DOP-14 diagonals) */
+const float* scion_ltree_dop_hi2(const scion_ltree* t);
+uint32_t scion_ltree_depth(const scion_ltree* t);
+uint64_t scion_ltree_nwnodes(const scion_ltree* t);
+const scion_wnode* scion_ltree_wnodes(const scion_ltree* t);
+uint64_t scion_ltree_nwleaves(const scion_ltree* t);
+const scion_wleaf* scion_ltree_wleaves(const scion_ltree* t);
+int32_t scion_ltree_wroot(const scion_ltree* t); /* child-style code of the 8-wide root */
+void scion_ltree_free(scion_ltree* t);
+
+/* ------------------------------------------------------------------------- */
+/* build_physical: LogicalTree -> byte buffers + globals + root ref */
+/* ------------------------------------------------------------------------- */
+int scion_encode(const scion_ltree* t, const char* layout, scion_ptree** out);
+const char* scion_ptree_layout(const scion_ptree* p);
+int scion_ptree_nbuffers(const scion_ptree* p);
+int scion_ptree_buffer(const scion_ptree* p, int i, const char** name, const uint8_t** data,
+                       uint64_t* bytes, uint64_t* count);
+/* segment base byte offsets of buffer i (plan.cpp:333-347); returns the count written */
+int scion_ptree_segment_bases(const scion_ptree* p, int i, uint64_t* bases, int max);
+int scion_ptree_nglobals(const scion_ptree* p);
+/* global slot: name + raw little-endian bits (up to 16 bytes: f32x3 / f32x4 / u64) */
+int scion_ptree_global(const scion_ptree* p, int i, const char** name, uint8_t raw[16], uint32_t* nbytes);
+/* root reference: component 0 as u64, tree-carried components as raw floats */
+int scion_ptree_root(const scion_ptree* p, uint64_t* ref0, float* carried6);
+uint64_t scion_ptree_total_bytes(const scion_ptree* p); /* footprint().total_bytes */
+uint64_t scion_ptree_node_bytes(const scion_ptree* p);  /* all buffers except primitives */
+/* fault injection for verify tests: xor one byte of a buffer */
+int scion_ptree_corrupt(scion_ptree* p, int buffer, uint64_t byte_offset, uint8_t xor_mask);
+void scion_ptree_free(scion_ptree* p);
+
+/* ------------------------------------------------------------------------- */
+/* Device residency                                                           */
+/* ------------------------------------------------------------------------- */
+int scion_device_count(int* out);
+/* host -> device copy of every buffer (the library owns the device memory) */
+int scion_dtree_upload(const scion_ptree* p, int device, scion_dtree** out);
+/* allocate an empty device tree with p's shapes (for receiving a broadcast) */
+int scion_dtree_alloc_like(const scion_ptree* p, int device, scion_dtree** out);
+/* Packed wire image used for replication: [header | globals | buffers...] in ONE
+ * contiguous device allocation so that a single ncclBroadcast replicates the tree. */
+int scion_dtree_image(const scion_dtree* t, void** d_ptr, uint64_t* bytes);
+/* rebuild a device tree around a received image (no copy; image owned by caller unless adopt=1) */
+int scion_dtree_from_image(const char* layout, void* d_image, uint64_t bytes, int device, int adopt,
+                           scion_dtree** out);
+void scion_dtree_free(scion_dtree* t);
+
+/* ------------------------------------------------------------------------- */
+/* Queries — stand in for interpret(program, tree, "closest_hit"|"closest_point", args)
+ * specialised per layout at build time by emit_cuda.        */
+/* ------------------------------------------------------------------------- */
+/* variant: 0 = default (tuned) kernel; other values select documented experimental
+ * kernel variants that must produce identical results. */
+int scion_closest_hit(const scion_dtree* t, const scion_ray* d_rays, uint64_t n, scion_hit* d_hits,
+                      uint32_t* d_status /* nullable */, scion_counters* d_counters /* nullable */,
+                      int variant, void* stream);
+int scion_closest_point(const scion_dtree* t, const float* d_points_xyz, uint64_t n, scion_cp* d_out,
+                        uint32_t* d_status, scion_counters* d_counters, int variant, void* stream);
+/* Host-buffer entry points (the reference-facing call: host in, host out). H2D copy,
+ * kernel, D2H copy, stream sync; chunked + double-buffered over two streams. */
+int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64_t n, scion_hit* h_hits,
+                           uint32_t* h_status /* nullable */);
+int scion_closest_point_host(const scion_dtree* t, const float* h_points_xyz, uint64_t n, scion_cp* h_out,
+                             uint32_t* h_status);
+
+/* ------------------------------------------------------------------------- */
+/* Query generators (src/rng.cpp placeholder): every query is
+ * a pure function of (seed, global index) so any rank count sees identical inputs. */
+/* ------------------------------------------------------------------------- */
+typedef struct scion_camera {
+  float eye[3];
+  float target[3];
+  float up[3];
+  float fov_y_deg;
+  uint32_t width, height;
+} scion_camera;
+/* default pinhole camera looking at the bounds (outside the +z face; +y for terrains) */
+void scion_camera_default(const float lo[3], const float hi[3], int look_down_y, uint32_t w, uint32_t h,
+                          scion_camera* out);
+int scion_gen_primary(const scion_camera* cam, uint64_t first, uint64_t n, scion_ray* d_rays, void* stream);
+/* secondary: origin = uniform point on a hash-chosen triangle + eps*normal, direction =
+ * uniform hemisphere about the geometric normal */
+int scion_gen_secondary(const scion_dtree* t, uint64_t seed, uint64_t first, uint64_t n, scion_ray* d_rays,
+                        void* stream);
+int scion_gen_points(const float lo[3], const float hi[3], uint64_t seed, uint64_t first, uint64_t n,
+                     float* d_points_xyz, void* stream);
+/* host twins of the generators (bit-identical results), used by CPU callers and tests */
+int scion_gen_primary_host(const scion_camera* cam, uint64_t first, uint64_t n, scion_ray* h_rays);
+int scion_gen_secondary_host(const float* tris9, uint64_t ntris, uint64_t seed, uint64_t first, uint64_t n,
+                             scion_ray* h_rays);
+int scion_gen_points_host(const float lo[3], const float hi[3], uint64_t seed, uint64_t first, uint64_t n,
+                          float* h_points_xyz);
+
+/* contiguous query partition for rank r of nranks: [first, first+count) */
+void scion_partition(uint64_t n, int rank, int nranks, uint64_t* first, uint64_t* count);
+
+/* number of product kernels launched by this process so far (bench `gpu_launches`) */
+uint64_t scion_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCION_B200_H */

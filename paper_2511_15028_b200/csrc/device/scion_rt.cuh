@@ -1,0 +1,386 @@
+// scion_rt.cuh — the runtime the emitted layout headers (gen/*.cuh) are written against.
+//
+// It provides the DSL's value types (f32x3, u16x3, records are emitted), the intrinsic table
+// of the reference (/root/reference/proj/include/layoutc/sema.hpp:16-34: dot cross select min
+// max floorf ceilf abs sum all fmul_rd fadd_rd fsub_rd fsub_ru fdiv_rd frcp_rd), `as` / `to`
+// casts (src/sema.cpp:753-786), bit ranges x[a:b], and the record loaders that turn a planned
+// element (stride, alignment) into the widest legal read-only vector loads.
+//
+// Dual mode: under nvcc everything is __device__ code for sm_100a (the product path).  Under a
+// plain host compiler the same text compiles with host twins of the intrinsics so that the
+// *generated decoders* can be unit-tested on a machine without a GPU (tests only; nothing in the
+// product calls the host mode).
+#pragma once
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__CUDACC__)
+#define SCION_DEV __device__ __forceinline__
+#define SCION_HOSTDEV __host__ __device__ __forceinline__
+#else
+#include <cfenv>
+#include <cmath>
+#define SCION_DEV inline
+#define SCION_HOSTDEV inline
+#endif
+
+namespace scion {
+
+// --------------------------------------------------------------------------- device tree view
+// Generic, layout-agnostic view of a PhysicalTree resident on the device: buffer base pointers
+// in plan order, segment base offsets (plan.cpp:333-347), element counts, and the global slots
+// as raw 16-byte cells.  Passed by value as a kernel parameter (constant bank).
+#define SCION_MAX_BUFFERS 6
+#define SCION_MAX_SEGMENTS 4
+#define SCION_MAX_GLOBALS 12
+struct TreeView {
+  const uint8_t* buf[SCION_MAX_BUFFERS];
+  uint64_t seg_base[SCION_MAX_BUFFERS][SCION_MAX_SEGMENTS];
+  uint64_t count[SCION_MAX_BUFFERS];
+  uint32_t glob[SCION_MAX_GLOBALS][4];
+  uint64_t root0;      // root reference, primary component
+  float root_carried[6];  // tree-carried components of the root reference (shared-slab)
+};
+
+// --------------------------------------------------------------------------- vectors
+template <class T, int N>
+struct vec {
+  T v[N];
+  SCION_HOSTDEV T& operator[](int i) { return v[i]; }
+  SCION_HOSTDEV const T& operator[](int i) const { return v[i]; }
+};
+template <class T>
+struct vec<T, 2> {
+  T x, y;
+  SCION_HOSTDEV T& operator[](int i) { return i == 0 ? x : y; }
+  SCION_HOSTDEV const T& operator[](int i) const { return i == 0 ? x : y; }
+};
+template <class T>
+struct vec<T, 3> {
+  T x, y, z;
+  SCION_HOSTDEV T& operator[](int i) { return i == 0 ? x : (i == 1 ? y : z); }
+  SCION_HOSTDEV const T& operator[](int i) const { return i == 0 ? x : (i == 1 ? y : z); }
+};
+template <class T>
+struct vec<T, 4> {
+  T x, y, z, w;
+  SCION_HOSTDEV T& operator[](int i) { return i == 0 ? x : (i == 1 ? y : (i == 2 ? z : w)); }
+  SCION_HOSTDEV const T& operator[](int i) const { return i == 0 ? x : (i == 1 ? y : (i == 2 ? z : w)); }
+};
+using f32x3 = vec<float, 3>;
+using f32x4 = vec<float, 4>;
+
+template <class T> struct is_vec { static constexpr bool value = false; };
+template <class T, int N> struct is_vec<vec<T, N>> { static constexpr bool value = true; };
+
+#define SCION_VEC_BINOP(OP)                                                                                  \
+  template <class T, int N> SCION_HOSTDEV vec<T, N> operator OP(const vec<T, N>& a, const vec<T, N>& b) {     \
+    vec<T, N> r;                                                                                             \
+    _Pragma("unroll") for (int i = 0; i < N; i++) r[i] = a[i] OP b[i];                                        \
+    return r;                                                                                                \
+  }                                                                                                          \
+  template <class T, int N, class S> SCION_HOSTDEV vec<T, N> operator OP(const vec<T, N>& a, S b) {           \
+    vec<T, N> r;                                                                                             \
+    _Pragma("unroll") for (int i = 0; i < N; i++) r[i] = a[i] OP (T)b;                                        \
+    return r;                                                                                                \
+  }                                                                                                          \
+  template <class T, int N, class S> SCION_HOSTDEV vec<T, N> operator OP(S a, const vec<T, N>& b) {           \
+    vec<T, N> r;                                                                                             \
+    _Pragma("unroll") for (int i = 0; i < N; i++) r[i] = (T)a OP b[i];                                        \
+    return r;                                                                                                \
+  }
+SCION_VEC_BINOP(+)
+SCION_VEC_BINOP(-)
+SCION_VEC_BINOP(*)
+SCION_VEC_BINOP(/)
+SCION_VEC_BINOP(&)
+SCION_VEC_BINOP(|)
+SCION_VEC_BINOP(^)
+#undef SCION_VEC_BINOP
+
+struct Slice {  // T[a : b] over a global array: element indices [begin, end)
+  uint64_t begin, end;
+};
+SCION_HOSTDEV Slice make_slice(uint64_t a, uint64_t b) { return Slice{a, b}; }
+
+// --------------------------------------------------------------------------- scalar intrinsics
+SCION_HOSTDEV float inf() { return __builtin_inff(); }
+SCION_HOSTDEV uint32_t f2u(float f) {
+#if defined(__CUDA_ARCH__)
+  return __float_as_uint(f);
+#else
+  uint32_t u; memcpy(&u, &f, 4); return u;
+#endif
+}
+SCION_HOSTDEV float u2f(uint32_t u) {
+#if defined(__CUDA_ARCH__)
+  return __uint_as_float(u);
+#else
+  float f; memcpy(&f, &u, 4); return f;
+#endif
+}
+
+// min/max: IEEE minNum/maxNum == C fminf/fmaxf == CUDA fminf/fmaxf
+SCION_HOSTDEV float min(float a, float b) { return fminf(a, b); }
+SCION_HOSTDEV float max(float a, float b) { return fmaxf(a, b); }
+SCION_HOSTDEV uint32_t min(uint32_t a, uint32_t b) { return a < b ? a : b; }
+SCION_HOSTDEV uint32_t max(uint32_t a, uint32_t b) { return a > b ? a : b; }
+SCION_HOSTDEV float floorf_(float a) { return ::floorf(a); }
+SCION_HOSTDEV float ceilf_(float a) { return ::ceilf(a); }
+SCION_HOSTDEV float abs(float a) { return u2f(f2u(a) & 0x7fffffffu); }
+template <class T> SCION_HOSTDEV T select(bool m, T a, T b) { return m ? a : b; }
+
+#define SCION_VEC_FN2(NAME)                                                                          \
+  template <class T, int N> SCION_HOSTDEV vec<T, N> NAME(const vec<T, N>& a, const vec<T, N>& b) {    \
+    vec<T, N> r;                                                                                     \
+    _Pragma("unroll") for (int i = 0; i < N; i++) r[i] = NAME(a[i], b[i]);                            \
+    return r;                                                                                        \
+  }                                                                                                  \
+  template <class T, int N> SCION_HOSTDEV vec<T, N> NAME(const vec<T, N>& a, T b) {                   \
+    vec<T, N> r;                                                                                     \
+    _Pragma("unroll") for (int i = 0; i < N; i++) r[i] = NAME(a[i], b);                               \
+    return r;                                                                                        \
+  }                                                                                                  \
+  template <class T, int N> SCION_HOSTDEV vec<T, N> NAME(T a, const vec<T, N>& b) {                   \
+    vec<T, N> r;                                                                                     \
+    _Pragma("unroll") for (int i = 0; i < N; i++) r[i] = NAME(a, b[i]);                               \
+    return r;                                                                                        \
+  }
+SCION_VEC_FN2(min)
+SCION_VEC_FN2(max)
+#undef SCION_VEC_FN2
+template <int N> SCION_HOSTDEV vec<float, N> floorf_(const vec<float, N>& a) {
+  vec<float, N> r;
+#pragma unroll
+  for (int i = 0; i < N; i++) r[i] = floorf_(a[i]);
+  return r;
+}
+template <int N> SCION_HOSTDEV vec<float, N> ceilf_(const vec<float, N>& a) {
+  vec<float, N> r;
+#pragma unroll
+  for (int i = 0; i < N; i++) r[i] = ceilf_(a[i]);
+  return r;
+}
+SCION_HOSTDEV float dot(const f32x3& a, const f32x3& b) { return ((a.x * b.x) + (a.y * b.y)) + (a.z * b.z); }
+SCION_HOSTDEV f32x3 cross(const f32x3& a, const f32x3& b) {
+  return f32x3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+SCION_HOSTDEV float sum(const f32x3& a) { return (a.x + a.y) + a.z; }
+
+// directed rounding (geometry-runtime): TRUE directed rounding, not the
+// binary64 shortcut.
+#if defined(__CUDA_ARCH__)
+SCION_DEV float fmul_rd(float a, float b) { return __fmul_rd(a, b); }
+SCION_DEV float fadd_rd(float a, float b) { return __fadd_rd(a, b); }
+SCION_DEV float fsub_rd(float a, float b) { return __fsub_rd(a, b); }
+SCION_DEV float fsub_ru(float a, float b) { return __fsub_ru(a, b); }
+SCION_DEV float fdiv_rd(float a, float b) { return __fdiv_rd(a, b); }
+SCION_DEV float frcp_rd(float a) { return __frcp_rd(a); }
+#elif !defined(__CUDACC__)
+namespace host_rounding {
+template <class F> inline float with_mode(int mode, F f) {
+  int old = fegetround();
+  fesetround(mode);
+  volatile float r = f();
+  fesetround(old);
+  return r;
+}
+}  // namespace host_rounding
+inline float fmul_rd(float a, float b) { volatile float x = a, y = b; return host_rounding::with_mode(FE_DOWNWARD, [&] { return x * y; }); }
+inline float fadd_rd(float a, float b) { volatile float x = a, y = b; return host_rounding::with_mode(FE_DOWNWARD, [&] { return x + y; }); }
+inline float fsub_rd(float a, float b) { volatile float x = a, y = b; return host_rounding::with_mode(FE_DOWNWARD, [&] { return x - y; }); }
+inline float fsub_ru(float a, float b) { volatile float x = a, y = b; return host_rounding::with_mode(FE_UPWARD, [&] { return x - y; }); }
+inline float fdiv_rd(float a, float b) { volatile float x = a, y = b; return host_rounding::with_mode(FE_DOWNWARD, [&] { return x / y; }); }
+inline float frcp_rd(float a) { volatile float x = a; return host_rounding::with_mode(FE_DOWNWARD, [&] { return 1.0f / x; }); }
+#else
+// host pass of nvcc over device-only code: never called
+__host__ __device__ inline float fmul_rd(float a, float b) { return a * b; }
+__host__ __device__ inline float fadd_rd(float a, float b) { return a + b; }
+__host__ __device__ inline float fsub_rd(float a, float b) { return a - b; }
+__host__ __device__ inline float fsub_ru(float a, float b) { return a - b; }
+__host__ __device__ inline float fdiv_rd(float a, float b) { return a / b; }
+__host__ __device__ inline float frcp_rd(float a) { return 1.0f / a; }
+#endif
+#define SCION_VEC_RD2(NAME)                                                                      \
+  template <int N> SCION_HOSTDEV vec<float, N> NAME(const vec<float, N>& a, const vec<float, N>& b) { \
+    vec<float, N> r;                                                                             \
+    _Pragma("unroll") for (int i = 0; i < N; i++) r[i] = NAME(a[i], b[i]);                        \
+    return r;                                                                                    \
+  }
+SCION_VEC_RD2(fmul_rd)
+SCION_VEC_RD2(fadd_rd)
+SCION_VEC_RD2(fsub_rd)
+SCION_VEC_RD2(fsub_ru)
+SCION_VEC_RD2(fdiv_rd)
+#undef SCION_VEC_RD2
+
+// --------------------------------------------------------------------------- casts
+// `e as T` value cast (sema.cpp:753-770); `e to T` equal-width bit cast (:771-786)
+template <class To> struct as_impl;
+template <> struct as_impl<float> {
+  SCION_HOSTDEV static float go(uint32_t x) { return (float)x; }
+  SCION_HOSTDEV static float go(int32_t x) { return (float)x; }
+  SCION_HOSTDEV static float go(uint64_t x) { return (float)x; }
+  SCION_HOSTDEV static float go(float x) { return x; }
+};
+template <int N> struct as_impl<vec<float, N>> {
+  template <class S> SCION_HOSTDEV static vec<float, N> go(const vec<S, N>& x) {
+    vec<float, N> r;
+#pragma unroll
+    for (int i = 0; i < N; i++) r[i] = as_impl<float>::go(x[i]);
+    return r;
+  }
+};
+template <class To, class From> SCION_HOSTDEV To as_(const From& x) { return as_impl<To>::go(x); }
+
+SCION_HOSTDEV uint64_t mask64(int w) { return w >= 64 ? ~0ull : ((1ull << w) - 1ull); }
+// unsigned integer target of width W (float source truncates toward zero; inputs are
+// pre-floored and clamped by the DSL code)
+template <int W> SCION_HOSTDEV uint32_t as_uint(float x) { return (uint32_t)x & (uint32_t)mask64(W); }
+template <int W> SCION_HOSTDEV uint32_t as_uint(uint32_t x) { return x & (uint32_t)mask64(W); }
+template <int W> SCION_HOSTDEV uint32_t as_uint(int32_t x) { return (uint32_t)x & (uint32_t)mask64(W); }
+template <int W> SCION_HOSTDEV uint32_t as_uint(uint64_t x) { return (uint32_t)(x & mask64(W)); }
+template <int W> SCION_HOSTDEV uint64_t as_uint64(uint64_t x) { return x & mask64(W); }
+template <int W> SCION_HOSTDEV uint64_t as_uint64(uint32_t x) { return (uint64_t)x & mask64(W); }
+template <int W, class S, int N> SCION_HOSTDEV vec<uint32_t, N> as_uint(const vec<S, N>& x) {
+  vec<uint32_t, N> r;
+#pragma unroll
+  for (int i = 0; i < N; i++) r[i] = as_uint<W>(x[i]);
+  return r;
+}
+template <int W> SCION_HOSTDEV int32_t as_sint(uint32_t x) {
+  return W >= 32 ? (int32_t)x : (int32_t)(x << (32 - W)) >> (32 - W);
+}
+template <int W> SCION_HOSTDEV int32_t as_sint(int32_t x) { return as_sint<W>((uint32_t)x); }
+
+SCION_HOSTDEV float bit_to_f32(uint32_t x) { return u2f(x); }
+SCION_HOSTDEV uint32_t bit_to_u32(float x) { return f2u(x); }
+SCION_HOSTDEV uint32_t bit_to_u32(int32_t x) { return (uint32_t)x; }
+SCION_HOSTDEV uint32_t bit_to_u32(uint32_t x) { return x; }
+SCION_HOSTDEV int32_t bit_to_i32(uint32_t x) { return (int32_t)x; }
+SCION_HOSTDEV int32_t bit_to_i32(int32_t x) { return x; }
+
+// x[a:b] — inclusive bit range (bvh8_q8_ci.scion: I[2:31], I[7:31], I[2:6])
+template <int LO, int HI> SCION_HOSTDEV uint32_t bits(uint32_t x) { return (x >> LO) & (uint32_t)mask64(HI - LO + 1); }
+template <int LO, int HI> SCION_HOSTDEV uint32_t bits(int32_t x) { return bits<LO, HI>((uint32_t)x); }
+template <int LO, int HI> SCION_HOSTDEV uint64_t bits(uint64_t x) { return (x >> LO) & mask64(HI - LO + 1); }
+
+// dynamic lane update: `t[axis] = S` (shared_slab.scion upd)
+template <class T, int N, class I> SCION_HOSTDEV void set_lane(vec<T, N>& v, I lane, T s) {
+#pragma unroll
+  for (int i = 0; i < N; i++)
+    if ((int)lane == i) v[i] = s;
+}
+template <class T, int N, class I> SCION_HOSTDEV T get_lane(const vec<T, N>& v, I lane) {
+  T r = v[0];
+#pragma unroll
+  for (int i = 1; i < N; i++)
+    if ((int)lane == i) r = v[i];
+  return r;
+}
+
+// --------------------------------------------------------------------------- record loads
+template <int NW>
+struct Words {
+  uint32_t w[NW];
+};
+
+SCION_HOSTDEV uint32_t ld32(const uint8_t* p) {
+#if defined(__CUDA_ARCH__)
+  return __ldg(reinterpret_cast<const uint32_t*>(p));
+#else
+  uint32_t v; memcpy(&v, p, 4); return v;
+#endif
+}
+SCION_HOSTDEV void ld64(const uint8_t* p, uint32_t* o) {
+#if defined(__CUDA_ARCH__)
+  uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  o[0] = v.x; o[1] = v.y;
+#else
+  memcpy(o, p, 8);
+#endif
+}
+SCION_HOSTDEV void ld128(const uint8_t* p, uint32_t* o) {
+#if defined(__CUDA_ARCH__)
+  uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+#else
+  memcpy(o, p, 16);
+#endif
+}
+SCION_HOSTDEV uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t shift_bits) {
+#if defined(__CUDA_ARCH__)
+  return __funnelshift_r(lo, hi, shift_bits);
+#else
+  return shift_bits == 0 ? lo : (lo >> shift_bits) | (hi << (32 - shift_bits));
+#endif
+}
+
+// Load one planned element of BYTES bytes whose address is known to be ALIGN-aligned
+// (ALIGN = gcd of the buffer base alignment, the segment base and the stride, computed by
+// emit_cuda).  16-byte read-only vector loads whenever the plan allows them; 8- and 4-byte
+// loads otherwise; byte-granular strides (pbrt-post 34 B, identity 41 B, shared-slab 29 B) read
+// the covering aligned words and funnel-shift.  Every device buffer is over-allocated by 16
+// bytes so the covering reads stay inside the allocation.
+template <int BYTES, int ALIGN>
+SCION_HOSTDEV void load_record(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
+  constexpr int NW = (BYTES + 3) / 4;
+  if constexpr (ALIGN % 16 == 0 && BYTES % 16 == 0) {
+#pragma unroll
+    for (int i = 0; i < NW; i += 4) ld128(p + 4 * i, r.w + i);
+  } else if constexpr (ALIGN % 8 == 0 && BYTES % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < NW; i += 2) ld64(p + 4 * i, r.w + i);
+  } else if constexpr (ALIGN % 4 == 0 && BYTES % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < NW; i++) r.w[i] = ld32(p + 4 * i);
+  } else {
+    const uint64_t a = (uint64_t)p;
+    const uint8_t* q = (const uint8_t*)(a & ~3ull);
+    const uint32_t sh = (uint32_t)(a & 3ull) * 8u;
+    uint32_t raw[NW + 1];
+#pragma unroll
+    for (int i = 0; i <= NW; i++) raw[i] = ld32(q + 4 * i);
+#pragma unroll
+    for (int i = 0; i < NW; i++) r.w[i] = funnel_r(raw[i], raw[i + 1], sh);
+  }
+}
+
+// constant-offset field extraction: the inverse of write_bits_raw
+// (/root/reference/proj/src/bits.cpp:21-36), little-endian, LSB first
+template <int OFF, int W, int NW>
+SCION_HOSTDEV uint32_t ext32(const Words<NW>& r) {
+  static_assert(W >= 1 && W <= 32, "ext32 width");
+  constexpr int i = OFF / 32, s = OFF % 32;
+  static_assert(i < NW, "field outside record");
+  if constexpr (s + W <= 32) {
+    if constexpr (W == 32) return r.w[i];
+    else return (r.w[i] >> s) & (uint32_t)((1ull << W) - 1ull);
+  } else {
+    static_assert(i + 1 < NW, "field outside record");
+    return ((r.w[i] >> s) | (r.w[i + 1] << (32 - s))) & (uint32_t)((1ull << W) - 1ull);
+  }
+}
+template <int OFF, int W, int NW>
+SCION_HOSTDEV uint64_t ext64(const Words<NW>& r) {
+  static_assert(W > 32 && W <= 64, "ext64 width");
+  uint64_t lo = ext32<OFF, 32, NW>(r);
+  uint64_t hi = ext32<OFF + 32, W - 32, NW>(r);
+  return lo | (hi << 32);
+}
+template <int OFF, int NW>
+SCION_HOSTDEV float extf(const Words<NW>& r) {
+  return u2f(ext32<OFF, 32, NW>(r));
+}
+
+template <class T> SCION_HOSTDEV T glob(const TreeView& T_, int i);
+template <> SCION_HOSTDEV float glob<float>(const TreeView& t, int i) { return u2f(t.glob[i][0]); }
+template <> SCION_HOSTDEV uint32_t glob<uint32_t>(const TreeView& t, int i) { return t.glob[i][0]; }
+template <> SCION_HOSTDEV int32_t glob<int32_t>(const TreeView& t, int i) { return (int32_t)t.glob[i][0]; }
+template <> SCION_HOSTDEV uint64_t glob<uint64_t>(const TreeView& t, int i) { return (uint64_t)t.glob[i][0] | ((uint64_t)t.glob[i][1] << 32); }
+template <> SCION_HOSTDEV f32x3 glob<f32x3>(const TreeView& t, int i) { return f32x3{u2f(t.glob[i][0]), u2f(t.glob[i][1]), u2f(t.glob[i][2])}; }
+template <> SCION_HOSTDEV f32x4 glob<f32x4>(const TreeView& t, int i) {
+  return f32x4{u2f(t.glob[i][0]), u2f(t.glob[i][1]), u2f(t.glob[i][2]), u2f(t.glob[i][3])};
+}
+
+}  // namespace scion

@@ -1,0 +1,619 @@
+// emit_cuda — CUDA codegen backend of the layout compiler.
+//
+// Fills, for CUDA, the slot the reference reserves for emit_c ("packed record
+// declarations matching MemoryPlan strides bit-for-bit ... a static assertion on node size ...
+// deterministic output (golden-testable)").  Per layout it emits one header with
+//   * the device node record(s) (one per segment) + static_asserts against the planned stride,
+//   * slot offset/width constants,
+//   * the record types and helper `func`s the layout's derive expressions reach,
+//   * `decode()` — reference + tree view -> ADT view (variant, bounds, children | prim range),
+//     i.e. destructor specialisation (Alg. 1 / src/specialize.cpp:20-122) resolved at compile
+//     time into constant-offset extractions, and `decode_cold()` for the fields that live
+//     behind a `---` separator.
+// The DSL is C-like; expressions translate 1:1 (as -> scion::as_*, to -> bit casts,
+// x[a:b] -> scion::bits<a,b>, fmul_rd -> __fmul_rd ...) and C++ overload resolution against
+// device/scion_rt.cuh does the typing.  The traversal kernels (device/traverse.cuh) are
+// templates over the emitted struct.
+#include <algorithm>
+#include <functional>
+#include <numeric>
+#include <sstream>
+
+#include "layoutc.hpp"
+
+namespace scion::lc {
+namespace {
+
+struct Emitter {
+  const Plan& plan;
+  const Program& prog;
+  std::ostringstream out;
+  std::string ref_ctype;
+  bool ref_is_struct = false;
+  std::set<std::string> global_names, array_names, ref_names;
+  std::set<std::string> used_funcs;  // reachable helper funcs
+  std::vector<std::string> func_order;
+
+  explicit Emitter(const Plan& p) : plan(p), prog(*p.program) {}
+
+  // ------------------------------------------------------------------ types
+  std::string ctype(const TypeP& t) const {
+    switch (t->kind) {
+      case Type::Int: return t->width <= 32 ? (t->is_signed ? "int32_t" : "uint32_t") : (t->is_signed ? "int64_t" : "uint64_t");
+      case Type::Float: return "float";
+      case Type::Bool: return "bool";
+      case Type::Ptr: return "uint64_t";
+      case Type::Vec: return "scion::vec<" + ctype(t->elem) + ", " + std::to_string(t->lanes) + ">";
+      case Type::Array:
+        if (!t->len_field.empty()) return "scion::Slice";
+        return "scion::vec<" + ctype(t->elem) + ", " + std::to_string(t->lanes) + ">";
+      case Type::Named: {
+        const TypeDecl* d = prog.find_type(t->name);
+        if (d && d->is_adt()) return "Ref";
+        return "rec_" + t->name;
+      }
+      case Type::Tuple: return "Ref";
+    }
+    return "void";
+  }
+
+  // ------------------------------------------------------------------ expressions
+  static bool is_intrinsic(const std::string& n) {
+    static const std::set<std::string> s = {"dot", "cross", "cross_", "select", "min", "max", "floorf", "ceilf", "abs", "sum", "all",
+                                            "fmul_rd", "fadd_rd", "fsub_rd", "fsub_ru", "fdiv_rd", "frcp_rd"};
+    return s.count(n) > 0;
+  }
+  std::string float_lit(const std::string& s) const {
+    std::string t = s;
+    if (t.find('.') == std::string::npos && t.find('e') == std::string::npos && t.find('E') == std::string::npos) t += ".0";
+    return t + "f";
+  }
+  // `in_layout`: identifiers may name reference components / globals
+  std::string ex(const ExprP& e, bool in_layout) {
+    switch (e->kind) {
+      case Expr::IntLit: {
+        std::string s = std::to_string(e->ival);
+        if (e->ival > 0x7fffffffull) return s + (e->ival > 0xffffffffull ? "ull" : "u");
+        return e->has_u ? s + "u" : s;
+      }
+      case Expr::FloatLit: return float_lit(e->text);
+      case Expr::Ident:
+        if (e->text == "inf") return "scion::inf()";
+        if (in_layout && ref_names.count(e->text)) return ref_is_struct ? "ref__." + e->text : "ref__";
+        return e->text;
+      case Expr::Binary: return "(" + ex(e->args[0], in_layout) + " " + e->text + " " + ex(e->args[1], in_layout) + ")";
+      case Expr::Unary: return "(" + e->text + ex(e->args[0], in_layout) + ")";
+      case Expr::Call: {
+        std::string fn;
+        if (is_intrinsic(e->text)) {
+          fn = e->text == "cross_" ? "cross" : e->text == "floorf" ? "floorf_" : e->text == "ceilf" ? "ceilf_" : e->text;
+          fn = "scion::" + fn;
+        } else {
+          fn = "fn_" + e->text;
+        }
+        std::string s = fn + "(";
+        for (size_t i = 0; i < e->args.size(); i++) s += (i ? ", " : "") + ex(e->args[i], in_layout);
+        return s + ")";
+      }
+      case Expr::Member:
+        if (in_layout && e->args[0]->kind == Expr::Ident && e->args[0]->text == "parent") return "ref__." + e->text;
+        return ex(e->args[0], in_layout) + "." + e->text;
+      case Expr::Index: {
+        // constant lane index -> operator[]; dynamic lane index -> scion::get_lane
+        if (e->args[1]->kind == Expr::IntLit) return ex(e->args[0], in_layout) + "[" + std::to_string(e->args[1]->ival) + "]";
+        return "scion::get_lane(" + ex(e->args[0], in_layout) + ", " + ex(e->args[1], in_layout) + ")";
+      }
+      case Expr::Range: {
+        const ExprP& base = e->args[0];
+        if (in_layout && base->kind == Expr::Ident && array_names.count(base->text))
+          return "scion::make_slice((uint64_t)(" + ex(e->args[1], in_layout) + "), (uint64_t)(" + ex(e->args[2], in_layout) + "))";
+        if (e->args[1]->kind != Expr::IntLit || e->args[2]->kind != Expr::IntLit) throw LayoutError("bit ranges need literal bounds");
+        return "scion::bits<" + std::to_string(e->args[1]->ival) + ", " + std::to_string(e->args[2]->ival) + ">(" + ex(base, in_layout) + ")";
+      }
+      case Expr::Cast: {
+        std::string a = ex(e->args[0], in_layout);
+        const TypeP& t = e->type;
+        const Type* leaf = t.get();
+        while (leaf->kind == Type::Vec) leaf = leaf->elem.get();
+        if (e->bitcast) {
+          if (t->kind == Type::Float) return "scion::bit_to_f32(" + a + ")";
+          if (t->kind == Type::Int && t->width == 32) return std::string(t->is_signed ? "scion::bit_to_i32(" : "scion::bit_to_u32(") + a + ")";
+          throw LayoutError("unsupported bit cast target " + t->str());
+        }
+        if (leaf->kind == Type::Float) return "scion::as_<" + ctype(t) + ">(" + a + ")";
+        if (leaf->kind == Type::Int) {
+          if (leaf->is_signed) return "scion::as_sint<" + std::to_string(leaf->width) + ">(" + a + ")";
+          if (leaf->width > 32) return "scion::as_uint64<" + std::to_string(leaf->width) + ">(" + a + ")";
+          return "scion::as_uint<" + std::to_string(leaf->width) + ">(" + a + ")";
+        }
+        if (leaf->kind == Type::Ptr) return "(uint64_t)(" + a + ")";
+        throw LayoutError("unsupported cast target " + t->str());
+      }
+      case Expr::Construct: case Expr::Brace: case Expr::Tuple: {
+        std::string s = e->kind == Expr::Construct ? ctype(e->type) : e->kind == Expr::Tuple ? std::string("Ref") : std::string();
+        s += "{";
+        for (size_t i = 0; i < e->args.size(); i++) s += (i ? ", " : "") + ex(e->args[i], in_layout);
+        return s + "}";
+      }
+    }
+    return "?";
+  }
+
+  void collect_calls(const ExprP& e, std::vector<std::string>& calls) const {
+    if (!e) return;
+    if (e->kind == Expr::Call && !is_intrinsic(e->text)) calls.push_back(e->text);
+    for (auto& a : e->args) collect_calls(a, calls);
+  }
+  void collect_calls(const std::vector<StmtP>& body, std::vector<std::string>& calls) const {
+    for (auto& s : body) {
+      collect_calls(s->value, calls);
+      collect_calls(s->lhs, calls);
+      collect_calls(s->cond, calls);
+      collect_calls(s->then_body, calls);
+      collect_calls(s->else_body, calls);
+    }
+  }
+  void collect_idents(const ExprP& e, std::set<std::string>& ids) const {
+    if (!e) return;
+    if (e->kind == Expr::Ident) ids.insert(e->text);
+    for (auto& a : e->args) collect_idents(a, ids);
+  }
+  const Func* find_func(const std::string& n) const {
+    for (auto& f : prog.funcs)
+      if (f.name == n) return &f;
+    return nullptr;
+  }
+  void reach(const std::string& fn) {
+    if (used_funcs.count(fn)) return;
+    const Func* f = find_func(fn);
+    if (!f) throw LayoutError("call to unknown function '" + fn + "'");
+    used_funcs.insert(fn);
+    std::vector<std::string> calls;
+    collect_calls(f->body, calls);
+    for (auto& c : calls) reach(c);
+    func_order.push_back(fn);  // callees first
+  }
+  void reach_members(const std::vector<MemberP>& ms) {
+    for (auto& m : ms) {
+      std::vector<std::string> calls;
+      collect_calls(m->value, calls);
+      collect_calls(m->size_expr, calls);
+      for (auto& c : calls) reach(c);
+      reach_members(m->members);
+      for (auto& a : m->arms) {
+        std::vector<std::string> k;
+        collect_calls(a.from_key, k);
+        for (auto& c : k) reach(c);
+        reach_members(a.members);
+      }
+    }
+  }
+
+  // ------------------------------------------------------------------ function bodies
+  void emit_stmts(const std::vector<StmtP>& body, int ind) {
+    std::string pad((size_t)ind * 2, ' ');
+    for (auto& s : body) {
+      switch (s->kind) {
+        case Stmt::Let:
+          out << pad << (s->is_mut ? "" : "const ") << ctype(s->type) << " " << s->name << " = " << ex(s->value, false) << ";\n";
+          break;
+        case Stmt::Assign:
+          if (s->lhs->kind == Expr::Index && s->lhs->args[1]->kind != Expr::IntLit)
+            out << pad << "scion::set_lane(" << ex(s->lhs->args[0], false) << ", " << ex(s->lhs->args[1], false) << ", " << ex(s->value, false) << ");\n";
+          else
+            out << pad << ex(s->lhs, false) << " = " << ex(s->value, false) << ";\n";
+          break;
+        case Stmt::If:
+          out << pad << "if (" << ex(s->cond, false) << ") {\n";
+          emit_stmts(s->then_body, ind + 1);
+          if (!s->else_body.empty()) {
+            out << pad << "} else {\n";
+            emit_stmts(s->else_body, ind + 1);
+          }
+          out << pad << "}\n";
+          break;
+        case Stmt::Return:
+          if (s->value && (s->value->kind == Expr::Brace)) out << pad << "return " << cur_ret << ex(s->value, false) << ";\n";
+          else out << pad << "return " << (s->value ? ex(s->value, false) : "") << ";\n";
+          break;
+        case Stmt::ExprS: out << pad << ex(s->value, false) << ";\n"; break;
+      }
+    }
+  }
+  std::string cur_ret;
+
+  // ------------------------------------------------------------------ field extraction
+  std::string extract(const TypeP& t, uint64_t off, const std::string& words) const {
+    auto o = std::to_string(off);
+    switch (t->kind) {
+      case Type::Float: return "scion::extf<" + o + ">(" + words + ")";
+      case Type::Bool: return "(scion::ext32<" + o + ", 1>(" + words + ") != 0u)";
+      case Type::Ptr: return "scion::ext64<" + o + ", 64>(" + words + ")";
+      case Type::Int: {
+        std::string w = std::to_string(t->width);
+        if (t->width > 32) return "scion::ext64<" + o + ", " + w + ">(" + words + ")";
+        std::string u = "scion::ext32<" + o + ", " + w + ">(" + words + ")";
+        return t->is_signed ? "scion::as_sint<" + w + ">(" + u + ")" : u;
+      }
+      case Type::Vec: case Type::Array: {
+        uint64_t ew = plan.type_bits(t->elem);
+        std::string s = ctype(t) + "{";
+        for (uint32_t i = 0; i < t->lanes; i++) s += (i ? ", " : "") + extract(t->elem, off + i * ew, words);
+        return s + "}";
+      }
+      case Type::Named: {
+        const TypeDecl* d = prog.find_type(t->name);
+        std::string s = ctype(t) + "{";
+        uint64_t o2 = off;
+        for (size_t i = 0; i < d->fields.size(); i++) {
+          s += (i ? ", " : "") + extract(d->fields[i].type, o2, words);
+          o2 += plan.type_bits(d->fields[i].type);
+        }
+        return s + "}";
+      }
+      case Type::Tuple: break;
+    }
+    throw LayoutError("cannot load a value of type " + t->str());
+  }
+
+  // ------------------------------------------------------------------ decode emission
+  struct GroupInfo {
+    const MemberNode* node = nullptr;
+    const Buffer* buf = nullptr;
+  };
+  std::map<std::string, GroupInfo> indirect_groups;
+  const MemberNode* primary = nullptr;
+  const Buffer* primary_buf = nullptr;
+
+  std::set<std::string> cold_names;  // stored fields behind `---` and everything depending on them
+  bool split_is_cold(const MemberNode& m) const {
+    std::set<std::string> ids;
+    collect_idents(m.value, ids);
+    for (auto& i : ids)
+      if (cold_names.count(i)) return true;
+    for (auto& a : m.arms)
+      for (auto& am : a.members)
+        if ((am->kind == MemberNode::Stored || am->kind == MemberNode::Derive || am->kind == MemberNode::Let) && cold_names.count(am->name)) return true;
+    return false;
+  }
+  void compute_cold(const std::vector<MemberP>& ms) {
+    // stored fields in segments >= 1
+    for (auto& s : plan.slots)
+      if (primary_buf && s.buffer == primary_buf->id && s.segment > 0) cold_names.insert(s.name);
+    bool changed = true;
+    std::function<void(const std::vector<MemberP>&)> pass = [&](const std::vector<MemberP>& v) {
+      for (auto& m : v) {
+        if ((m->kind == MemberNode::Derive || m->kind == MemberNode::Let) && !cold_names.count(m->name)) {
+          std::set<std::string> ids;
+          collect_idents(m->value, ids);
+          for (auto& i : ids)
+            if (cold_names.count(i)) { cold_names.insert(m->name); changed = true; break; }
+        }
+        if (m->kind == MemberNode::Split) {
+          bool cold = split_is_cold(*m);
+          for (auto& a : m->arms) {
+            if (cold)
+              for (auto& am : a.members)
+                if (!am->name.empty() && !cold_names.count(am->name)) { cold_names.insert(am->name); changed = true; }
+            pass(a.members);
+          }
+        }
+      }
+    };
+    while (changed) {
+      changed = false;
+      pass(ms);
+    }
+  }
+
+  int gcd_align(const Buffer& b, int segment) const {
+    uint64_t g = 256;  // cudaMalloc'd sub-allocations are 256-byte aligned
+    if (b.is_arena) return (int)std::gcd<uint64_t>(g, b.align);
+    for (int s = 0; s <= segment; s++) g = std::gcd<uint64_t>(g, b.segments[(size_t)s].stride_bytes);
+    if (segment > 0) g = std::gcd<uint64_t>(g, b.align > 1 ? b.align : g);
+    return (int)g;
+  }
+
+  // emits loads of every segment of `buf` that holds a wanted stored field
+  void emit_record_loads(const Buffer& buf, const std::string& index_expr, const std::string& tag, int ind, bool hot_only) {
+    std::string pad((size_t)ind * 2, ' ');
+    for (size_t s = 0; s < buf.segments.size(); s++) {
+      if (hot_only && s > 0) break;
+      uint64_t bytes = buf.segments[s].stride_bytes;
+      std::string w = "w_" + tag + std::to_string(s);
+      out << pad << "scion::Words<" << (bytes + 3) / 4 << "> " << w << ";\n";
+      out << pad << "scion::load_record<" << bytes << ", " << gcd_align(buf, (int)s) << ">(tree__.buf[" << buf.id << "] + ";
+      if (buf.is_arena) out << "(uint64_t)(" << index_expr << ")";
+      else out << "tree__.seg_base[" << buf.id << "][" << s << "] + (uint64_t)(" << index_expr << ") * " << bytes << "ull";
+      out << ", " << w << ");\n";
+    }
+  }
+
+  enum class Mode { All, Hot, Cold };
+
+  bool is_adt_field(const std::string& n, const Variant* v) const {
+    for (auto& f : plan.adt->fields)
+      if (f.name == n) return true;
+    if (v)
+      for (auto& f : v->fields)
+        if (f.name == n) return true;
+    return false;
+  }
+  const Variant* find_variant(const std::string& n) const {
+    for (auto& v : plan.adt->variants)
+      if (v.name == n) return &v;
+    return nullptr;
+  }
+  int variant_index(const std::string& n) const {
+    for (size_t i = 0; i < plan.adt->variants.size(); i++)
+      if (plan.adt->variants[i].name == n) return (int)i;
+    return -1;
+  }
+
+  // Emits one member list. `bound` accumulates the names visible so far (for ADT assignment);
+  // `assigned` the ADT fields already written at an outer level.
+  void emit_members(const std::vector<MemberP>& ms, const Buffer* buf, const std::string& tag, int ind, Mode mode,
+                    std::set<std::string> bound, std::set<std::string> assigned, const Variant* variant, bool arm_level) {
+    std::string pad((size_t)ind * 2, ' ');
+    auto wanted = [&](const std::string& name) {
+      bool cold = cold_names.count(name) > 0;
+      return mode == Mode::All || (mode == Mode::Hot && !cold) || mode == Mode::Cold;
+    };
+    auto assign_ok = [&](const std::string& name) {
+      bool cold = cold_names.count(name) > 0;
+      return mode == Mode::All || (mode == Mode::Hot && !cold) || (mode == Mode::Cold && cold);
+    };
+    // 1. stored fields of this level
+    for (auto& m : ms)
+      if (m->kind == MemberNode::Stored && wanted(m->name)) {
+        const Slot* s = nullptr;
+        for (auto& sl : plan.slots)
+          if (sl.member == m.get()) s = &sl;
+        if (!s) throw LayoutError("internal: unplanned field " + m->name);
+        if (mode == Mode::Hot && s->segment > 0) continue;
+        out << pad << "const " << ctype(m->type) << " " << m->name << " = " << extract(m->type, s->offset, "w_" + tag + std::to_string(s->segment)) << ";\n";
+        bound.insert(m->name);
+      }
+    // 2. lets / derives in dependency order
+    std::vector<const MemberNode*> pend;
+    for (auto& m : ms)
+      if ((m->kind == MemberNode::Let || m->kind == MemberNode::Derive) && wanted(m->name)) pend.push_back(m.get());
+    std::set<std::string> pend_names;
+    for (auto* m : pend) pend_names.insert(m->name);
+    while (!pend.empty()) {
+      bool progress = false;
+      for (size_t i = 0; i < pend.size(); i++) {
+        std::set<std::string> ids;
+        collect_idents(pend[i]->value, ids);
+        bool ready = true;
+        for (auto& id : ids)
+          if (pend_names.count(id) && id != pend[i]->name) ready = false;
+        if (!ready) continue;
+        const MemberNode* m = pend[i];
+        std::string ty = m->kind == MemberNode::Let ? ctype(m->type) : std::string("auto");
+        if (m->kind == MemberNode::Derive) {  // derives of ADT fields get the field's type
+          for (auto& f : plan.adt->fields)
+            if (f.name == m->name) ty = ctype(f.type);
+          if (variant)
+            for (auto& f : variant->fields)
+              if (f.name == m->name) ty = ctype(f.type);
+        }
+        out << pad << "const " << ty << " " << m->name << " = " << ex(m->value, true) << ";\n";
+        bound.insert(m->name);
+        pend_names.erase(m->name);
+        pend.erase(pend.begin() + (long)i);
+        progress = true;
+        break;
+      }
+      if (!progress) throw LayoutError("cyclic derives in layout " + plan.layout_name);
+    }
+    // 3. ADT fields resolvable at this level
+    auto assign_fields = [&](const std::vector<Param>& fs) {
+      for (auto& f : fs)
+        if (bound.count(f.name) && !assigned.count(f.name)) {
+          if (assign_ok(f.name)) out << pad << "node__." << f.name << " = " << f.name << ";\n";
+          assigned.insert(f.name);
+        }
+    };
+    assign_fields(plan.adt->fields);
+    if (arm_level && variant) {
+      assign_fields(variant->fields);
+      for (auto& f : variant->fields)
+        if (!assigned.count(f.name)) throw LayoutError("layout " + plan.layout_name + ": field '" + f.name + "' of variant " + variant->name + " is not defined");
+      for (auto& f : plan.adt->fields)
+        if (!assigned.count(f.name)) throw LayoutError("layout " + plan.layout_name + ": field '" + f.name + "' is not defined for variant " + variant->name);
+    }
+    // 4. splits
+    for (auto& m : ms) {
+      if (m->kind != MemberNode::Split) continue;
+      bool cold = split_is_cold(*m);
+      if ((mode == Mode::Hot && cold)) continue;
+      if (mode == Mode::Cold && !cold) continue;
+      out << pad << "const auto disc__ = " << ex(m->value, true) << ";\n";
+      for (size_t a = 0; a < m->arms.size(); a++) {
+        const Arm& arm = m->arms[a];
+        bool last = a + 1 == m->arms.size();
+        std::string test;
+        switch (arm.pat) {
+          case Arm::Literal: test = "disc__ == " + std::to_string(arm.value); break;
+          case Arm::Gt: test = "disc__ > " + std::to_string(arm.value); break;
+          case Arm::Lt: test = "disc__ < " + std::to_string(arm.value); break;
+          case Arm::Ge: test = "disc__ >= " + std::to_string(arm.value); break;
+          case Arm::Le: test = "disc__ <= " + std::to_string(arm.value); break;
+          case Arm::Wildcard: test = ""; break;
+        }
+        if (a == 0) out << pad << "if (" << test << ") {\n";
+        else if (last || test.empty()) out << pad << "} else {" << (test.empty() ? "" : "  // " + test) << "\n";
+        else out << pad << "} else if (" << test << ") {\n";
+        const Variant* v = find_variant(arm.variant);
+        if (!v) throw LayoutError("split arm names unknown variant " + arm.variant);
+        std::string pad2 = pad + "  ";
+        out << pad2 << "node__.variant = " << variant_index(arm.variant) << ";  // " << arm.variant << "\n";
+        if (arm.is_from) {
+          auto it = indirect_groups.find(arm.from_group);
+          if (it == indirect_groups.end()) throw LayoutError("unknown indirect group " + arm.from_group);
+          std::string t2 = ident_of(arm.from_group) + "_";
+          out << pad2 << "const uint64_t key__ = (uint64_t)(" << ex(arm.from_key, true) << ");\n";
+          emit_record_loads(*it->second.buf, "key__", t2, ind + 1, false);
+          emit_members(it->second.node->members, it->second.buf, t2, ind + 1, Mode::All, bound, assigned, v, true);
+        } else {
+          emit_members(arm.members, buf, tag, ind + 1, mode == Mode::Cold ? Mode::Cold : mode, bound, assigned, v, true);
+        }
+      }
+      out << pad << "}\n";
+    }
+  }
+
+  void find_groups(const std::vector<MemberP>& ms) {
+    for (auto& m : ms) {
+      if (m->kind != MemberNode::Group) continue;
+      const Buffer* b = nullptr;
+      std::string nm = m->group_name;
+      for (auto& bb : plan.buffers)
+        if (!bb.is_global_array && (bb.name == nm || (nm.empty() && bb.name == "group" + std::to_string(bb.id)))) b = &bb;
+      if (m->indirect) indirect_groups[m->group_name] = {m.get(), b};
+      else if (!m->index_binding.empty() && !primary) { primary = m.get(); primary_buf = b; }
+      find_groups(m->members);
+    }
+  }
+
+  std::string run() {
+    const std::string id = ident_of(plan.layout_name);
+    for (auto& r : plan.ref) ref_names.insert(r.name);
+    for (auto& g : plan.globals) global_names.insert(g.name);
+    for (auto& b : plan.buffers)
+      if (b.is_global_array) array_names.insert(b.name);
+    ref_is_struct = plan.ref.size() > 1;
+    find_groups(plan.layout->members);
+    if (!primary) throw LayoutError("layout has no direct group indexed by a reference component");
+    reach_members(plan.layout->members);
+    if (primary_buf && primary_buf->segments.size() > 1) compute_cold(primary->members);
+    bool has_cold = !cold_names.empty();
+
+    out << "// GENERATED by scionc emit-cuda from layouts/" << id << ".scion — do not edit.\n";
+    out << "// layout '" << plan.layout_name << "' : ADT " << plan.adt->name << ", family "
+        << (plan.family == Family::Bvh2 ? "bvh2" : plan.family == Family::Dop14 ? "dop14" : "bvh8") << ", node group '" << plan.node_group << "'\n";
+    out << "#pragma once\n#include \"../device/scion_rt.cuh\"\n\nnamespace scion_gen {\n\nstruct L_" << id << " {\n";
+    out << "  static constexpr const char* kName = \"" << plan.layout_name << "\";\n";
+    out << "  static constexpr int kFamily = " << (int)plan.family << ";\n";
+    out << "  static constexpr uint32_t kMaxLeaf = " << plan.max_leaf << "u;\n";
+    out << "  static constexpr bool kHasCold = " << (has_cold ? "true" : "false") << ";\n";
+    // buffers, records, slots
+    for (auto& b : plan.buffers) {
+      out << "  // buffer " << b.id << ": " << b.name << (b.is_arena ? " (arena, byte-offset references)" : b.is_global_array ? " (global array)" : "")
+          << ", count '" << b.count_name << "', align " << b.align << "\n";
+      out << "  static constexpr int kBuf_" << ident_of(b.name) << " = " << b.id << ";\n";
+      out << "  static constexpr uint32_t kStride_" << ident_of(b.name) << " = " << b.node_stride() << "u;\n";
+      for (size_t s = 0; s < b.segments.size(); s++) {
+        std::string rn = "Record_" + ident_of(b.name) + "_s" + std::to_string(s);
+        out << "  struct " << rn << " { uint8_t bytes[" << b.segments[s].stride_bytes << "]; };  // " << b.segments[s].stride_bits << " bits used\n";
+        out << "  static_assert(sizeof(" << rn << ") == " << b.segments[s].stride_bytes << ", \"node record must match the planned stride\");\n";
+      }
+    }
+    for (auto& s : plan.slots)
+      out << "  static constexpr uint32_t kOff_" << s.name << " = " << s.offset << "u, kWidth_" << s.name << " = " << s.width << "u, kSeg_" << s.name << " = " << s.segment << "u;  // "
+          << s.type->str() << " in buffer " << s.buffer << "\n";
+    for (size_t g = 0; g < plan.globals.size(); g++) out << "  static constexpr int kGlobal_" << plan.globals[g].name << " = " << g << ";  // " << plan.globals[g].type->str() << "\n";
+    // record types
+    for (auto& t : prog.types) {
+      if (t.is_adt() || t.name == "Triangle") continue;
+      out << "  struct rec_" << t.name << " {";
+      for (auto& f : t.fields) out << " " << ctype(f.type) << " " << f.name << ";";
+      out << " };\n";
+    }
+    // reference type
+    if (ref_is_struct) {
+      out << "  struct Ref {";
+      for (auto& r : plan.ref) out << " " << ctype(r.type) << " " << r.name << ";";
+      out << " };\n";
+    } else {
+      out << "  using Ref = " << ctype(plan.ref[0].type) << ";\n";
+    }
+    out << "  static constexpr uint32_t kRefBits = " << plan.type_bits(plan.ref[0].type) << "u;\n";
+    for (size_t v = 0; v < plan.adt->variants.size(); v++) out << "  static constexpr int k" << plan.adt->variants[v].name << " = " << v << ";\n";
+    // ADT view
+    out << "  struct Node {\n    int variant;\n";
+    std::set<std::string> seen;
+    auto node_field = [&](const Param& f) {
+      if (seen.count(f.name)) return;
+      seen.insert(f.name);
+      out << "    " << ctype(f.type) << " " << f.name << ";\n";
+    };
+    for (auto& f : plan.adt->fields) node_field(f);
+    for (auto& v : plan.adt->variants)
+      for (auto& f : v.fields) node_field(f);
+    out << "  };\n";
+    // root reference
+    out << "  SCION_HOSTDEV static Ref root(const scion::TreeView& tree__) {\n";
+    if (ref_is_struct) {
+      out << "    Ref r;\n    r." << plan.ref[0].name << " = (" << ctype(plan.ref[0].type) << ")tree__.root0;\n";
+      int k = 0;
+      for (size_t i = 1; i < plan.ref.size(); i++) {
+        const TypeP& t = plan.ref[i].type;
+        if (t->kind == Type::Vec && t->elem->kind == Type::Float) {
+          for (uint32_t l = 0; l < t->lanes; l++) out << "    r." << plan.ref[i].name << "[" << l << "] = tree__.root_carried[" << k++ << "];\n";
+        } else if (t->kind == Type::Float) {
+          out << "    r." << plan.ref[i].name << " = tree__.root_carried[" << k++ << "];\n";
+        } else {
+          throw LayoutError("unsupported tree-carried reference component type " + t->str());
+        }
+      }
+      out << "    return r;\n";
+    } else {
+      out << "    return (Ref)tree__.root0;\n";
+    }
+    out << "  }\n";
+    // helper funcs
+    for (auto& fn : func_order) {
+      const Func* f = find_func(fn);
+      cur_ret = f->ret ? ctype(f->ret) : "void";
+      out << "  SCION_HOSTDEV static " << cur_ret << " fn_" << f->name << "(";
+      for (size_t i = 0; i < f->params.size(); i++) out << (i ? ", " : "") << ctype(f->params[i].type) << " " << f->params[i].name;
+      out << ") {\n";
+      emit_stmts(f->body, 2);
+      out << "  }\n";
+    }
+    // decode
+    auto emit_decode = [&](const char* name, Mode mode) {
+      out << "  SCION_HOSTDEV static void " << name << "(const scion::TreeView& tree__, const Ref& ref__, Node& node__) {\n";
+      // globals referenced by layout expressions
+      std::set<std::string> ids;
+      std::function<void(const std::vector<MemberP>&)> scan = [&](const std::vector<MemberP>& ms) {
+        for (auto& m : ms) {
+          collect_idents(m->value, ids);
+          scan(m->members);
+          for (auto& a : m->arms) {
+            collect_idents(a.from_key, ids);
+            scan(a.members);
+          }
+        }
+      };
+      scan(plan.layout->members);
+      for (size_t g = 0; g < plan.globals.size(); g++)
+        if (ids.count(plan.globals[g].name) && !plan.globals[g].inferred)
+          out << "    const " << ctype(plan.globals[g].type) << " " << plan.globals[g].name << " = scion::glob<" << ctype(plan.globals[g].type) << ">(tree__, " << g << ");\n";
+      std::string index_expr = ref_is_struct ? "ref__." + primary->index_binding : std::string("ref__");
+      if (primary_buf && !primary_buf->segments.empty()) emit_record_loads(*primary_buf, index_expr, "", 2, mode == Mode::Hot);
+      emit_members(primary->members, primary_buf, "", 2, mode, {}, {}, nullptr, false);
+      out << "  }\n";
+    };
+    if (has_cold) {
+      emit_decode("decode", Mode::Hot);
+      emit_decode("decode_cold", Mode::Cold);
+    } else {
+      emit_decode("decode", Mode::All);
+      out << "  SCION_HOSTDEV static void decode_cold(const scion::TreeView&, const Ref&, Node&) {}\n";
+    }
+    out << "};\n\n}  // namespace scion_gen\n";
+    return out.str();
+  }
+};
+
+}  // namespace
+
+std::string emit_cuda(const Plan& plan) {
+  Emitter e(plan);
+  return e.run();
+}
+
+}  // namespace scion::lc
