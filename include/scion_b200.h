@@ -86,8 +86,10 @@ typedef struct scion_cp {
 } scion_cp;
 
 typedef struct scion_counters { /* interpreter cost counters */
-  uint32_t node_visits; /* node decodes (CPQ: incl. the two child peeks per interior) */
+  uint32_t node_visits; /* node decodes (CPQ: incl. the two child peeks per interior; 8-wide: interiors only) */
   uint32_t prim_tests;  /* triangle tests */
+  uint32_t cold_loads;  /* reads of segments behind `---` (dop14 diagonals, pbrt-soa topology) */
+  uint32_t max_stack;   /* peak occupancy of the 64-entry explicit stack */
 } scion_counters;
 
 /* ------------------------------------------------------------------------- */

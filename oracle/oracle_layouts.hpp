@@ -1,0 +1,273 @@
+// TEST INFRASTRUCTURE — CPU oracle, not part of the product.
+//
+// Per-layout node DECODE over the raw byte image, restating the `layout` block of every corpus
+// layout (/root/reference/proj/corpus/layouts/*.scion, cited per function).  Bit offsets and
+// strides are hard-coded from the REFERENCE planner's output for those files (plan_layout,
+// /root/reference/proj/src/plan.cpp:349; dumped by oracle/ref_probe.cpp into
+// tests/golden/ref_plans.json and asserted equal to this table by tests/test_oracle_layouts.py),
+// and every field is fetched with a naive bit-by-bit reader — the semantics of read_bits_raw
+// (/root/reference/proj/src/bits.cpp:7-19: little-endian, LSB first) without sharing its code
+// or the product's extraction templates.
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "oracle_geometry.hpp"
+
+namespace oracle {
+
+struct TreeBytes {          // mirror of the PhysicalTree handed over by the test harness
+  const char* layout;
+  int nbuf;
+  const uint8_t* buf[6];
+  uint64_t bytes[6];
+  uint64_t count[6];
+  uint64_t seg_base[6][4];
+  int nglob;
+  uint8_t glob[12][16];
+  uint64_t root0;
+  float carried[6];
+};
+
+inline uint64_t read_bits(const uint8_t* buf, uint64_t bit, uint32_t width) {
+  // byte-granular gather of exactly the bytes the field spans (never reads past the field)
+  const uint64_t first = bit >> 3, last = (bit + width - 1) >> 3;
+  const uint32_t sh = (uint32_t)(bit & 7);
+  unsigned __int128 acc = 0;
+  for (uint64_t b = first; b <= last; b++) acc |= (unsigned __int128)buf[b] << (8 * (b - first));
+  uint64_t v = (uint64_t)(acc >> sh);
+  return width >= 64 ? v : v & ((1ull << width) - 1ull);
+}
+inline uint64_t read_bits_naive(const uint8_t* buf, uint64_t bit, uint32_t width) {  // bit-array cross-check
+  uint64_t v = 0;
+  for (uint32_t i = 0; i < width; i++) {
+    uint64_t b = bit + i;
+    if ((buf[b >> 3] >> (b & 7)) & 1) v |= 1ull << i;
+  }
+  return v;
+}
+inline float read_f32(const uint8_t* buf, uint64_t bit) { return float_of((uint32_t)read_bits(buf, bit, 32)); }
+inline V3 read_v3(const uint8_t* buf, uint64_t bit) { return {read_f32(buf, bit), read_f32(buf, bit + 32), read_f32(buf, bit + 64)}; }
+inline V4 read_v4(const uint8_t* buf, uint64_t bit) { return {read_f32(buf, bit), read_f32(buf, bit + 32), read_f32(buf, bit + 64), read_f32(buf, bit + 96)}; }
+inline V3 glob_v3(const TreeBytes& t, int i) { V3 v; std::memcpy(&v, t.glob[i], 12); return v; }
+
+struct Ref {
+  uint64_t r = 0;
+  V3 plo{0, 0, 0}, phi{0, 0, 0};  // tree-carried components (shared-slab)
+};
+
+struct Node2 {  // view of the binary / DOP ADT:  BVH(low, high[, lo2, hi2]) = Interior(left,right) | Leaf(nprims,data)
+  Box box;
+  V4 lo2{0, 0, 0, 0}, hi2{0, 0, 0, 0};
+  bool leaf = false;
+  Ref left, right;
+  uint64_t prim_begin = 0;
+  uint32_t nprims = 0;
+  uint32_t segments_touched = 1;
+};
+
+enum LayoutId {
+  L_PBRT, L_PBRT_ALIGN16, L_PBRT_SOA, L_PBRT_POST, L_PBRT_Q16, L_SG_EQ, L_SG_EQ_ALIGN16, L_PTR, L_IDENTITY, L_SHARED_SLAB, L_DOP14,
+  L_BVH8, L_BVH8_Q8, L_BVH8_Q8_CI, L_BVH8_Q16, L_BVH8_Q16_CI, L_UNKNOWN
+};
+struct LayoutDesc {
+  const char* name;
+  LayoutId id;
+  int family;       // 0 bvh2, 1 dop14, 2 bvh8
+  uint32_t stride;  // node bytes (sum of segments)
+  int node_buffer;  // plan buffer id of the node group
+};
+static const LayoutDesc kLayouts[] = {
+    {"pbrt", L_PBRT, 0, 32, 1},           {"pbrt-align16", L_PBRT_ALIGN16, 0, 32, 1}, {"pbrt-soa", L_PBRT_SOA, 0, 32, 1},
+    {"pbrt-post", L_PBRT_POST, 0, 34, 1}, {"pbrt-q16", L_PBRT_Q16, 0, 16, 1},         {"sg-eq", L_SG_EQ, 0, 12, 1},
+    {"sg-eq-align16", L_SG_EQ_ALIGN16, 0, 16, 1}, {"ptr", L_PTR, 0, 48, 1},           {"identity", L_IDENTITY, 0, 41, 1},
+    {"shared-slab", L_SHARED_SLAB, 0, 29, 1},     {"dop14", L_DOP14, 1, 64, 1},       {"bvh8", L_BVH8, 2, 256, 1},
+    {"bvh8-q8", L_BVH8_Q8, 2, 136, 1},    {"bvh8-q8-ci", L_BVH8_Q8_CI, 2, 104, 1},    {"bvh8-q16", L_BVH8_Q16, 2, 184, 1},
+    {"bvh8-q16-ci", L_BVH8_Q16_CI, 2, 152, 1},
+};
+inline const LayoutDesc* find_layout(const char* name) {
+  for (auto& l : kLayouts)
+    if (std::string(l.name) == name) return &l;
+  return nullptr;
+}
+
+inline Ref root_ref(const TreeBytes& t, LayoutId id) {
+  Ref r;
+  r.r = t.root0;
+  if (id == L_SHARED_SLAB) {
+    r.plo = {t.carried[0], t.carried[1], t.carried[2]};
+    r.phi = {t.carried[3], t.carried[4], t.carried[5]};
+  }
+  return r;
+}
+
+// ------------------------------------------------------------------ binary + DOP decode
+inline Node2 decode2(const TreeBytes& t, LayoutId id, const Ref& ref) {
+  Node2 n;
+  const uint8_t* nodes = t.buf[1];
+  const uint64_t I = ref.r;
+  switch (id) {
+    case L_PBRT: case L_PBRT_ALIGN16: {  // pbrt.scion:5-19: low@0 high@96 union@192 nprims@224, stride 32
+      uint64_t b = I * 32 * 8;
+      n.box = {read_v3(nodes, b), read_v3(nodes, b + 96)};
+      uint32_t np = (uint32_t)read_bits(nodes, b + 224, 16);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b + 192, 32); }
+      else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b + 192, 32)); }
+      break;
+    }
+    case L_PBRT_SOA: {  // authored: seg0 = low@0 high@96 (24 B); seg1 = union@0 nprims@32 (8 B with align=8)
+      uint64_t b0 = (t.seg_base[1][0] + I * 24) * 8, b1 = (t.seg_base[1][1] + I * 8) * 8;
+      n.box = {read_v3(nodes, b0), read_v3(nodes, b0 + 96)};
+      n.segments_touched = 2;
+      uint32_t np = (uint32_t)read_bits(nodes, b1 + 32, 16);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b1, 32); }
+      else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b1, 32)); }
+      break;
+    }
+    case L_PBRT_POST: {  // pbrt_post.scion:5-19: low@0 high@96 {c_l@192,c_r@224 | p_o@192} nprims@256, stride 34
+      uint64_t b = I * 34 * 8;
+      n.box = {read_v3(nodes, b), read_v3(nodes, b + 96)};
+      uint32_t np = (uint32_t)read_bits(nodes, b + 256, 16);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b + 192, 32); }
+      else { n.left.r = (uint32_t)(I - read_bits(nodes, b + 192, 32)); n.right.r = (uint32_t)(I - read_bits(nodes, b + 224, 32)); }
+      break;
+    }
+    case L_PBRT_Q16: {  // pbrt_q16.scion:6-13,25-47: bounds_q@0:96 nprims@96:4 union@100:28, stride 16
+      uint64_t b = I * 16 * 8;
+      V3 wl = glob_v3(t, 1), we = glob_v3(t, 2);  // globals: primitive_count, world_low, world_extent, node_count
+      float rcp = 1.0f / 65535.0f;
+      float q[6];
+      for (int k = 0; k < 6; k++) q[k] = (float)(uint32_t)read_bits(nodes, b + 16 * k, 16);
+      n.box.lo = {wl.x + (q[0] * rcp) * we.x, wl.y + (q[1] * rcp) * we.y, wl.z + (q[2] * rcp) * we.z};
+      n.box.hi = {wl.x + (q[3] * rcp) * we.x, wl.y + (q[4] * rcp) * we.y, wl.z + (q[5] * rcp) * we.z};
+      uint32_t np = (uint32_t)read_bits(nodes, b + 96, 4);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b + 100, 28); }
+      else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b + 100, 28)); }
+      break;
+    }
+    case L_SG_EQ: case L_SG_EQ_ALIGN16: {  // sg_eq.scion:5-8,32-51: q_min@0:30 q_max@30:30 nprims@60:4 union@64:32
+      uint64_t b = I * (id == L_SG_EQ ? 12 : 16) * 8;
+      V3 wlow = glob_v3(t, 1), whigh = glob_v3(t, 2), bins = glob_v3(t, 3);  // primitive_count, wlow, whigh, bins, bins_inv, node_count
+      uint32_t qmin = (uint32_t)read_bits(nodes, b, 30), qmax = (uint32_t)read_bits(nodes, b + 30, 30);
+      auto deq = [&](uint32_t v) {
+        uint32_t x_ = (v >> 20) & 1023, y_ = (v >> 10) & 1023, z_ = (v >> 0) & 1023;
+        return V3{fmul_rd((float)x_, bins.x), fmul_rd((float)y_, bins.y), fmul_rd((float)z_, bins.z)};
+      };
+      V3 dl = deq(qmin), dh = deq(qmax);
+      n.box.lo = {fadd_rd(wlow.x, dl.x), fadd_rd(wlow.y, dl.y), fadd_rd(wlow.z, dl.z)};
+      n.box.hi = {fsub_ru(whigh.x, dh.x), fsub_ru(whigh.y, dh.y), fsub_ru(whigh.z, dh.z)};
+      uint32_t np = (uint32_t)read_bits(nodes, b + 60, 4);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b + 64, 32); }
+      else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b + 64, 32)); }
+      break;
+    }
+    case L_PTR: {  // ptr.scion:4-14: arena, low@0 high@96 {L@192:64,R@256:64 | p_o@192:32} nprims@320:16
+      uint64_t b = I * 8;  // reference = byte offset (plan.cpp:315-318)
+      n.box = {read_v3(nodes, b), read_v3(nodes, b + 96)};
+      uint32_t np = (uint32_t)read_bits(nodes, b + 320, 16);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b + 192, 32); }
+      else { n.left.r = read_bits(nodes, b + 192, 64); n.right.r = read_bits(nodes, b + 256, 64); }
+      break;
+    }
+    case L_IDENTITY: {  // identity.scion:5-15: low@0 high@96 tag@192:8 {left@200:64,right@264:64 | nprims@200:16,p_o@216:32}
+      uint64_t b = I * 8;
+      n.box = {read_v3(nodes, b), read_v3(nodes, b + 96)};
+      uint32_t tag = (uint32_t)read_bits(nodes, b + 192, 8);
+      if (tag == 0) { n.left.r = read_bits(nodes, b + 200, 64); n.right.r = read_bits(nodes, b + 264, 64); }
+      else { n.leaf = true; n.nprims = (uint32_t)read_bits(nodes, b + 200, 16); n.prim_begin = read_bits(nodes, b + 216, 32); }
+      break;
+    }
+    case L_SHARED_SLAB: {  // shared_slab.scion:4-38: L@0 R@64 slo@128 shi@160 o@192 axis@224:2 is_leaf@226:1 nprims@227:5
+      uint64_t b = I * 8;
+      n.box = {ref.plo, ref.phi};  // low = parent.plo; high = parent.phi
+      uint32_t is_leaf = (uint32_t)read_bits(nodes, b + 226, 1);
+      if (is_leaf == 0) {
+        uint32_t axis = (uint32_t)read_bits(nodes, b + 224, 2);
+        float slo = read_f32(nodes, b + 128), shi = read_f32(nodes, b + 160);
+        V3 alpha = ref.plo, beta = ref.phi;
+        (axis == 0 ? alpha.x : axis == 1 ? alpha.y : alpha.z) = slo;
+        (axis == 0 ? beta.x : axis == 1 ? beta.y : beta.z) = shi;
+        n.left.r = read_bits(nodes, b, 64);
+        n.right.r = read_bits(nodes, b + 64, 64);
+        n.left.plo = n.right.plo = alpha;
+        n.left.phi = n.right.phi = beta;
+      } else {
+        n.leaf = true;
+        n.nprims = (uint32_t)read_bits(nodes, b + 227, 5);
+        n.prim_begin = read_bits(nodes, b + 192, 32);
+      }
+      break;
+    }
+    case L_DOP14: {  // dop14.scion:7-22: seg0 lo1@0 hi1@96 c0@192 c1@224 (32 B); seg1 lo2@0 hi2@128 (32 B)
+      uint64_t b0 = (t.seg_base[1][0] + I * 32) * 8, b1 = (t.seg_base[1][1] + I * 32) * 8;
+      n.box = {read_v3(nodes, b0), read_v3(nodes, b0 + 96)};
+      n.lo2 = read_v4(nodes, b1);
+      n.segments_touched = 2;
+      n.hi2 = read_v4(nodes, b1 + 128);
+      int32_t c0 = (int32_t)(uint32_t)read_bits(nodes, b0 + 192, 32), c1 = (int32_t)(uint32_t)read_bits(nodes, b0 + 224, 32);
+      if (c1 >= 0) { n.left.r = (uint32_t)c0; n.right.r = (uint32_t)c1; }
+      else { n.leaf = true; n.nprims = (uint32_t)c1 & 15u; n.prim_begin = ((uint32_t)c1 >> 4) & ((1u << 27) - 1u); }
+      break;
+    }
+    default: break;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ 8-wide decode
+struct Node8 {  // BVH = Interior(children[8], lo[8], hi[8]) | Leaf(nprims, data)
+  bool leaf = false;
+  uint64_t children[8];
+  Box box[8];
+  uint64_t prim_begin = 0;
+  uint32_t nprims = 0;
+};
+inline Node8 decode8(const TreeBytes& t, LayoutId id, uint64_t I) {
+  Node8 n;
+  const bool ci = id == L_BVH8_Q8_CI || id == L_BVH8_Q16_CI;
+  const uint32_t rb = ci ? 32 : 64;
+  if ((I & 3) != 1) {  // bvh8.scion:13-15: `_ -> Leaf { O = I[7:hi]; nprims = I[2:6] + 1 }`
+    n.leaf = true;
+    n.prim_begin = ci ? ((I >> 7) & ((1ull << 25) - 1)) : (I >> 7);
+    n.nprims = (uint32_t)((I >> 2) & 31) + 1;
+    return n;
+  }
+  const uint64_t idx = ci ? ((I >> 2) & ((1ull << 30) - 1)) : (I >> 2);  // `1 -> Interior from Interiors[I[2:hi]]`
+  const uint8_t* nodes = t.buf[1];
+  switch (id) {
+    case L_BVH8: {  // bvh8.scion:8-10: lo@0:768 hi@768:768 children@1536:512, stride 256
+      uint64_t b = idx * 256 * 8;
+      for (int k = 0; k < 8; k++) {
+        n.box[k] = {read_v3(nodes, b + 96 * k), read_v3(nodes, b + 768 + 96 * k)};
+        n.children[k] = read_bits(nodes, b + 1536 + 64 * k, 64);
+      }
+      break;
+    }
+    default: {  // bvh8_q8*.scion:5-38 / bvh8_q16*.scion: mlo@0 mex@96 child_bounds@192 children after
+      const uint32_t q = (id == L_BVH8_Q8 || id == L_BVH8_Q8_CI) ? 8 : 16;
+      const uint32_t stride = id == L_BVH8_Q8 ? 136 : id == L_BVH8_Q8_CI ? 104 : id == L_BVH8_Q16 ? 184 : 152;
+      const float rcp = q == 8 ? 1 / 255.0f : 1 / 65535.0f;
+      uint64_t b = idx * stride * 8;
+      V3 mlo = read_v3(nodes, b), mex = read_v3(nodes, b + 96);
+      uint64_t cb = b + 192, ch = cb + 8 * 6 * q;
+      for (int k = 0; k < 8; k++) {
+        float c[6];
+        for (int j = 0; j < 6; j++) c[j] = (float)(uint32_t)read_bits(nodes, cb + (uint64_t)(k * 6 + j) * q, q);
+        n.box[k].lo = {mlo.x + (c[0] * rcp) * mex.x, mlo.y + (c[1] * rcp) * mex.y, mlo.z + (c[2] * rcp) * mex.z};
+        n.box[k].hi = {mlo.x + (c[3] * rcp) * mex.x, mlo.y + (c[4] * rcp) * mex.y, mlo.z + (c[5] * rcp) * mex.z};
+        n.children[k] = read_bits(nodes, ch + (uint64_t)rb * k, rb);
+      }
+      break;
+    }
+  }
+  return n;
+}
+
+inline Tri load_tri(const TreeBytes& t, uint64_t i) {  // Triangle = 3 x f32x3, stride 36 (test_plan.cpp:148)
+  Tri tr;
+  std::memcpy(&tr, t.buf[0] + i * 36, 36);
+  return tr;
+}
+
+}  // namespace oracle

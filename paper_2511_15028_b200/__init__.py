@@ -1,0 +1,497 @@
+"""scion-b200: B200-native traversal backend for Scion BVH layouts.
+
+Thin ctypes binding over the C ABI in ``include/scion_b200.h`` (``libscion_b200.so``).  The
+Python layer mirrors the operations the reference's harness/pybind module would expose for
+this path (SPEC.md:367-423 exec-backend, :593-652 cli-harness; python/layoutc_module.cpp is a
+placeholder in the reference) and adds nothing to the data path: every query runs in the CUDA
+kernels of the shared library.  There is NO CPU fallback — if the library is missing, or no
+CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libscion_b200.so")
+
+
+class ScionError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"scion error {code}: {message}")
+        self.code = code
+
+
+# status codes (scion_status)
+OK, ERR_ARG, ERR_LAYOUT, ERR_BUILD, ERR_CUDA, ERR_NO_DEVICE, ERR_QUERY = range(7)
+MISS_PRIM = 0xFFFFFFFF
+FAMILY_BVH2, FAMILY_DOP14, FAMILY_BVH8 = 0, 1, 2
+W_SENTINEL = -(2 ** 31)
+
+RAY_DTYPE = np.dtype([("ox", "f4"), ("oy", "f4"), ("oz", "f4"), ("tmax", "f4"), ("dx", "f4"), ("dy", "f4"), ("dz", "f4"), ("pad", "f4")])
+HIT_DTYPE = np.dtype([("t", "f4"), ("prim", "u4")])
+CP_DTYPE = np.dtype([("d2", "f4"), ("x", "f4"), ("y", "f4"), ("z", "f4"), ("prim", "u4")])
+COUNTERS_DTYPE = np.dtype([("node_visits", "u4"), ("prim_tests", "u4"), ("cold_loads", "u4"), ("max_stack", "u4")])
+LNODE_DTYPE = np.dtype([("lo", "f4", 3), ("hi", "f4", 3), ("left", "i4"), ("right", "i4"), ("first_prim", "u4"), ("nprims", "u4")])
+WNODE_DTYPE = np.dtype([("lo", "f4", (8, 3)), ("hi", "f4", (8, 3)), ("child", "i4", 8)])
+WLEAF_DTYPE = np.dtype([("first_prim", "u4"), ("nprims", "u4")])
+
+
+class LayoutInfo(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("family", C.c_int), ("arity", C.c_int), ("node_stride", C.c_uint32), ("node_align", C.c_uint32),
+                ("n_segments", C.c_uint32), ("ref_bits", C.c_uint32), ("max_leaf", C.c_uint32), ("has_cpq", C.c_int)]
+
+
+class Camera(C.Structure):
+    _fields_ = [("eye", C.c_float * 3), ("target", C.c_float * 3), ("up", C.c_float * 3), ("fov_y_deg", C.c_float), ("width", C.c_uint32), ("height", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the product library; fails loudly when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` (make -C paper_2511_15028_b200/csrc). "
+                          "The B200 backend has no CPU fallback.")
+    L = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    vp, u64, u32, i32, cp = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_char_p
+    P = C.POINTER
+    sigs = {
+        "scion_last_error": (cp, []),
+        "scion_abi_version": (i32, []),
+        "scion_free": (None, [vp]),
+        "scion_kernel_launches": (u64, []),
+        "scion_layout_count": (i32, []),
+        "scion_layout_info_at": (i32, [i32, P(LayoutInfo)]),
+        "scion_layout_find": (i32, [cp, P(LayoutInfo)]),
+        "scion_layout_plan_json": (i32, [cp, P(vp)]),
+        "scion_layout_emit_cuda": (i32, [cp, P(vp)]),
+        "scion_compile_layout_text": (i32, [cp, P(vp), P(vp)]),
+        "scion_scene_terrain": (i32, [u32, u64, P(vp)]),
+        "scion_scene_sphere": (i32, [u32, u64, P(vp)]),
+        "scion_scene_cloud": (i32, [u64, u64, P(vp)]),
+        "scion_scene_from_triangles": (i32, [vp, u64, P(vp)]),
+        "scion_scene_ntris": (u64, [vp]),
+        "scion_scene_triangles": (vp, [vp]),
+        "scion_scene_bounds": (None, [vp, P(C.c_float * 3), P(C.c_float * 3)]),
+        "scion_scene_free": (None, [vp]),
+        "scion_build_sah": (i32, [vp, u32, u32, u32, P(vp)]),
+        "scion_build_median": (i32, [vp, u32, P(vp)]),
+        "scion_ltree_collapse8": (i32, [vp]),
+        "scion_ltree_nnodes": (u64, [vp]),
+        "scion_ltree_nodes": (vp, [vp]),
+        "scion_ltree_nprims": (u64, [vp]),
+        "scion_ltree_triangles": (vp, [vp]),
+        "scion_ltree_prim_ids": (vp, [vp]),
+        "scion_ltree_dop_lo2": (vp, [vp]),
+        "scion_ltree_dop_hi2": (vp, [vp]),
+        "scion_ltree_depth": (u32, [vp]),
+        "scion_ltree_nwnodes": (u64, [vp]),
+        "scion_ltree_wnodes": (vp, [vp]),
+        "scion_ltree_nwleaves": (u64, [vp]),
+        "scion_ltree_wleaves": (vp, [vp]),
+        "scion_ltree_wroot": (C.c_int32, [vp]),
+        "scion_ltree_free": (None, [vp]),
+        "scion_encode": (i32, [vp, cp, P(vp)]),
+        "scion_ptree_layout": (cp, [vp]),
+        "scion_ptree_nbuffers": (i32, [vp]),
+        "scion_ptree_buffer": (i32, [vp, i32, P(cp), P(vp), P(u64), P(u64)]),
+        "scion_ptree_segment_bases": (i32, [vp, i32, P(u64), i32]),
+        "scion_ptree_nglobals": (i32, [vp]),
+        "scion_ptree_global": (i32, [vp, i32, P(cp), P(C.c_uint8), P(u32)]),
+        "scion_ptree_root": (i32, [vp, P(u64), P(C.c_float)]),
+        "scion_ptree_total_bytes": (u64, [vp]),
+        "scion_ptree_node_bytes": (u64, [vp]),
+        "scion_ptree_corrupt": (i32, [vp, i32, u64, C.c_uint8]),
+        "scion_ptree_free": (None, [vp]),
+        "scion_device_count": (i32, [P(i32)]),
+        "scion_dtree_upload": (i32, [vp, i32, P(vp)]),
+        "scion_dtree_alloc_like": (i32, [vp, i32, P(vp)]),
+        "scion_dtree_image": (i32, [vp, P(vp), P(u64)]),
+        "scion_dtree_from_image": (i32, [cp, vp, u64, i32, i32, P(vp)]),
+        "scion_dtree_free": (None, [vp]),
+        "scion_closest_hit": (i32, [vp, vp, u64, vp, vp, vp, i32, vp]),
+        "scion_closest_point": (i32, [vp, vp, u64, vp, vp, vp, i32, vp]),
+        "scion_closest_hit_host": (i32, [vp, vp, u64, vp, vp]),
+        "scion_closest_point_host": (i32, [vp, vp, u64, vp, vp]),
+        "scion_camera_default": (None, [P(C.c_float * 3), P(C.c_float * 3), i32, u32, u32, P(Camera)]),
+        "scion_gen_primary": (i32, [P(Camera), u64, u64, vp, vp]),
+        "scion_gen_secondary": (i32, [vp, u64, u64, u64, vp, vp]),
+        "scion_gen_points": (i32, [P(C.c_float * 3), P(C.c_float * 3), u64, u64, u64, vp, vp]),
+        "scion_gen_primary_host": (i32, [P(Camera), u64, u64, vp]),
+        "scion_gen_secondary_host": (i32, [vp, u64, u64, u64, u64, vp]),
+        "scion_gen_points_host": (i32, [P(C.c_float * 3), P(C.c_float * 3), u64, u64, u64, vp]),
+        "scion_partition": (None, [u64, i32, i32, P(u64), P(u64)]),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)  # AttributeError here == the library does not export a declared symbol
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+ABI_SYMBOLS = None  # filled lazily by abi_symbols()
+
+
+def abi_symbols():
+    """Every function name declared in include/scion_b200.h (parsed from the header text)."""
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "scion_b200.h")
+    text = open(hdr).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(scion_[a-z0-9_]+)\s*\(", text)))
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise ScionError(rc, lib().scion_last_error().decode())
+
+
+def _take_string(p: C.c_void_p) -> str:
+    s = C.string_at(p).decode()
+    lib().scion_free(p)
+    return s
+
+
+def _f3(v):
+    return (C.c_float * 3)(*[float(x) for x in v])
+
+
+def _np_view(ptr, count, dtype):
+    if not ptr or count == 0:
+        return np.zeros(0, dtype=dtype)
+    nbytes = int(count) * np.dtype(dtype).itemsize
+    buf = (C.c_uint8 * nbytes).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype)
+
+
+# --------------------------------------------------------------------------------------- registry
+def layouts():
+    out = []
+    n = lib().scion_layout_count()
+    for i in range(n):
+        info = LayoutInfo()
+        _check(lib().scion_layout_info_at(i, C.byref(info)))
+        out.append(dict(name=info.name.decode(), family=info.family, arity=info.arity, node_stride=info.node_stride, node_align=info.node_align,
+                        n_segments=info.n_segments, ref_bits=info.ref_bits, max_leaf=info.max_leaf, has_cpq=bool(info.has_cpq)))
+    return out
+
+
+def layout_info(name: str) -> dict:
+    for l in layouts():
+        if l["name"] == name:
+            return l
+    raise ScionError(ERR_ARG, f"unknown layout '{name}'")
+
+
+def layout_plan(name: str) -> dict:
+    p = C.c_void_p()
+    _check(lib().scion_layout_plan_json(name.encode(), C.byref(p)))
+    return json.loads(_take_string(p))
+
+
+def emit_cuda(name: str) -> str:
+    p = C.c_void_p()
+    _check(lib().scion_layout_emit_cuda(name.encode(), C.byref(p)))
+    return _take_string(p)
+
+
+def compile_layout_text(source: str):
+    """Layout compiler front door: .scion text -> (plan dict, CUDA header text)."""
+    pj, pc = C.c_void_p(), C.c_void_p()
+    _check(lib().scion_compile_layout_text(source.encode(), C.byref(pj), C.byref(pc)))
+    return json.loads(_take_string(pj)), _take_string(pc)
+
+
+# --------------------------------------------------------------------------------------- scene tools
+class Scene:
+    def __init__(self, handle):
+        self._h = handle
+
+    @staticmethod
+    def terrain(grid: int, seed: int = 1) -> "Scene":
+        h = C.c_void_p()
+        _check(lib().scion_scene_terrain(grid, seed, C.byref(h)))
+        return Scene(h)
+
+    @staticmethod
+    def sphere(grid: int, seed: int = 1) -> "Scene":
+        h = C.c_void_p()
+        _check(lib().scion_scene_sphere(grid, seed, C.byref(h)))
+        return Scene(h)
+
+    @staticmethod
+    def cloud(npoints: int, seed: int = 1) -> "Scene":
+        h = C.c_void_p()
+        _check(lib().scion_scene_cloud(npoints, seed, C.byref(h)))
+        return Scene(h)
+
+    @staticmethod
+    def from_triangles(tris) -> "Scene":
+        a = np.ascontiguousarray(tris, dtype=np.float32).reshape(-1, 9)
+        h = C.c_void_p()
+        _check(lib().scion_scene_from_triangles(a.ctypes.data, a.shape[0], C.byref(h)))
+        return Scene(h)
+
+    @property
+    def ntris(self) -> int:
+        return lib().scion_scene_ntris(self._h)
+
+    def triangles(self) -> np.ndarray:
+        return _np_view(lib().scion_scene_triangles(self._h), self.ntris * 9, np.float32).reshape(-1, 9)
+
+    def bounds(self):
+        lo, hi = (C.c_float * 3)(), (C.c_float * 3)()
+        lib().scion_scene_bounds(self._h, C.byref(lo), C.byref(hi))
+        return np.array(lo[:], np.float32), np.array(hi[:], np.float32)
+
+    def build_sah(self, bins: int = 32, max_leaf: int = 4, max_depth: int = 0) -> "LogicalTree":
+        h = C.c_void_p()
+        _check(lib().scion_build_sah(self._h, bins, max_leaf, max_depth, C.byref(h)))
+        return LogicalTree(h)
+
+    def build_median(self, max_leaf: int = 1) -> "LogicalTree":
+        h = C.c_void_p()
+        _check(lib().scion_build_median(self._h, max_leaf, C.byref(h)))
+        return LogicalTree(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.scion_scene_free(self._h)
+            self._h = None
+
+
+class LogicalTree:
+    def __init__(self, handle):
+        self._h = handle
+
+    def collapse8(self) -> "LogicalTree":
+        _check(lib().scion_ltree_collapse8(self._h))
+        return self
+
+    @property
+    def nnodes(self) -> int:
+        return lib().scion_ltree_nnodes(self._h)
+
+    @property
+    def nprims(self) -> int:
+        return lib().scion_ltree_nprims(self._h)
+
+    @property
+    def depth(self) -> int:
+        return lib().scion_ltree_depth(self._h)
+
+    def nodes(self) -> np.ndarray:
+        return _np_view(lib().scion_ltree_nodes(self._h), self.nnodes, LNODE_DTYPE)
+
+    def triangles(self) -> np.ndarray:
+        return _np_view(lib().scion_ltree_triangles(self._h), self.nprims * 9, np.float32).reshape(-1, 9)
+
+    def prim_ids(self) -> np.ndarray:
+        return _np_view(lib().scion_ltree_prim_ids(self._h), self.nprims, np.uint32)
+
+    def dop(self):
+        n = self.nnodes
+        return (_np_view(lib().scion_ltree_dop_lo2(self._h), n * 4, np.float32).reshape(-1, 4),
+                _np_view(lib().scion_ltree_dop_hi2(self._h), n * 4, np.float32).reshape(-1, 4))
+
+    def wnodes(self) -> np.ndarray:
+        return _np_view(lib().scion_ltree_wnodes(self._h), lib().scion_ltree_nwnodes(self._h), WNODE_DTYPE)
+
+    def wleaves(self) -> np.ndarray:
+        return _np_view(lib().scion_ltree_wleaves(self._h), lib().scion_ltree_nwleaves(self._h), WLEAF_DTYPE)
+
+    @property
+    def wroot(self) -> int:
+        return lib().scion_ltree_wroot(self._h)
+
+    def encode(self, layout: str) -> "PhysicalTree":
+        h = C.c_void_p()
+        _check(lib().scion_encode(self._h, layout.encode(), C.byref(h)))
+        return PhysicalTree(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.scion_ltree_free(self._h)
+            self._h = None
+
+
+class PhysicalTree:
+    """Host PhysicalTree: buffer id -> bytes, globals, root reference."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @property
+    def layout(self) -> str:
+        return lib().scion_ptree_layout(self._h).decode()
+
+    def buffers(self):
+        out = []
+        for i in range(lib().scion_ptree_nbuffers(self._h)):
+            name, data, nbytes, count = C.c_char_p(), C.c_void_p(), C.c_uint64(), C.c_uint64()
+            _check(lib().scion_ptree_buffer(self._h, i, C.byref(name), C.byref(data), C.byref(nbytes), C.byref(count)))
+            bases = (C.c_uint64 * 4)()
+            ns = lib().scion_ptree_segment_bases(self._h, i, bases, 4)
+            out.append(dict(name=name.value.decode(), data=_np_view(data.value, nbytes.value, np.uint8), ptr=data.value, bytes=nbytes.value,
+                            count=count.value, seg_bases=list(bases[:ns])))
+        return out
+
+    def globals(self):
+        out = []
+        for i in range(lib().scion_ptree_nglobals(self._h)):
+            name, raw, nb = C.c_char_p(), (C.c_uint8 * 16)(), C.c_uint32()
+            _check(lib().scion_ptree_global(self._h, i, C.byref(name), raw, C.byref(nb)))
+            out.append(dict(name=name.value.decode(), raw=bytes(raw), nbytes=nb.value))
+        return out
+
+    def root(self):
+        r, carried = C.c_uint64(), (C.c_float * 6)()
+        _check(lib().scion_ptree_root(self._h, C.byref(r), carried))
+        return r.value, list(carried)
+
+    @property
+    def total_bytes(self) -> int:
+        return lib().scion_ptree_total_bytes(self._h)
+
+    @property
+    def node_bytes(self) -> int:
+        return lib().scion_ptree_node_bytes(self._h)
+
+    def corrupt(self, buffer: int, byte_offset: int, xor_mask: int = 0xFF):
+        _check(lib().scion_ptree_corrupt(self._h, buffer, byte_offset, xor_mask))
+
+    def upload(self, device: int = 0) -> "DeviceTree":
+        h = C.c_void_p()
+        _check(lib().scion_dtree_upload(self._h, device, C.byref(h)))
+        return DeviceTree(h, device)
+
+    def alloc_like(self, device: int = 0) -> "DeviceTree":
+        h = C.c_void_p()
+        _check(lib().scion_dtree_alloc_like(self._h, device, C.byref(h)))
+        return DeviceTree(h, device)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.scion_ptree_free(self._h)
+            self._h = None
+
+
+def device_count() -> int:
+    n = C.c_int()
+    rc = lib().scion_device_count(C.byref(n))
+    return n.value if rc == 0 else 0
+
+
+class DeviceTree:
+    """PhysicalTree resident on one GPU; immutable, safe to query from several streams."""
+
+    def __init__(self, handle, device):
+        self._h = handle
+        self.device = device
+
+    def image(self):
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(lib().scion_dtree_image(self._h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    @staticmethod
+    def from_image(d_ptr: int, nbytes: int, device: int, layout: Optional[str] = None, adopt: bool = False) -> "DeviceTree":
+        h = C.c_void_p()
+        _check(lib().scion_dtree_from_image(layout.encode() if layout else None, d_ptr, nbytes, device, 1 if adopt else 0, C.byref(h)))
+        return DeviceTree(h, device)
+
+    # device-pointer entry points (asynchronous on `stream`)
+    def closest_hit(self, d_rays: int, n: int, d_hits: int, d_status: int = 0, d_counters: int = 0, variant: int = 0, stream: int = 0):
+        _check(lib().scion_closest_hit(self._h, d_rays, n, d_hits, d_status or None, d_counters or None, variant, stream or None))
+
+    def closest_point(self, d_points: int, n: int, d_out: int, d_status: int = 0, d_counters: int = 0, variant: int = 0, stream: int = 0):
+        _check(lib().scion_closest_point(self._h, d_points, n, d_out, d_status or None, d_counters or None, variant, stream or None))
+
+    # host-buffer entry points (H2D + kernel + D2H inside the call)
+    def closest_hit_host(self, rays: np.ndarray, hits: Optional[np.ndarray] = None, status: Optional[np.ndarray] = None):
+        assert rays.dtype == RAY_DTYPE and rays.flags.c_contiguous
+        n = rays.shape[0]
+        if hits is None:
+            hits = np.empty(n, HIT_DTYPE)
+        _check(lib().scion_closest_hit_host(self._h, rays.ctypes.data, n, hits.ctypes.data, status.ctypes.data if status is not None else None))
+        return hits
+
+    def closest_point_host(self, points: np.ndarray, out: Optional[np.ndarray] = None, status: Optional[np.ndarray] = None):
+        pts = np.ascontiguousarray(points, np.float32).reshape(-1, 3)
+        n = pts.shape[0]
+        if out is None:
+            out = np.empty(n, CP_DTYPE)
+        _check(lib().scion_closest_point_host(self._h, pts.ctypes.data, n, out.ctypes.data, status.ctypes.data if status is not None else None))
+        return out
+
+    def gen_secondary(self, seed: int, first: int, n: int, d_rays: int, stream: int = 0):
+        _check(lib().scion_gen_secondary(self._h, seed, first, n, d_rays, stream or None))
+
+    def free(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.scion_dtree_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.free()
+
+
+# --------------------------------------------------------------------------------------- generators
+def default_camera(lo, hi, look_down_y: bool, width: int, height: int) -> Camera:
+    cam = Camera()
+    lib().scion_camera_default(C.byref(_f3(lo)), C.byref(_f3(hi)), 1 if look_down_y else 0, width, height, C.byref(cam))
+    return cam
+
+
+def gen_primary(cam: Camera, first: int, n: int, d_rays: int, stream: int = 0):
+    _check(lib().scion_gen_primary(C.byref(cam), first, n, d_rays, stream or None))
+
+
+def gen_points(lo, hi, seed: int, first: int, n: int, d_points: int, stream: int = 0):
+    _check(lib().scion_gen_points(C.byref(_f3(lo)), C.byref(_f3(hi)), seed, first, n, d_points, stream or None))
+
+
+def gen_primary_host(cam: Camera, first: int, n: int) -> np.ndarray:
+    rays = np.empty(n, RAY_DTYPE)
+    _check(lib().scion_gen_primary_host(C.byref(cam), first, n, rays.ctypes.data))
+    return rays
+
+
+def gen_secondary_host(tris: np.ndarray, seed: int, first: int, n: int) -> np.ndarray:
+    t = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
+    rays = np.empty(n, RAY_DTYPE)
+    _check(lib().scion_gen_secondary_host(t.ctypes.data, t.shape[0], seed, first, n, rays.ctypes.data))
+    return rays
+
+
+def gen_points_host(lo, hi, seed: int, first: int, n: int) -> np.ndarray:
+    pts = np.empty((n, 3), np.float32)
+    _check(lib().scion_gen_points_host(C.byref(_f3(lo)), C.byref(_f3(hi)), seed, first, n, pts.ctypes.data))
+    return pts
+
+
+def partition(n: int, rank: int, nranks: int):
+    """Contiguous query partition [first, first+count) of rank `rank`."""
+    a, b = C.c_uint64(), C.c_uint64()
+    lib().scion_partition(n, rank, nranks, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def kernel_launches() -> int:
+    return lib().scion_kernel_launches()
+
+
+def seed_from_env(default: int) -> int:
+    """LAYOUTC_SEED overrides the configured seed."""
+    v = os.environ.get("LAYOUTC_SEED")
+    return int(v, 0) if v else default

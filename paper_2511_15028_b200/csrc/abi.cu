@@ -1,0 +1,568 @@
+// C ABI of the backend (include/scion_b200.h): thin extern "C" layer over the host C++ (layout
+// compiler, scene tools, encoders) and the CUDA kernels.  Nothing here falls back to a CPU
+// traversal: without a CUDA device every query entry point fails with SCION_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "device/launch.cuh"
+#include "host/physical.hpp"
+#include "host/rng.hpp"
+#include "host/scene.hpp"
+#include "scion_b200.h"
+
+namespace {
+
+thread_local std::string g_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+#define SCION_TRY(...)                                              \
+  try {                                                             \
+    __VA_ARGS__                                                     \
+  } catch (const scion::lc::LayoutError& e) {                       \
+    return fail(SCION_ERR_LAYOUT, e.what());                        \
+  } catch (const std::bad_alloc&) {                                 \
+    return fail(SCION_ERR_BUILD, "out of host memory");             \
+  } catch (const std::exception& e) {                               \
+    return fail(SCION_ERR_BUILD, e.what());                         \
+  }
+#define CUDA_OK(expr)                                                                                  \
+  do {                                                                                                 \
+    cudaError_t e__ = (expr);                                                                          \
+    if (e__ != cudaSuccess) return fail(e__ == cudaErrorNoDevice || e__ == cudaErrorInsufficientDriver ? SCION_ERR_NO_DEVICE : SCION_ERR_CUDA, \
+                                        std::string(#expr) + ": " + cudaGetErrorString(e__));          \
+  } while (0)
+
+char* dup_string(const std::string& s) {
+  char* p = (char*)malloc(s.size() + 1);
+  if (p) memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+// ------------------------------------------------------------------ device image
+// One contiguous allocation: [ImageHeader | buffer 0 | buffer 1 | ...], every buffer 256-byte
+// aligned and followed by >= 16 bytes of slack (covering vector loads, geometry.cuh).
+constexpr uint64_t kImageMagic = 0x3130304d49434353ull;  // "SCCIM001"
+struct ImageHeader {
+  uint64_t magic;
+  uint64_t total_bytes;
+  char layout[48];
+  int32_t nbuf, nglob;
+  uint64_t offset[SCION_MAX_BUFFERS];
+  uint64_t bytes[SCION_MAX_BUFFERS];
+  uint64_t count[SCION_MAX_BUFFERS];
+  uint64_t seg_base[SCION_MAX_BUFFERS][SCION_MAX_SEGMENTS];
+  uint32_t glob[SCION_MAX_GLOBALS][4];
+  uint64_t root0;
+  float carried[6];
+  uint64_t nprims;
+  uint8_t pad[16];
+};
+static_assert(sizeof(ImageHeader) % 16 == 0, "image header must keep 16-byte alignment");
+constexpr uint64_t kHeaderBytes = (sizeof(ImageHeader) + 255) / 256 * 256;
+constexpr int kCounterSlots = 64;
+
+}  // namespace
+
+struct scion_dtree {
+  const scion::LayoutEntry* layout = nullptr;
+  const scion::KernelEntry* kernels = nullptr;
+  int device = 0;
+  uint8_t* image = nullptr;
+  bool owns_image = true;
+  ImageHeader header{};
+  scion::TreeView view{};
+  unsigned long long* counters = nullptr;  // kCounterSlots work-fetch counters
+  std::atomic<uint32_t> next_slot{0};
+  // staging for the host entry points
+  void* h2d[2] = {nullptr, nullptr};
+  void* d2h[2] = {nullptr, nullptr};
+  uint32_t* d_status[2] = {nullptr, nullptr};
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  uint64_t chunk = 0;
+  std::mutex host_mutex;
+};
+
+namespace {
+
+void fill_view(scion_dtree& t) {
+  const ImageHeader& h = t.header;
+  memset(&t.view, 0, sizeof(t.view));
+  for (int b = 0; b < h.nbuf; b++) {
+    t.view.buf[b] = t.image + h.offset[b];
+    t.view.count[b] = h.count[b];
+    for (int s = 0; s < SCION_MAX_SEGMENTS; s++) t.view.seg_base[b][s] = h.seg_base[b][s];
+  }
+  memcpy(t.view.glob, h.glob, sizeof(h.glob));
+  t.view.root0 = h.root0;
+  memcpy(t.view.root_carried, h.carried, sizeof(h.carried));
+}
+
+int header_from_ptree(const scion_ptree& p, ImageHeader& h) {
+  memset(&h, 0, sizeof(h));
+  h.magic = kImageMagic;
+  if (p.buffers.size() > SCION_MAX_BUFFERS || p.globals.size() > SCION_MAX_GLOBALS) return fail(SCION_ERR_LAYOUT, "layout exceeds the device view limits");
+  strncpy(h.layout, p.layout.c_str(), sizeof(h.layout) - 1);
+  h.nbuf = (int32_t)p.buffers.size();
+  h.nglob = (int32_t)p.globals.size();
+  uint64_t off = kHeaderBytes;
+  for (size_t b = 0; b < p.buffers.size(); b++) {
+    if (p.seg_bases[b].size() > SCION_MAX_SEGMENTS) return fail(SCION_ERR_LAYOUT, "too many segments");
+    h.offset[b] = off;
+    h.bytes[b] = p.buffers[b].size();
+    h.count[b] = p.counts[b];
+    for (size_t s = 0; s < p.seg_bases[b].size(); s++) h.seg_base[b][s] = p.seg_bases[b][s];
+    off += (p.buffers[b].size() + 16 + 255) / 256 * 256;
+  }
+  for (size_t g = 0; g < p.globals.size(); g++) memcpy(h.glob[g], p.globals[g].data(), 16);
+  h.root0 = p.root0;
+  memcpy(h.carried, p.carried, sizeof(h.carried));
+  h.nprims = p.nprims;
+  h.total_bytes = off;
+  return SCION_OK;
+}
+
+int finish_dtree(scion_dtree* t) {
+  t->kernels = scion::find_kernels(t->layout->name.c_str());
+  if (!t->kernels) return fail(SCION_ERR_LAYOUT, "no kernels were compiled for layout '" + t->layout->name + "'");
+  CUDA_OK(cudaMalloc(&t->counters, kCounterSlots * sizeof(unsigned long long)));
+  fill_view(*t);
+  return SCION_OK;
+}
+
+unsigned long long* take_counter(const scion_dtree* t) {
+  scion_dtree* m = const_cast<scion_dtree*>(t);
+  return m->counters + (m->next_slot.fetch_add(1) % kCounterSlots);
+}
+
+}  // namespace
+
+namespace scion {
+int device_sm_count() {
+  static int sms[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (sms[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    sms[dev] = v;
+  }
+  return sms[dev];
+}
+}  // namespace scion
+
+extern "C" {
+
+const char* scion_last_error(void) { return g_error.c_str(); }
+int scion_abi_version(void) { return SCION_ABI_VERSION; }
+void scion_free(void* p) { free(p); }
+uint64_t scion_kernel_launches(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------------ layout registry
+static void info_of(const scion::LayoutEntry& e, scion_layout_info* out) {
+  const scion::lc::Plan& p = *e.plan;
+  out->name = e.name.c_str();
+  out->family = (int)p.family;
+  out->arity = p.family == scion::lc::Family::Bvh8 ? 8 : 2;
+  const scion::lc::Buffer* nb = p.buffer_named(p.node_group);
+  out->node_stride = nb ? (uint32_t)nb->node_stride() : 0;
+  out->node_align = nb ? nb->align : 1;
+  out->n_segments = nb ? (uint32_t)nb->segments.size() : 0;
+  out->ref_bits = (uint32_t)p.type_bits(p.ref[0].type);
+  out->max_leaf = p.max_leaf;
+  out->has_cpq = e.has_cpq ? 1 : 0;
+}
+int scion_layout_count(void) {
+  SCION_TRY(return (int)scion::layout_registry().size();)
+}
+int scion_layout_info_at(int index, scion_layout_info* out) {
+  SCION_TRY(auto& r = scion::layout_registry(); if (index < 0 || index >= (int)r.size() || !out) return fail(SCION_ERR_ARG, "layout index out of range"); info_of(r[(size_t)index], out); return SCION_OK;)
+}
+int scion_layout_find(const char* name, scion_layout_info* out) {
+  SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + (name ? name : "") + "'"); if (out) info_of(*e, out); return SCION_OK;)
+}
+int scion_layout_plan_json(const char* name, char** out_json) {
+  SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e || !out_json) return fail(SCION_ERR_ARG, "unknown layout"); *out_json = dup_string(e->plan->to_json()); return SCION_OK;)
+}
+int scion_layout_emit_cuda(const char* name, char** out_text) {
+  SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e || !out_text) return fail(SCION_ERR_ARG, "unknown layout"); *out_text = dup_string(scion::lc::emit_cuda(*e->plan)); return SCION_OK;)
+}
+int scion_compile_layout_text(const char* src, char** out_plan_json, char** out_cuda) {
+  if (!src) return fail(SCION_ERR_ARG, "null source");
+  SCION_TRY(scion::lc::Program prog = scion::lc::parse_program({std::string(src)}); scion::lc::Plan plan = scion::lc::plan_layout(prog, "user-layout");
+            if (out_plan_json) *out_plan_json = dup_string(plan.to_json()); if (out_cuda) *out_cuda = dup_string(scion::lc::emit_cuda(plan)); return SCION_OK;)
+}
+
+// ------------------------------------------------------------------ scene tools
+int scion_scene_terrain(uint32_t grid, uint64_t seed, scion_scene** out) {
+  if (!out) return fail(SCION_ERR_ARG, "null out");
+  SCION_TRY(auto* s = new scion_scene(); scion::make_terrain(grid, seed, *s); *out = s; return SCION_OK;)
+}
+int scion_scene_sphere(uint32_t grid, uint64_t seed, scion_scene** out) {
+  if (!out) return fail(SCION_ERR_ARG, "null out");
+  SCION_TRY(auto* s = new scion_scene(); scion::make_sphere(grid, seed, *s); *out = s; return SCION_OK;)
+}
+int scion_scene_cloud(uint64_t npoints, uint64_t seed, scion_scene** out) {
+  if (!out) return fail(SCION_ERR_ARG, "null out");
+  SCION_TRY(auto* s = new scion_scene(); scion::make_cloud(npoints, seed, *s); *out = s; return SCION_OK;)
+}
+int scion_scene_from_triangles(const float* xyz9, uint64_t ntris, scion_scene** out) {
+  if (!out || (!xyz9 && ntris)) return fail(SCION_ERR_ARG, "null argument");
+  SCION_TRY(auto* s = new scion_scene(); s->name = "user"; s->tris.assign(xyz9, xyz9 + ntris * 9); *out = s; return SCION_OK;)
+}
+uint64_t scion_scene_ntris(const scion_scene* s) { return s ? s->ntris() : 0; }
+const float* scion_scene_triangles(const scion_scene* s) { return s ? s->tris.data() : nullptr; }
+void scion_scene_bounds(const scion_scene* s, float lo[3], float hi[3]) { if (s) scion::scene_bounds(*s, lo, hi); }
+void scion_scene_free(scion_scene* s) { delete s; }
+
+int scion_build_sah(const scion_scene* s, uint32_t bins, uint32_t max_leaf, uint32_t max_depth, scion_ltree** out) {
+  if (!s || !out) return fail(SCION_ERR_ARG, "null argument");
+  SCION_TRY(auto* t = new scion_ltree(); try { scion::build_binary(*s, scion::Builder::SAH, bins, max_leaf, max_depth, *t); } catch (...) { delete t; throw; } *out = t; return SCION_OK;)
+}
+int scion_build_median(const scion_scene* s, uint32_t max_leaf, scion_ltree** out) {
+  if (!s || !out) return fail(SCION_ERR_ARG, "null argument");
+  SCION_TRY(auto* t = new scion_ltree(); try { scion::build_binary(*s, scion::Builder::Median, 2, max_leaf, 0, *t); } catch (...) { delete t; throw; } *out = t; return SCION_OK;)
+}
+int scion_ltree_collapse8(scion_ltree* t) {
+  if (!t) return fail(SCION_ERR_ARG, "null tree");
+  SCION_TRY(scion::collapse8(*t); return SCION_OK;)
+}
+uint64_t scion_ltree_nnodes(const scion_ltree* t) { return t->nodes.size(); }
+const scion_lnode* scion_ltree_nodes(const scion_ltree* t) { return t->nodes.data(); }
+uint64_t scion_ltree_nprims(const scion_ltree* t) { return t->tris.size() / 9; }
+const float* scion_ltree_triangles(const scion_ltree* t) { return t->tris.data(); }
+const uint32_t* scion_ltree_prim_ids(const scion_ltree* t) { return t->prim_ids.data(); }
+const float* scion_ltree_dop_lo2(const scion_ltree* t) { return t->dop_lo2.data(); }
+const float* scion_ltree_dop_hi2(const scion_ltree* t) { return t->dop_hi2.data(); }
+uint32_t scion_ltree_depth(const scion_ltree* t) { return t->depth; }
+uint64_t scion_ltree_nwnodes(const scion_ltree* t) { return t->wnodes.size(); }
+const scion_wnode* scion_ltree_wnodes(const scion_ltree* t) { return t->wnodes.data(); }
+uint64_t scion_ltree_nwleaves(const scion_ltree* t) { return t->wleaves.size(); }
+const scion_wleaf* scion_ltree_wleaves(const scion_ltree* t) { return t->wleaves.data(); }
+int32_t scion_ltree_wroot(const scion_ltree* t) { return t->wroot; }
+void scion_ltree_free(scion_ltree* t) { delete t; }
+
+// ------------------------------------------------------------------ build_physical
+int scion_encode(const scion_ltree* t, const char* layout, scion_ptree** out) {
+  if (!t || !layout || !out) return fail(SCION_ERR_ARG, "null argument");
+  SCION_TRY(const scion::LayoutEntry* e = scion::find_layout(layout); if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + layout + "'");
+            if (e->plan->family == scion::lc::Family::Bvh8 && !t->has_wide) return fail(SCION_ERR_BUILD, "8-wide layouts need scion_ltree_collapse8 first");
+            auto* p = new scion_ptree(); try { scion::encode_tree(*t, *e, *p); } catch (...) { delete p; throw; } *out = p; return SCION_OK;)
+}
+const char* scion_ptree_layout(const scion_ptree* p) { return p->layout.c_str(); }
+int scion_ptree_nbuffers(const scion_ptree* p) { return (int)p->buffers.size(); }
+int scion_ptree_buffer(const scion_ptree* p, int i, const char** name, const uint8_t** data, uint64_t* bytes, uint64_t* count) {
+  if (!p || i < 0 || i >= (int)p->buffers.size()) return fail(SCION_ERR_ARG, "buffer index out of range");
+  if (name) *name = p->plan->buffers[(size_t)i].name.c_str();
+  if (data) *data = p->buffers[(size_t)i].data();
+  if (bytes) *bytes = p->buffers[(size_t)i].size();
+  if (count) *count = p->counts[(size_t)i];
+  return SCION_OK;
+}
+int scion_ptree_segment_bases(const scion_ptree* p, int i, uint64_t* bases, int max) {
+  if (!p || i < 0 || i >= (int)p->buffers.size()) return 0;
+  int n = (int)p->seg_bases[(size_t)i].size();
+  for (int s = 0; s < n && s < max; s++) bases[s] = p->seg_bases[(size_t)i][(size_t)s];
+  return n;
+}
+int scion_ptree_nglobals(const scion_ptree* p) { return (int)p->globals.size(); }
+int scion_ptree_global(const scion_ptree* p, int i, const char** name, uint8_t raw[16], uint32_t* nbytes) {
+  if (!p || i < 0 || i >= (int)p->globals.size()) return fail(SCION_ERR_ARG, "global index out of range");
+  if (name) *name = p->plan->globals[(size_t)i].name.c_str();
+  if (raw) memcpy(raw, p->globals[(size_t)i].data(), 16);
+  if (nbytes) *nbytes = (uint32_t)((p->plan->type_bits(p->plan->globals[(size_t)i].type) + 7) / 8);
+  return SCION_OK;
+}
+int scion_ptree_root(const scion_ptree* p, uint64_t* ref0, float* carried6) {
+  if (!p) return fail(SCION_ERR_ARG, "null tree");
+  if (ref0) *ref0 = p->root0;
+  if (carried6) memcpy(carried6, p->carried, sizeof(p->carried));
+  return SCION_OK;
+}
+uint64_t scion_ptree_total_bytes(const scion_ptree* p) {
+  uint64_t s = 0;
+  for (auto& b : p->buffers) s += b.size();
+  return s;
+}
+uint64_t scion_ptree_node_bytes(const scion_ptree* p) {
+  uint64_t s = 0;
+  for (size_t b = 0; b < p->buffers.size(); b++)
+    if (!p->plan->buffers[b].is_global_array) s += p->buffers[b].size();
+  return s;
+}
+int scion_ptree_corrupt(scion_ptree* p, int buffer, uint64_t byte_offset, uint8_t xor_mask) {
+  if (!p || buffer < 0 || buffer >= (int)p->buffers.size() || byte_offset >= p->buffers[(size_t)buffer].size()) return fail(SCION_ERR_ARG, "corrupt: out of range");
+  p->buffers[(size_t)buffer][byte_offset] ^= xor_mask;
+  return SCION_OK;
+}
+void scion_ptree_free(scion_ptree* p) { delete p; }
+
+// ------------------------------------------------------------------ device residency
+int scion_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) { if (out) *out = 0; return fail(SCION_ERR_NO_DEVICE, cudaGetErrorString(e)); }
+  if (out) *out = n;
+  return SCION_OK;
+}
+
+static int dtree_create(const scion_ptree* p, int device, bool copy, scion_dtree** out) {
+  if (!p || !out) return fail(SCION_ERR_ARG, "null argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(SCION_ERR_NO_DEVICE, "no CUDA device: the B200 backend has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(SCION_ERR_ARG, "device index out of range");
+  const scion::LayoutEntry* e = scion::find_layout(p->layout);
+  if (!e) return fail(SCION_ERR_ARG, "unknown layout");
+  auto* t = new scion_dtree();
+  t->layout = e;
+  t->device = device;
+  int rc = header_from_ptree(*p, t->header);
+  if (rc) { delete t; return rc; }
+  CUDA_OK(cudaSetDevice(device));
+  CUDA_OK(cudaMalloc(&t->image, t->header.total_bytes));
+  CUDA_OK(cudaMemset(t->image, 0, t->header.total_bytes));
+  CUDA_OK(cudaMemcpy(t->image, &t->header, sizeof(ImageHeader), cudaMemcpyHostToDevice));
+  if (copy)
+    for (size_t b = 0; b < p->buffers.size(); b++)
+      if (!p->buffers[b].empty()) CUDA_OK(cudaMemcpy(t->image + t->header.offset[b], p->buffers[b].data(), p->buffers[b].size(), cudaMemcpyHostToDevice));
+  rc = finish_dtree(t);
+  if (rc) { scion_dtree_free(t); return rc; }
+  *out = t;
+  return SCION_OK;
+}
+int scion_dtree_upload(const scion_ptree* p, int device, scion_dtree** out) { return dtree_create(p, device, true, out); }
+int scion_dtree_alloc_like(const scion_ptree* p, int device, scion_dtree** out) { return dtree_create(p, device, false, out); }
+
+int scion_dtree_image(const scion_dtree* t, void** d_ptr, uint64_t* bytes) {
+  if (!t) return fail(SCION_ERR_ARG, "null tree");
+  if (d_ptr) *d_ptr = t->image;
+  if (bytes) *bytes = t->header.total_bytes;
+  return SCION_OK;
+}
+int scion_dtree_from_image(const char* layout, void* d_image, uint64_t bytes, int device, int adopt, scion_dtree** out) {
+  if (!d_image || !out || bytes < sizeof(ImageHeader)) return fail(SCION_ERR_ARG, "bad image");
+  CUDA_OK(cudaSetDevice(device));
+  auto* t = new scion_dtree();
+  t->device = device;
+  t->image = (uint8_t*)d_image;
+  t->owns_image = adopt != 0;
+  cudaError_t ce = cudaMemcpy(&t->header, d_image, sizeof(ImageHeader), cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) { t->owns_image = false; delete t; return fail(SCION_ERR_CUDA, cudaGetErrorString(ce)); }
+  if (t->header.magic != kImageMagic || t->header.total_bytes > bytes) { t->owns_image = false; delete t; return fail(SCION_ERR_ARG, "not a scion device image"); }
+  t->header.layout[sizeof(t->header.layout) - 1] = 0;
+  if (layout && strcmp(layout, t->header.layout) != 0) { t->owns_image = false; delete t; return fail(SCION_ERR_ARG, "image holds a different layout"); }
+  t->layout = scion::find_layout(t->header.layout);
+  if (!t->layout) { t->owns_image = false; delete t; return fail(SCION_ERR_ARG, "image names an unknown layout"); }
+  int rc = finish_dtree(t);
+  if (rc) { if (!adopt) t->owns_image = false; scion_dtree_free(t); return rc; }
+  *out = t;
+  return SCION_OK;
+}
+void scion_dtree_free(scion_dtree* t) {
+  if (!t) return;
+  cudaSetDevice(t->device);
+  for (int i = 0; i < 2; i++) {
+    if (t->streams[i]) { cudaStreamSynchronize(t->streams[i]); cudaStreamDestroy(t->streams[i]); }
+    if (t->h2d[i]) cudaFree(t->h2d[i]);
+    if (t->d2h[i]) cudaFree(t->d2h[i]);
+    if (t->d_status[i]) cudaFree(t->d_status[i]);
+  }
+  if (t->counters) cudaFree(t->counters);
+  if (t->image && t->owns_image) cudaFree(t->image);
+  delete t;
+}
+
+// ------------------------------------------------------------------ queries
+static int run_query(const scion_dtree* t, bool hit, const void* in, uint64_t n, void* out, uint32_t* status, scion_counters* counters, int variant, void* stream) {
+  if (!t || (!in && n) || (!out && n)) return fail(SCION_ERR_ARG, "null argument");
+  if (n == 0) return SCION_OK;
+  scion::launch_fn fn = hit ? t->kernels->closest_hit : t->kernels->closest_point;
+  if (!fn) return fail(SCION_ERR_ARG, "closest_point requires a binary layout (8-wide layouts have no CPQ, corpus.cpp:83)");
+  CUDA_OK(cudaSetDevice(t->device));
+  scion::LaunchArgs a;
+  a.view = t->view;
+  a.in = in;
+  a.n = n;
+  a.out = out;
+  a.status = status;
+  a.counters = counters;
+  a.next = take_counter(t);
+  a.stream = (cudaStream_t)stream;
+  a.variant = variant;
+  a.grid = 0;
+  CUDA_OK(cudaMemsetAsync(a.next, 0, sizeof(unsigned long long), a.stream));
+  CUDA_OK(fn(a));
+  g_launches.fetch_add(1);
+  return SCION_OK;
+}
+int scion_closest_hit(const scion_dtree* t, const scion_ray* d_rays, uint64_t n, scion_hit* d_hits, uint32_t* d_status, scion_counters* d_counters, int variant, void* stream) {
+  return run_query(t, true, d_rays, n, d_hits, d_status, d_counters, variant, stream);
+}
+int scion_closest_point(const scion_dtree* t, const float* d_points, uint64_t n, scion_cp* d_out, uint32_t* d_status, scion_counters* d_counters, int variant, void* stream) {
+  return run_query(t, false, d_points, n, d_out, d_status, d_counters, variant, stream);
+}
+
+// Host entry points: chunked, double-buffered over two streams so that the H2D copy of chunk
+// k+1 and the D2H copy of chunk k-1 overlap the traversal of chunk k.
+static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uint64_t n, void* h_out, uint32_t* h_status) {
+  if (!ct || (!h_in && n) || (!h_out && n)) return fail(SCION_ERR_ARG, "null argument");
+  scion_dtree* t = const_cast<scion_dtree*>(ct);
+  std::lock_guard<std::mutex> lock(t->host_mutex);
+  CUDA_OK(cudaSetDevice(t->device));
+  const uint64_t in_sz = hit ? sizeof(scion_ray) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
+  const uint64_t kChunk = 1ull << 22;
+  if (t->chunk == 0) {
+    for (int i = 0; i < 2; i++) {
+      CUDA_OK(cudaStreamCreateWithFlags(&t->streams[i], cudaStreamNonBlocking));
+      CUDA_OK(cudaMalloc(&t->h2d[i], kChunk * sizeof(scion_ray)));
+      CUDA_OK(cudaMalloc(&t->d2h[i], kChunk * sizeof(scion_cp)));
+      CUDA_OK(cudaMalloc(&t->d_status[i], kChunk * sizeof(uint32_t)));
+    }
+    t->chunk = kChunk;
+  }
+  int k = 0;
+  for (uint64_t off = 0; off < n; off += kChunk, k ^= 1) {
+    const uint64_t m = std::min(kChunk, n - off);
+    cudaStream_t s = t->streams[k];
+    CUDA_OK(cudaMemcpyAsync(t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s));
+    int rc = run_query(t, hit, t->h2d[k], m, t->d2h[k], h_status ? t->d_status[k] : nullptr, nullptr, 0, s);
+    if (rc) return rc;
+    CUDA_OK(cudaMemcpyAsync((uint8_t*)h_out + off * out_sz, t->d2h[k], m * out_sz, cudaMemcpyDeviceToHost, s));
+    if (h_status) CUDA_OK(cudaMemcpyAsync(h_status + off, t->d_status[k], m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_OK(cudaStreamSynchronize(t->streams[0]));
+  CUDA_OK(cudaStreamSynchronize(t->streams[1]));
+  return SCION_OK;
+}
+int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64_t n, scion_hit* h_hits, uint32_t* h_status) {
+  return run_query_host(t, true, h_rays, n, h_hits, h_status);
+}
+int scion_closest_point_host(const scion_dtree* t, const float* h_points, uint64_t n, scion_cp* h_out, uint32_t* h_status) {
+  return run_query_host(t, false, h_points, n, h_out, h_status);
+}
+
+// ------------------------------------------------------------------ generators
+static scion::CameraBasis basis_of(const scion_camera& c) {
+  scion::CameraBasis b;
+  double f[3], r[3], u[3], up[3] = {c.up[0], c.up[1], c.up[2]};
+  for (int a = 0; a < 3; a++) f[a] = (double)c.target[a] - c.eye[a];
+  double fl = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+  for (int a = 0; a < 3; a++) f[a] /= fl;
+  r[0] = f[1] * up[2] - f[2] * up[1]; r[1] = f[2] * up[0] - f[0] * up[2]; r[2] = f[0] * up[1] - f[1] * up[0];
+  double rl = std::sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  for (int a = 0; a < 3; a++) r[a] /= rl;
+  u[0] = r[1] * f[2] - r[2] * f[1]; u[1] = r[2] * f[0] - r[0] * f[2]; u[2] = r[0] * f[1] - r[1] * f[0];
+  for (int a = 0; a < 3; a++) { b.eye[a] = c.eye[a]; b.fwd[a] = (float)f[a]; b.right[a] = (float)r[a]; b.up[a] = (float)u[a]; }
+  double th = std::tan(0.5 * c.fov_y_deg * 3.14159265358979323846 / 180.0);
+  b.tan_half_y = (float)th;
+  b.tan_half_x = (float)(th * (double)c.width / (double)c.height);
+  b.width = c.width;
+  b.height = c.height;
+  return b;
+}
+void scion_camera_default(const float lo[3], const float hi[3], int look_down_y, uint32_t w, uint32_t h, scion_camera* out) {
+  float c[3], e[3];
+  for (int a = 0; a < 3; a++) { c[a] = 0.5f * (lo[a] + hi[a]); e[a] = hi[a] - lo[a]; }
+  float diag = std::sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+  for (int a = 0; a < 3; a++) { out->target[a] = c[a]; out->eye[a] = c[a]; }
+  if (look_down_y) {  // terrains: above the +y face, looking down at a slant
+    out->eye[1] = hi[1] + 0.9f * diag;
+    out->eye[2] = hi[2] + 0.35f * diag;
+    out->up[0] = 0; out->up[1] = 1; out->up[2] = 0;
+  } else {  // outside the +z face
+    out->eye[2] = hi[2] + 1.1f * diag;
+    out->eye[0] = c[0] + 0.07f * diag;
+    out->eye[1] = c[1] + 0.05f * diag;
+    out->up[0] = 0; out->up[1] = 1; out->up[2] = 0;
+  }
+  out->fov_y_deg = 42.0f;
+  out->width = w;
+  out->height = h;
+}
+
+}  // extern "C"
+
+namespace scion {
+__global__ void gen_primary_kernel(CameraBasis cam, uint64_t first, uint64_t n, scion_ray* rays) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rays[i] = primary_ray(cam, first + i);
+}
+__global__ void gen_secondary_kernel(const float* tris, uint64_t ntris, uint64_t seed, uint64_t first, uint64_t n, scion_ray* rays) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rays[i] = secondary_ray(tris, ntris, seed, first + i);
+}
+__global__ void gen_points_kernel(float3 lo, float3 hi, uint64_t seed, uint64_t first, uint64_t n, float* pts) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z}, o[3];
+    query_point(l, h, seed, first + i, o);
+    pts[3 * i] = o[0]; pts[3 * i + 1] = o[1]; pts[3 * i + 2] = o[2];
+  }
+}
+}  // namespace scion
+
+extern "C" {
+
+int scion_gen_primary(const scion_camera* cam, uint64_t first, uint64_t n, scion_ray* d_rays, void* stream) {
+  if (!cam || (!d_rays && n)) return fail(SCION_ERR_ARG, "null argument");
+  if (n == 0) return SCION_OK;
+  scion::gen_primary_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(basis_of(*cam), first, n, d_rays);
+  CUDA_OK(cudaGetLastError());
+  g_launches.fetch_add(1);
+  return SCION_OK;
+}
+int scion_gen_secondary(const scion_dtree* t, uint64_t seed, uint64_t first, uint64_t n, scion_ray* d_rays, void* stream) {
+  if (!t || (!d_rays && n)) return fail(SCION_ERR_ARG, "null argument");
+  if (n == 0) return SCION_OK;
+  CUDA_OK(cudaSetDevice(t->device));
+  // buffer 0 is the primitives array in every layout of the registry (Triangle stride 36, 4-byte aligned)
+  scion::gen_secondary_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>((const float*)t->view.buf[0], t->header.nprims, seed, first, n, d_rays);
+  CUDA_OK(cudaGetLastError());
+  g_launches.fetch_add(1);
+  return SCION_OK;
+}
+int scion_gen_points(const float lo[3], const float hi[3], uint64_t seed, uint64_t first, uint64_t n, float* d_points, void* stream) {
+  if (!lo || !hi || (!d_points && n)) return fail(SCION_ERR_ARG, "null argument");
+  if (n == 0) return SCION_OK;
+  scion::gen_points_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(make_float3(lo[0], lo[1], lo[2]), make_float3(hi[0], hi[1], hi[2]), seed, first, n, d_points);
+  CUDA_OK(cudaGetLastError());
+  g_launches.fetch_add(1);
+  return SCION_OK;
+}
+int scion_gen_primary_host(const scion_camera* cam, uint64_t first, uint64_t n, scion_ray* h_rays) {
+  if (!cam || (!h_rays && n)) return fail(SCION_ERR_ARG, "null argument");
+  scion::CameraBasis b = basis_of(*cam);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)n; i++) h_rays[i] = scion::primary_ray(b, first + (uint64_t)i);
+  return SCION_OK;
+}
+int scion_gen_secondary_host(const float* tris9, uint64_t ntris, uint64_t seed, uint64_t first, uint64_t n, scion_ray* h_rays) {
+  if (!tris9 || !ntris || (!h_rays && n)) return fail(SCION_ERR_ARG, "null argument");
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)n; i++) h_rays[i] = scion::secondary_ray(tris9, ntris, seed, first + (uint64_t)i);
+  return SCION_OK;
+}
+int scion_gen_points_host(const float lo[3], const float hi[3], uint64_t seed, uint64_t first, uint64_t n, float* h_points) {
+  if (!lo || !hi || (!h_points && n)) return fail(SCION_ERR_ARG, "null argument");
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)n; i++) scion::query_point(lo, hi, seed, first + (uint64_t)i, h_points + 3 * i);
+  return SCION_OK;
+}
+
+void scion_partition(uint64_t n, int rank, int nranks, uint64_t* first, uint64_t* count) {
+  if (nranks < 1) nranks = 1;
+  uint64_t a = n * (uint64_t)rank / (uint64_t)nranks, b = n * (uint64_t)(rank + 1) / (uint64_t)nranks;
+  if (first) *first = a;
+  if (count) *count = b - a;
+}
+
+}  // extern "C"

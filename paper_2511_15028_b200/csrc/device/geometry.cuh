@@ -1,0 +1,169 @@
+// Device restatement of the DSL standard library the traversals call
+// (/root/reference/proj/corpus/lib/geometry.scion, corpus/lib/dop.scion), strict binary32:
+// compiled with -fmad=false -prec-div=true -prec-sqrt=true -ftz=false, no fast-math, so that
+// every + - * / is a separately rounded IEEE operation exactly as in the CPU oracle
+// (reference flag -ffp-contract=off, proj/CMakeLists.txt:13-15).
+#pragma once
+#include "scion_rt.cuh"
+
+namespace scion {
+
+struct RayCtx {
+  float ox, oy, oz, tmax;
+  float dx, dy, dz;
+  float rdx, rdy, rdz;  // 1.0 / direction, hoisted (pure, geometry.scion:13)
+  bool nx, ny, nz;      // direction < 0.0 per axis (-0.0 is not negative)
+};
+
+SCION_DEV RayCtx make_ray(float ox, float oy, float oz, float tmax, float dx, float dy, float dz) {
+  RayCtx r;
+  r.ox = ox; r.oy = oy; r.oz = oz; r.tmax = tmax;
+  r.dx = dx; r.dy = dy; r.dz = dz;
+  r.rdx = 1.0f / dx; r.rdy = 1.0f / dy; r.rdz = 1.0f / dz;
+  r.nx = dx < 0.0f; r.ny = dy < 0.0f; r.nz = dz < 0.0f;
+  return r;
+}
+
+// intersectsp_ray_aabb, geometry.scion:12-22.  Returns `some`; t_near/t_far are the interval.
+SCION_DEV bool ray_aabb(const RayCtx& r, const f32x3& lo, const f32x3& hi, float& t_near, float& t_far) {
+  const float nx = r.nx ? hi.x : lo.x, fx = r.nx ? lo.x : hi.x;
+  const float ny = r.ny ? hi.y : lo.y, fy = r.ny ? lo.y : hi.y;
+  const float nz = r.nz ? hi.z : lo.z, fz = r.nz ? lo.z : hi.z;
+  const float t_nx = (nx - r.ox) * r.rdx, t_fx = (fx - r.ox) * r.rdx;
+  const float t_ny = (ny - r.oy) * r.rdy, t_fy = (fy - r.oy) * r.rdy;
+  const float t_nz = (nz - r.oz) * r.rdz, t_fz = (fz - r.oz) * r.rdz;
+  t_near = fmaxf(0.0f, fmaxf(t_nx, fmaxf(t_ny, t_nz)));
+  t_far = fminf(r.tmax, fminf(t_fx, fminf(t_fy, t_fz)));
+  return t_near <= t_far;
+}
+// intersects(Ray, AABB) geometry.scion:61-63 given the interval
+SCION_DEV bool interval_intersects(const RayCtx& r, bool some, float t_near, float t_far) {
+  return some && (t_near < r.tmax) && (t_far > 0.0f);
+}
+
+// intersectsp_ray_tri_mt, geometry.scion:25-38 (sign-masked Moeller-Trumbore); returns hit and t
+SCION_DEV bool ray_tri_mt(const RayCtx& ray, const float* p, float& t_out) {
+  const f32x3 p0{p[0], p[1], p[2]}, p1{p[3], p[4], p[5]}, p2{p[6], p[7], p[8]};
+  const f32x3 e1 = p0 - p1, e2 = p2 - p0;
+  const f32x3 ng = cross(e2, e1);
+  const f32x3 c = p0 - f32x3{ray.ox, ray.oy, ray.oz};
+  const f32x3 d{ray.dx, ray.dy, ray.dz};
+  const f32x3 r = cross(c, d);
+  const float D = dot(ng, d);
+  if (D == 0.0f) return false;
+  const float abs_D = scion::abs(D);
+  const uint32_t sgn_D = f2u(D) & 2147483648u;
+  const float u_raw = u2f(f2u(dot(r, e2)) ^ sgn_D);
+  const float v_raw = u2f(f2u(dot(r, e1)) ^ sgn_D);
+  if (!(u_raw >= 0.0f && v_raw >= 0.0f && u_raw + v_raw <= abs_D)) return false;
+  const float t_raw = u2f(f2u(dot(ng, c)) ^ sgn_D);
+  if (!(abs_D * 0.0f < t_raw && t_raw <= abs_D * ray.tmax)) return false;
+  const float inv_abs_D = 1.0f / abs_D;
+  t_out = t_raw * inv_abs_D;
+  return true;
+}
+
+// slab_hit, dop.scion:5-17
+SCION_DEV bool slab_hit(float o, float d, float lo, float hi, float& tn, float& tf) {
+  if (d == 0.0f) return !(o < lo || o > hi);
+  const float inv = 1.0f / d;
+  const float ta = (lo - o) * inv, tb = (hi - o) * inv;
+  const float t0 = fminf(ta, tb), t1 = fmaxf(ta, tb);
+  const float ntn = fmaxf(tn, t0), ntf = fminf(tf, t1);
+  if (ntn <= ntf) { tn = ntn; tf = ntf; return true; }
+  return false;
+}
+// the four diagonal slabs of dop_interval, dop.scion:22-43, refining an AABB interval in place
+SCION_DEV bool dop_diagonals(const RayCtx& r, const f32x4& lo2, const f32x4& hi2, float& tn, float& tf) {
+  const float o0 = r.ox + r.oy + r.oz, d0 = r.dx + r.dy + r.dz;
+  const float o1 = r.ox + r.oy - r.oz, d1 = r.dx + r.dy - r.dz;
+  const float o2 = r.ox - r.oy + r.oz, d2 = r.dx - r.dy + r.dz;
+  const float o3 = r.ox - r.oy - r.oz, d3 = r.dx - r.dy - r.dz;
+  if (!slab_hit(o0, d0, lo2.x, hi2.x, tn, tf)) return false;
+  if (!slab_hit(o1, d1, lo2.y, hi2.y, tn, tf)) return false;
+  if (!slab_hit(o2, d2, lo2.z, hi2.z, tn, tf)) return false;
+  return slab_hit(o3, d3, lo2.w, hi2.w, tn, tf);
+}
+
+// square_distance_point_aabb, geometry.scion:105-110
+SCION_DEV float sqdist_point_aabb(const f32x3& v, const f32x3& lo, const f32x3& hi) {
+  const f32x3 dl = lo - v, dh = v - hi;
+  const f32x3 sq_low = dl * dl, sq_high = dh * dh;
+  const f32x3 low{v.x < lo.x ? sq_low.x : 0.0f, v.y < lo.y ? sq_low.y : 0.0f, v.z < lo.z ? sq_low.z : 0.0f};
+  const f32x3 high{v.x > hi.x ? sq_high.x : 0.0f, v.y > hi.y ? sq_high.y : 0.0f, v.z > hi.z ? sq_high.z : 0.0f};
+  return sum(low + high);
+}
+// distmax, geometry.scion:116-118
+SCION_DEV float distmax_point_aabb(const f32x3& p, const f32x3& lo, const f32x3& hi) {
+  const f32x3 u = lo - p, v = p - hi;
+  const f32x3 d{fminf(u.x, v.x), fminf(u.y, v.y), fminf(u.z, v.z)};
+  return dot(d, d);
+}
+// distmin_dop_point, dop.scion:61-77
+SCION_DEV float distmin_dop_point(const f32x3& p, const f32x3& lo1, const f32x3& hi1, const f32x4& lo2, const f32x4& hi2) {
+  const float base = sqdist_point_aabb(p, lo1, hi1);
+  const float s0 = p.x + p.y + p.z, s1 = p.x + p.y - p.z, s2 = p.x - p.y + p.z, s3 = p.x - p.y - p.z;
+  const float v0 = fmaxf(lo2.x - s0, fmaxf(s0 - hi2.x, 0.0f));
+  const float v1 = fmaxf(lo2.y - s1, fmaxf(s1 - hi2.y, 0.0f));
+  const float v2 = fmaxf(lo2.z - s2, fmaxf(s2 - hi2.z, 0.0f));
+  const float v3 = fmaxf(lo2.w - s3, fmaxf(s3 - hi2.w, 0.0f));
+  const float third = 1.0f / 3.0f;
+  const float d0 = v0 * v0 * third, d1 = v1 * v1 * third, d2 = v2 * v2 * third, d3 = v3 * v3 * third;
+  return fmaxf(base, fmaxf(fmaxf(d0, d1), fmaxf(d2, d3)));
+}
+// distmin_point_triangle, geometry.scion:76-100 (closest point only; barycentrics are unused by cpq)
+SCION_DEV f32x3 closest_point_triangle(const f32x3& p, const float* t) {
+  const f32x3 a{t[0], t[1], t[2]}, b{t[3], t[4], t[5]}, c{t[6], t[7], t[8]};
+  const f32x3 ab = b - a, ac = c - a, ap = p - a;
+  const float d1 = dot(ab, ap), d2 = dot(ac, ap);
+  if (d1 <= 0.0f && d2 <= 0.0f) return a;
+  const f32x3 bp = p - b;
+  const float d3 = dot(ab, bp), d4 = dot(ac, bp);
+  if (d3 >= 0.0f && d4 <= d3) return b;
+  const float vc = d1 * d4 - d3 * d2;
+  if (vc <= 0.0f && d1 >= 0.0f && d3 <= 0.0f) {
+    const float v0 = d1 / (d1 - d3);
+    return a + ab * v0;  // a + v0 * ab: multiplication commutes bitwise
+  }
+  const f32x3 cp = p - c;
+  const float d5 = dot(ab, cp), d6 = dot(ac, cp);
+  if (d6 >= 0.0f && d5 <= d6) return c;
+  const float vb = d5 * d2 - d1 * d6;
+  if (vb <= 0.0f && d2 >= 0.0f && d6 <= 0.0f) {
+    const float w0 = d2 / (d2 - d6);
+    return a + ac * w0;
+  }
+  const float va = d3 * d6 - d5 * d4;
+  if (va <= 0.0f && (d4 - d3) >= 0.0f && (d5 - d6) >= 0.0f) {
+    const float w1 = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+    return b + (c - b) * w1;
+  }
+  const float D = 1.0f / (va + vb + vc);
+  const float v = vb * D, w = vc * D;
+  return (a + ab * v) + ac * w;
+}
+
+// Triangle = 3 x f32x3 = 36 B at a 4-byte-aligned address (stride 36, plan.cpp:195-210).  One
+// triangle is fetched as the three aligned 16-byte words that cover it — 3 read-only vector
+// loads instead of nine 4-byte ones — and re-aligned in registers.  Device buffers carry 16
+// bytes of slack so the covering read of the last triangle stays inside the allocation.
+SCION_DEV void load_triangle36(const uint8_t* prims, uint64_t index, float (&v)[9]) {
+#if defined(__CUDA_ARCH__)
+  const uint64_t addr = (uint64_t)prims + index * 36ull;
+  const uint4* q = reinterpret_cast<const uint4*>(addr & ~15ull);
+  const uint32_t s = (uint32_t)(addr >> 2) & 3u;
+  const uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+  const bool s1 = (s & 1u) != 0u, s2 = (s & 2u) != 0u;
+#pragma unroll
+  for (int j = 0; j < 9; j++) {
+    const uint32_t lo = s1 ? w[j + 1] : w[j];
+    const uint32_t hi = s1 ? w[j + 3] : w[j + 2];
+    v[j] = u2f(s2 ? hi : lo);
+  }
+#else
+  memcpy(v, prims + index * 36ull, 36);
+#endif
+}
+
+}  // namespace scion

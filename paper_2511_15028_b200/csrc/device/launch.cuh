@@ -1,0 +1,37 @@
+// Kernel registry: one KernelEntry per layout, filled by the per-layout instantiation units
+// (build/inst_<layout>.cu, stamped from device/inst.cu.in by the Makefile).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "scion_b200.h"
+#include "scion_rt.cuh"
+
+namespace scion {
+
+struct LaunchArgs {
+  TreeView view;
+  const void* in;     // scion_ray* (closest_hit) or float* xyz (closest_point), device
+  uint64_t n;
+  void* out;          // scion_hit* or scion_cp*, device
+  uint32_t* status;   // nullable
+  scion_counters* counters;  // nullable => the counter-free kernel is launched
+  unsigned long long* next;  // work-fetch counter, zeroed on the stream before launch
+  cudaStream_t stream;
+  int variant;
+  int grid;           // 0 => occupancy * SM count
+};
+
+typedef cudaError_t (*launch_fn)(const LaunchArgs&);
+typedef cudaError_t (*occupancy_fn)(int* blocks_per_sm, int* regs, size_t* smem);
+
+struct KernelEntry {
+  const char* layout;
+  launch_fn closest_hit;
+  launch_fn closest_point;  // null for 8-wide layouts (corpus.cpp:83)
+  occupancy_fn hit_occupancy;
+};
+
+const KernelEntry* find_kernels(const char* layout);
+int device_sm_count();
+
+}  // namespace scion

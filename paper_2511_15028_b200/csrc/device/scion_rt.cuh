@@ -104,7 +104,6 @@ struct Slice {  // T[a : b] over a global array: element indices [begin, end)
 SCION_HOSTDEV Slice make_slice(uint64_t a, uint64_t b) { return Slice{a, b}; }
 
 // --------------------------------------------------------------------------- scalar intrinsics
-SCION_HOSTDEV float inf() { return __builtin_inff(); }
 SCION_HOSTDEV uint32_t f2u(float f) {
 #if defined(__CUDA_ARCH__)
   return __float_as_uint(f);
@@ -119,6 +118,7 @@ SCION_HOSTDEV float u2f(uint32_t u) {
   float f; memcpy(&f, &u, 4); return f;
 #endif
 }
+SCION_HOSTDEV float inf() { return u2f(0x7f800000u); }
 
 // min/max: IEEE minNum/maxNum == C fminf/fmaxf == CUDA fminf/fmaxf
 SCION_HOSTDEV float min(float a, float b) { return fminf(a, b); }

@@ -20,6 +20,14 @@
 
 namespace scion {
 
+SCION_HD float rng_inf() {
+#if defined(__CUDA_ARCH__)
+  return __int_as_float(0x7f800000);
+#else
+  return __builtin_inff();
+#endif
+}
+
 SCION_HD uint64_t splitmix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ull;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -96,7 +104,7 @@ SCION_HD scion_ray primary_ray(const CameraBasis& c, uint64_t index) {
   scion_ray r;
   r.ox = c.eye[0]; r.oy = c.eye[1]; r.oz = c.eye[2];
   r.dx = div_rn(d[0], len); r.dy = div_rn(d[1], len); r.dz = div_rn(d[2], len);
-  r.tmax = __builtin_inff();
+  r.tmax = rng_inf();
   r.pad = 0.0f;
   return r;
 }
@@ -138,7 +146,7 @@ SCION_HD scion_ray secondary_ray(const float* tris9, uint64_t ntris, uint64_t se
   scion_ray r;
   r.ox = add_rn(o[0], mul_rn(eps, n[0])); r.oy = add_rn(o[1], mul_rn(eps, n[1])); r.oz = add_rn(o[2], mul_rn(eps, n[2]));
   r.dx = d[0]; r.dy = d[1]; r.dz = d[2];
-  r.tmax = __builtin_inff();
+  r.tmax = rng_inf();
   r.pad = 0.0f;
   return r;
 }

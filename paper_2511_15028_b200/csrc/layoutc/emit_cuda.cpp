@@ -419,9 +419,11 @@ struct Emitter {
     if (arm_level && variant) {
       assign_fields(variant->fields);
       for (auto& f : variant->fields)
-        if (!assigned.count(f.name)) throw LayoutError("layout " + plan.layout_name + ": field '" + f.name + "' of variant " + variant->name + " is not defined");
+        if (!assigned.count(f.name) && !(mode == Mode::Hot && cold_names.count(f.name)))
+          throw LayoutError("layout " + plan.layout_name + ": field '" + f.name + "' of variant " + variant->name + " is not defined");
       for (auto& f : plan.adt->fields)
-        if (!assigned.count(f.name)) throw LayoutError("layout " + plan.layout_name + ": field '" + f.name + "' is not defined for variant " + variant->name);
+        if (!assigned.count(f.name) && !(mode == Mode::Hot && cold_names.count(f.name)))
+          throw LayoutError("layout " + plan.layout_name + ": field '" + f.name + "' is not defined for variant " + variant->name);
     }
     // 4. splits
     for (auto& m : ms) {

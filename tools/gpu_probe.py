@@ -1,0 +1,88 @@
+"""Scratch GPU probe: parity of every layout vs the oracle on a small scene + quick timings."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2511_15028_b200 as sb
+from tests.oracle_lib import Oracle
+
+orc = Oracle()
+dev = "cuda:0"
+def dbuf(nbytes): return torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+def parity(G, W, nsec):
+    scene = sb.Scene.terrain(G, seed=3)
+    lt = scene.build_sah(32, 4).collapse8()
+    lo, hi = scene.bounds()
+    cam = sb.default_camera(lo, hi, True, W, W)
+    n = W * W
+    rays_p = sb.gen_primary_host(cam, 0, n)
+    rays_s = sb.gen_secondary_host(lt.triangles(), 11, 0, nsec)
+    rays = np.concatenate([rays_p, rays_s])
+    pts = sb.gen_points_host(lo - 0.2, hi + 0.2, 5, 0, 8192)
+    n = rays.shape[0]
+    d_rays = torch.from_numpy(rays.view(np.uint8).reshape(-1)).to(dev)
+    d_pts = torch.from_numpy(pts.reshape(-1)).to(dev)
+    ok = True
+    for l in sb.layouts():
+        name = l["name"]
+        pt = lt.encode(name)
+        tb = orc.tree_bytes(pt)
+        dt = pt.upload(0)
+        d_hits, d_st, d_ctr = dbuf(n * 8), dbuf(n * 4), dbuf(n * 16)
+        dt.closest_hit(d_rays.data_ptr(), n, d_hits.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+        torch.cuda.synchronize()
+        got = d_hits.cpu().numpy().view(sb.HIT_DTYPE); st = d_st.cpu().numpy().view(np.uint32); ctr = d_ctr.cpu().numpy().view(sb.COUNTERS_DTYPE)
+        want, wst, wctr = orc.closest_hit(tb, rays, counters=True)
+        bad_p = int((got["prim"] != want["prim"]).sum()); bad_t = int((got["t"].view(np.uint32) != want["t"].view(np.uint32)).sum())
+        bad_c = int((ctr != wctr).sum()); bad_s = int((st != wst).sum())
+        # counter-free kernel must agree too
+        d_hits2 = dbuf(n * 8)
+        dt.closest_hit(d_rays.data_ptr(), n, d_hits2.data_ptr())
+        torch.cuda.synchronize()
+        bad_nc = int((d_hits2.cpu().numpy().view(np.uint32) != d_hits.cpu().numpy().view(np.uint32)).sum())
+        msg = f"{name:14s} chrt: prim_mismatch {bad_p} t_mismatch {bad_t} counters {bad_c} status {bad_s} nocount {bad_nc} hits {(got['prim']!=sb.MISS_PRIM).mean():.3f} visits/ray {ctr['node_visits'].mean():.1f} tris/ray {ctr['prim_tests'].mean():.1f} maxstack {ctr['max_stack'].max()}"
+        if l["has_cpq"]:
+            m = pts.shape[0]
+            d_out, d_st2, d_ctr2 = dbuf(m * 20), dbuf(m * 4), dbuf(m * 16)
+            dt.closest_point(d_pts.data_ptr(), m, d_out.data_ptr(), d_st2.data_ptr(), d_ctr2.data_ptr())
+            torch.cuda.synchronize()
+            gc = d_out.cpu().numpy().view(sb.CP_DTYPE); cc = d_ctr2.cpu().numpy().view(sb.COUNTERS_DTYPE)
+            wc, wcs, wcc = orc.closest_point(tb, pts, counters=True)
+            badc = int((gc.view(np.uint8).reshape(m, 20) != wc.view(np.uint8).reshape(m, 20)).any(axis=1).sum())
+            msg += f" | cpq: mismatch {badc} counters {int((cc != wcc).sum())} visits {cc['node_visits'].mean():.1f}"
+            ok &= badc == 0
+        print(msg, flush=True)
+        ok &= (bad_p == 0 and bad_t == 0 and bad_c == 0 and bad_s == 0 and bad_nc == 0)
+        dt.free()
+    return ok
+
+def timing(G, nrays, layouts):
+    t0 = time.time(); scene = sb.Scene.terrain(G, seed=3); t1 = time.time()
+    lt = scene.build_sah(32, 4).collapse8(); t2 = time.time()
+    print(f"scene {scene.ntris} tris gen {t1-t0:.2f}s build {t2-t1:.2f}s nodes {lt.nnodes} depth {lt.depth}", flush=True)
+    lo, hi = scene.bounds()
+    cam = sb.default_camera(lo, hi, True, 4096, 4096)
+    d_rays = dbuf(nrays * 32); d_hits = dbuf(nrays * 8)
+    for name in layouts:
+        t3 = time.time(); pt = lt.encode(name); t4 = time.time()
+        dt = pt.upload(0)
+        for kind in ("primary", "secondary"):
+            if kind == "primary": sb.gen_primary(cam, 0, nrays, d_rays.data_ptr())
+            else: dt.gen_secondary(77, 0, nrays, d_rays.data_ptr())
+            torch.cuda.synchronize()
+            for _ in range(2): dt.closest_hit(d_rays.data_ptr(), nrays, d_hits.data_ptr())
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3): dt.closest_hit(d_rays.data_ptr(), nrays, d_hits.data_ptr())
+            e1.record(); torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 3
+            print(f"  {name:14s} {kind:9s} {nrays/ms/1e3:9.1f} Mrays/s  ({ms:.2f} ms)  encode {t4-t3:.2f}s bytes/prim {pt.node_bytes/lt.nprims:.1f}", flush=True)
+        dt.free()
+
+if __name__ == "__main__":
+    print(torch.cuda.get_device_name(0))
+    ok = parity(40, 128, 8192)
+    print("PARITY", "OK" if ok else "FAILED", flush=True)
+    if "--time" in sys.argv:
+        timing(708, 1 << 24, ["pbrt", "pbrt-soa", "pbrt-q16", "sg-eq", "sg-eq-align16", "dop14", "bvh8", "bvh8-q8-ci", "bvh8-q16-ci"])
