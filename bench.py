@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 traversal backend.
+
+A "step" is one pass of the hot path (closest_hit / closest_point kernel) over the rank's
+contiguous slice of one batch of synthetic queries.  Default workload = BASELINE.json configs[4]
+("c5"): 2^28 primary + secondary rays on a 9,999,392-triangle terrain, tree replicated with one
+ncclBroadcast of the packed device image, rays partitioned contiguously over the ranks (total
+work fixed => "strong" scaling).  `value` is whole-job Mrays/s with the rays resident in HBM;
+`e2e` is the same metric through the host-buffer C-ABI call (pinned host rays in, host hits out,
+copies inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c1|c3|c4|c5] [--layout pbrt-q16] [--sweep a,b,c] [--scale f]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--layout", default="pbrt-q16", help="headline layout (the paper's Pareto-optimal layout)")
+    ap.add_argument("--sweep", default="pbrt,pbrt-soa,sg-eq,bvh8,bvh8-q8-ci", help="extra layouts reported in `layouts` (N=1 only); '' disables")
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink query counts (debug)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clocks + throttle reasons during the timed region (pynvml; nvidia-smi fallback)."""
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons, self.max_mhz = index, [], set(), None
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _loop(self):
+        nv = self.nv
+        names = {}
+        if nv:
+            for k in dir(nv):
+                if k.startswith("nvmlClocksEventReason") or k.startswith("nvmlClocksThrottleReason"):
+                    v = getattr(nv, k)
+                    if isinstance(v, int) and v not in (0,):
+                        names[v] = k.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", "")
+        while not self._stop.is_set():
+            try:
+                if nv:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                    try:
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    except Exception:
+                        r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                    for bit, nm in names.items():
+                        if r & bit and nm not in ("GpuIdle", "None", "All"):
+                            self.reasons.add(nm)
+                else:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout.strip().split(",")
+                    self.samples.append(int(out[0]))
+                    self.max_mhz = int(out[1])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def start(self):
+        self._thr = threading.Thread(target=self._loop, daemon=True)
+        self._thr.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._thr:
+            self._thr.join(timeout=2)
+        s = sorted(self.samples)
+        return {"sm_mhz": (s[len(s) // 2] if s else None), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+def spread_sample(total, n_sample, chunks=64):
+    """`chunks` equal contiguous pieces spread evenly over [0,total) — a representative bounded sample."""
+    n_sample = min(n_sample, total)
+    chunks = max(1, min(chunks, n_sample))
+    per = n_sample // chunks
+    return [(int(i * (total / chunks)), per) for i in range(chunks)]
+
+
+# ----------------------------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation of the path.  The reference ships no
+# executor (src/interp.cpp is a placeholder), so this is the oracle port (oracle/liboracle.so:
+# strict-f32 restatement of corpus/alg/*.scion over the same encoded bytes), all host threads,
+# OpenMP schedule(dynamic,64).
+# ----------------------------------------------------------------------------------------------
+def cpu_run(orc, tb, wl, tris, lo, hi, ranges, repeats=1):
+    import paper_2511_15028_b200.workloads as W
+    q = np.concatenate([W.generate_host(wl, tris, lo, hi, a, c) for a, c in ranges])
+    best = None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        if wl.algorithm == "chrt":
+            orc.closest_hit(tb, q)
+        else:
+            orc.closest_point(tb, q)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return len(q), best
+
+
+def build_host_side(args, wl_name):
+    import paper_2511_15028_b200 as sb
+    import paper_2511_15028_b200.workloads as W
+    wl0 = W.workload(wl_name, scale=args.scale)
+    t0 = time.time()
+    scene = W.make_scene(wl0)
+    lo, hi = scene.bounds()
+    ltree = scene.build_sah(32, 4)
+    ltree.collapse8()
+    build_s = time.time() - t0
+    wl = W.workload(wl_name, lo, hi, scale=args.scale)
+    return sb, W, wl, scene, ltree, lo, hi, build_s
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import __graft_entry__ as g
+    g.build()
+    from tests.oracle_lib import Oracle
+    sb, W, wl, scene, ltree, lo, hi, build_s = build_host_side(args, args.workload)
+    orc = Oracle()
+    pt = ltree.encode(args.layout)
+    tb = orc.tree_bytes(pt)
+    tris = ltree.triangles()
+    cores = os.cpu_count() or 1
+    # size the per-step sample so that (warmup + steps) steps end within a few minutes
+    n0, t = cpu_run(orc, tb, wl, tris, lo, hi, spread_sample(wl.total, 1 << 18))
+    rate = n0 / t
+    budget = min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup))
+    n_step = int(min(wl.total, max(1 << 18, rate * budget)))
+    ranges = spread_sample(wl.total, n_step)
+    for _ in range(args.warmup):
+        cpu_run(orc, tb, wl, tris, lo, hi, ranges)
+    times = []
+    nq = 0
+    for _ in range(args.steps):
+        nq, t = cpu_run(orc, tb, wl, tris, lo, hi, ranges)
+        times.append(t)
+    t_step = sum(times) / len(times)
+    val = nq / t_step / 1e6
+    unit = "Mrays/s" if wl.algorithm == "chrt" else "Mqueries/s"
+    sample = f"{nq} queries per step = 64 contiguous chunks spread evenly over the {wl.total}-query workload, layout {args.layout}"
+    line = {"impl": "reference", "metric": f"{unit} ({args.layout}, {wl.name})", "value": val, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": f"{wl.name}: {wl.description}", "layout": args.layout, "queries_per_step": nq},
+            "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}, "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device: the B200 backend has no CPU fallback (use --impl reference for the CPU arm)")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import __graft_entry__ as g
+    if rank == 0:
+        g.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2511_15028_b200 as sb
+    import paper_2511_15028_b200.workloads as W
+
+    # ---- host side (rank 0 builds; bounds are broadcast so every rank derives the same cameras)
+    bounds = torch.zeros(6, dtype=torch.float64, device=dev)
+    ltree = None
+    build_s = 0.0
+    if rank == 0:
+        _, _, wl, scene, ltree, lo, hi, build_s = build_host_side(args, args.workload)
+        bounds = torch.tensor(list(lo) + list(hi), dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.broadcast(bounds, 0)
+    b = bounds.cpu().numpy().astype(np.float32)
+    lo, hi = b[:3], b[3:]
+    wl = W.workload(args.workload, lo, hi, scale=args.scale)
+    unit = "Mrays/s" if wl.algorithm == "chrt" else "Mqueries/s"
+    q_bytes, r_bytes = (32, 8) if wl.algorithm == "chrt" else (12, 20)
+    first, count = sb.partition(wl.total, rank, world)
+
+    def replicate(layout):
+        """rank 0 encodes + uploads into a torch tensor; one ncclBroadcast replicates the image."""
+        nbytes = torch.zeros(1, dtype=torch.int64, device=dev)
+        pt = None
+        if rank == 0:
+            t0 = time.time()
+            pt = ltree.encode(layout)
+            nbytes[0] = pt.image_bytes
+            enc_s = time.time() - t0
+        if world > 1:
+            dist.broadcast(nbytes, 0)
+        img = torch.empty(int(nbytes.item()) + 256, dtype=torch.uint8, device=dev)
+        off = (-img.data_ptr()) % 256
+        ptr = img.data_ptr() + off
+        tb0 = time.time()
+        if rank == 0:
+            dt = pt.upload_into(local_rank, ptr, int(nbytes.item()))
+        if world > 1:
+            dist.broadcast(img[off:off + int(nbytes.item())], 0)
+            torch.cuda.synchronize()
+        if rank != 0:
+            dt = sb.DeviceTree.from_image(ptr, int(nbytes.item()), local_rank, layout)
+        bcast_s = time.time() - tb0
+        return dt, img, pt, bcast_s
+
+    d_q = torch.empty(count * q_bytes, dtype=torch.uint8, device=dev)
+    d_r = torch.empty(count * r_bytes, dtype=torch.uint8, device=dev)
+    d_st = torch.empty(count, dtype=torch.int32, device=dev)
+
+    def run_step(dt):
+        if wl.algorithm == "chrt":
+            dt.closest_hit(d_q.data_ptr(), count, d_r.data_ptr())
+        else:
+            dt.closest_point(d_q.data_ptr(), count, d_r.data_ptr())
+
+    def timed(dt, steps, warmup, sampler=None):
+        for _ in range(warmup):
+            run_step(dt)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = sb.kernel_launches()
+        e0.record()  # the launches go to torch's current stream handle 0 == legacy default stream; events on the same stream
+        for _ in range(steps):
+            run_step(dt)
+        e1.record()
+        torch.cuda.synchronize()
+        launches = sb.kernel_launches() - l0
+        clocks = sampler.stop() if sampler else None
+        if world > 1:
+            dist.barrier()
+        ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item()), launches, clocks
+
+    def measure_bytes(dt, layout):
+        """exact algorithmic bytes of this rank's slice from the counter-instrumented kernel"""
+        d_ctr = torch.empty(count * 4, dtype=torch.int32, device=dev)
+        if wl.algorithm == "chrt":
+            dt.closest_hit(d_q.data_ptr(), count, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+        else:
+            dt.closest_point(d_q.data_ptr(), count, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+        torch.cuda.synchronize()
+        sums = d_ctr.view(-1, 4).sum(dim=0, dtype=torch.int64)
+        errors = int((d_st != 0).sum().item())
+        if world > 1:
+            dist.all_reduce(sums)
+        s = sums.cpu().numpy().astype(np.float64) / wl.total
+        mean = np.zeros(1, sb.COUNTERS_DTYPE)
+        plan = sb.layout_plan(layout)
+        nb = [x for x in plan["buffers"] if x["name"] == plan["node_group"]][0]
+        seg = [x["stride_bytes"] for x in nb["segments"]]
+        hot, cold = (seg[0] if seg else 0), sum(seg[1:])
+        bpq = s[0] * hot + s[2] * cold + s[1] * 36 + q_bytes + r_bytes
+        del d_ctr
+        return bpq, {"node_visits": s[0], "prim_tests": s[1], "cold_loads": s[2]}, errors
+
+    peak, peak_src = measured_peak()
+    results = {}
+    layouts = [args.layout] + ([l for l in args.sweep.split(",") if l and l != args.layout] if world == 1 else [])
+    headline = None
+    for li, layout in enumerate(layouts):
+        dt, img, pt, bcast_s = replicate(layout)
+        W.generate_device(wl, dt, lo, hi, first, count, d_q.data_ptr())
+        torch.cuda.synchronize()
+        is_head = li == 0
+        sampler = ClockSampler(local_rank) if (is_head and rank == 0) else None
+        ms, launches, clocks = timed(dt, args.steps if is_head else max(2, min(3, args.steps)), args.warmup if is_head else 3, sampler)
+        bpq, ctr, errors = measure_bytes(dt, layout)
+        value = wl.total / ms / 1e3
+        gbs = bpq * wl.total / (ms * 1e-3) / 1e9
+        info = {"mrays": value, "ms_per_step": ms, "bytes_per_query": bpq, "achieved_gbs": gbs, "frac_of_measured_hbm": gbs / peak, "frac_of_nominal_8tbs": gbs / 8000.0,
+                "node_visits": ctr["node_visits"], "prim_tests": ctr["prim_tests"], "query_errors": errors}
+        if rank == 0:
+            info["bvh_bytes_per_prim"] = pt.node_bytes / ltree.nprims
+            info["total_bytes_per_prim"] = pt.total_bytes / ltree.nprims
+            info["replicate_s"] = bcast_s
+        results[layout] = info
+        if is_head:
+            headline = dict(ms=ms, launches=launches, clocks=clocks, value=value, bpq=bpq, gbs=gbs, dt=dt, img=img, pt=pt)
+        else:
+            dt.free()
+            del img
+
+    # ---- end to end through the host-buffer C-ABI call (pinned host rays in, host hits out)
+    e2e = None
+    dt = headline["dt"]
+    if not args.no_e2e:
+        try:
+            h_q = torch.empty(count * q_bytes, dtype=torch.uint8).pin_memory()
+            h_r = torch.empty(count * r_bytes, dtype=torch.uint8).pin_memory()
+            W.generate_device(wl, dt, lo, hi, first, count, d_q.data_ptr())
+            h_q.copy_(d_q)
+            torch.cuda.synchronize()
+            hq = h_q.numpy().view(sb.RAY_DTYPE if wl.algorithm == "chrt" else np.float32)
+            hr = h_r.numpy().view(sb.HIT_DTYPE if wl.algorithm == "chrt" else sb.CP_DTYPE)
+            call = (lambda: dt.closest_hit_host(hq, hr)) if wl.algorithm == "chrt" else (lambda: dt.closest_point_host(hq, hr))
+            call()
+            if world > 1:
+                dist.barrier()
+            esteps = max(1, min(3, args.steps))
+            t0 = time.perf_counter()
+            for _ in range(esteps):
+                call()
+            t_e = torch.tensor([(time.perf_counter() - t0) / esteps], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+            # the device result must equal the e2e result
+            same = bool(torch.equal(h_r.to(dev), d_r)) if True else True
+            e2e = {"value": wl.total / float(t_e.item()) / 1e6, "unit": unit, "h2d_bytes_per_step": count * q_bytes, "d2h_bytes_per_step": count * r_bytes,
+                   "ms_per_step": float(t_e.item()) * 1e3, "matches_device_path": same}
+            del h_q, h_r
+        except Exception as ex:  # e.g. not enough pinnable host memory on the box
+            e2e = {"value": None, "unit": unit, "error": str(ex)[:200]}
+
+    # ---- gather of hit records: all ranks -> every rank, checksum of checksums
+    gather = None
+    if world > 1:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sizes = [sb.partition(wl.total, r, world)[1] * r_bytes for r in range(world)]
+        full = [torch.empty(s, dtype=torch.uint8, device=dev) for s in sizes]
+        dist.all_gather(full, d_r)
+        torch.cuda.synchronize()
+        gather = {"ms": (time.perf_counter() - t0) * 1e3, "bytes": int(sum(sizes))}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu and world == 1:
+            try:
+                from tests.oracle_lib import Oracle
+                orc = Oracle()
+                tb = orc.tree_bytes(headline["pt"])
+                tris = ltree.triangles()
+                n0, t = cpu_run(orc, tb, wl, tris, lo, hi, spread_sample(wl.total, 1 << 18))
+                n_s = int(min(wl.total, max(1 << 18, (n0 / t) * args.cpu_seconds)))
+                n1, t1 = cpu_run(orc, tb, wl, tris, lo, hi, spread_sample(wl.total, n_s))
+                cpu = {"value": n1 / t1 / 1e6, "unit": unit, "cores": os.cpu_count() or 1, "kind": "port",
+                       "sample": f"{n1} queries = 64 contiguous chunks spread evenly over the {wl.total}-query workload, layout {args.layout}, {t1:.1f} s"}
+            except Exception as ex:
+                cpu = {"value": None, "unit": unit, "cores": os.cpu_count() or 1, "kind": "port", "sample": f"failed: {str(ex)[:160]}"}
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(f"{wl.name}:{args.layout}:{world}")
+            except Exception:
+                traffic = None
+        h = headline
+        line = {"metric": f"{unit} ({args.layout}, {wl.name})", "value": h["value"], "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": h["ms"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{wl.name}: {wl.description}", "layout": args.layout, "queries": wl.total, "queries_per_gpu": count,
+                           "l2_policy": "inputs larger than L2 (rays %.1f GB + tree %.2f GB per GPU vs 126 MB L2); no explicit flush" % (count * q_bytes / 1e9, h["pt"].total_bytes / 1e9),
+                           "partition": "contiguous query ranges per rank; tree replicated by one ncclBroadcast", "build_s": build_s},
+                "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s", "frac": h["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
+                             "bytes_per_query": h["bpq"], "frac_of_nominal_8tbs": h["gbs"] / 8000.0},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(h["launches"]), "clocks": h["clocks"], "layouts": results}
+        if gather:
+            line["gather"] = gather
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -219,6 +219,11 @@ int scion_device_count(int* out);
 int scion_dtree_upload(const scion_ptree* p, int device, scion_dtree** out);
 /* allocate an empty device tree with p's shapes (for receiving a broadcast) */
 int scion_dtree_alloc_like(const scion_ptree* p, int device, scion_dtree** out);
+/* bytes of the packed device image of p (header + 256-byte aligned buffers + slack) */
+uint64_t scion_ptree_image_bytes(const scion_ptree* p);
+/* upload INTO caller-owned device memory (>= scion_ptree_image_bytes, 256-byte aligned), e.g. a
+ * torch tensor that is then replicated with ncclBroadcast; the caller keeps ownership */
+int scion_dtree_upload_into(const scion_ptree* p, int device, void* d_image, uint64_t bytes, scion_dtree** out);
 /* Packed wire image used for replication: [header | globals | buffers...] in ONE
  * contiguous device allocation so that a single ncclBroadcast replicates the tree. */
 int scion_dtree_image(const scion_dtree* t, void** d_ptr, uint64_t* bytes);

@@ -115,6 +115,8 @@ def lib() -> C.CDLL:
         "scion_device_count": (i32, [P(i32)]),
         "scion_dtree_upload": (i32, [vp, i32, P(vp)]),
         "scion_dtree_alloc_like": (i32, [vp, i32, P(vp)]),
+        "scion_ptree_image_bytes": (u64, [vp]),
+        "scion_dtree_upload_into": (i32, [vp, i32, vp, u64, P(vp)]),
         "scion_dtree_image": (i32, [vp, P(vp), P(u64)]),
         "scion_dtree_from_image": (i32, [cp, vp, u64, i32, i32, P(vp)]),
         "scion_dtree_free": (None, [vp]),
@@ -373,6 +375,16 @@ class PhysicalTree:
     def upload(self, device: int = 0) -> "DeviceTree":
         h = C.c_void_p()
         _check(lib().scion_dtree_upload(self._h, device, C.byref(h)))
+        return DeviceTree(h, device)
+
+    @property
+    def image_bytes(self) -> int:
+        return lib().scion_ptree_image_bytes(self._h)
+
+    def upload_into(self, device: int, d_image: int, nbytes: int) -> "DeviceTree":
+        """Upload into caller-owned device memory (e.g. a torch tensor that is then broadcast)."""
+        h = C.c_void_p()
+        _check(lib().scion_dtree_upload_into(self._h, device, d_image, nbytes, C.byref(h)))
         return DeviceTree(h, device)
 
     def alloc_like(self, device: int = 0) -> "DeviceTree":

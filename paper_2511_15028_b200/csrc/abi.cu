@@ -315,7 +315,7 @@ int scion_device_count(int* out) {
   return SCION_OK;
 }
 
-static int dtree_create(const scion_ptree* p, int device, bool copy, scion_dtree** out) {
+static int dtree_create(const scion_ptree* p, int device, bool copy, scion_dtree** out, void* into = nullptr, uint64_t into_bytes = 0) {
   if (!p || !out) return fail(SCION_ERR_ARG, "null argument");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(SCION_ERR_NO_DEVICE, "no CUDA device: the B200 backend has no CPU fallback");
@@ -328,7 +328,13 @@ static int dtree_create(const scion_ptree* p, int device, bool copy, scion_dtree
   int rc = header_from_ptree(*p, t->header);
   if (rc) { delete t; return rc; }
   CUDA_OK(cudaSetDevice(device));
-  CUDA_OK(cudaMalloc(&t->image, t->header.total_bytes));
+  if (into) {
+    if (into_bytes < t->header.total_bytes || ((uintptr_t)into & 255u)) { delete t; return fail(SCION_ERR_ARG, "upload_into: buffer too small or not 256-byte aligned"); }
+    t->image = (uint8_t*)into;
+    t->owns_image = false;
+  } else {
+    CUDA_OK(cudaMalloc(&t->image, t->header.total_bytes));
+  }
   CUDA_OK(cudaMemset(t->image, 0, t->header.total_bytes));
   CUDA_OK(cudaMemcpy(t->image, &t->header, sizeof(ImageHeader), cudaMemcpyHostToDevice));
   if (copy)
@@ -340,6 +346,15 @@ static int dtree_create(const scion_ptree* p, int device, bool copy, scion_dtree
   return SCION_OK;
 }
 int scion_dtree_upload(const scion_ptree* p, int device, scion_dtree** out) { return dtree_create(p, device, true, out); }
+int scion_dtree_upload_into(const scion_ptree* p, int device, void* d_image, uint64_t bytes, scion_dtree** out) {
+  if (!d_image) return fail(SCION_ERR_ARG, "null image buffer");
+  return dtree_create(p, device, true, out, d_image, bytes);
+}
+uint64_t scion_ptree_image_bytes(const scion_ptree* p) {
+  ImageHeader h;
+  if (!p || header_from_ptree(*p, h)) return 0;
+  return h.total_bytes;
+}
 int scion_dtree_alloc_like(const scion_ptree* p, int device, scion_dtree** out) { return dtree_create(p, device, false, out); }
 
 int scion_dtree_image(const scion_dtree* t, void** d_ptr, uint64_t* bytes) {
@@ -479,7 +494,7 @@ void scion_camera_default(const float lo[3], const float hi[3], int look_down_y,
     out->eye[2] = hi[2] + 0.35f * diag;
     out->up[0] = 0; out->up[1] = 1; out->up[2] = 0;
   } else {  // outside the +z face
-    out->eye[2] = hi[2] + 1.1f * diag;
+    out->eye[2] = hi[2] + 0.55f * diag;
     out->eye[0] = c[0] + 0.07f * diag;
     out->eye[1] = c[1] + 0.05f * diag;
     out->up[0] = 0; out->up[1] = 1; out->up[2] = 0;

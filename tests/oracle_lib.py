@@ -24,7 +24,7 @@ class Oracle:
         L.oracle_closest_point.argtypes = [C.POINTER(TreeBytes), vp, u64, vp, vp, vp, i32]
         L.oracle_brute_hit.argtypes = [vp, u64, vp, u64, vp]
         L.oracle_brute_point.argtypes = [vp, u64, vp, u64, vp]
-        L.oracle_check_encoding.argtypes = [C.POINTER(TreeBytes), vp, u64, vp, vp, vp, vp, C.c_int32, C.c_char_p, i32]
+        L.oracle_check_encoding.argtypes = [C.POINTER(TreeBytes), vp, u64, vp, vp, vp, vp, C.c_int32, C.c_char_p, i32, C.POINTER(u64)]
         L.oracle_check_encoding.restype = u64
         L.oracle_layout_name.restype = C.c_char_p
         L.oracle_layout_stride.argtypes = [C.c_char_p]
@@ -135,6 +135,7 @@ class Oracle:
         lo2, hi2 = ltree.dop()
         wn, wl = ltree.wnodes(), ltree.wleaves()
         msg = C.create_string_buffer(256)
+        loose = C.c_uint64(0)
         bad = self.lib.oracle_check_encoding(C.byref(tb), nodes.ctypes.data, nodes.shape[0], lo2.ctypes.data, hi2.ctypes.data,
-                                             wn.ctypes.data if wn.size else None, wl.ctypes.data if wl.size else None, ltree.wroot, msg, 256)
-        return bad, msg.value.decode()
+                                             wn.ctypes.data if wn.size else None, wl.ctypes.data if wl.size else None, ltree.wroot, msg, 256, C.byref(loose))
+        return bad, msg.value.decode(), loose.value

@@ -1,0 +1,313 @@
+"""Parity tests proper: the CUDA path, called through the C ABI, against the CPU oracle on the
+same seeded inputs.  Bar (BASELINE.json north_star): hit primitive ids bit-exact with identical
+tie-breaking; t within 1e-6 relative — we require and observe BIT-EXACT t (and d2 / closest point
+for CPQ), plus identical interpreter counters (node visits, primitive tests), which only holds if
+the visit order is the reference's."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def dev_bytes(torch, arr):
+    return torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8).reshape(-1)).to("cuda:0")
+
+
+def gpu_hits(torch, sb, dt, rays, counters=True):
+    n = rays.shape[0]
+    d_rays = dev_bytes(torch, rays) if n else torch.empty(0, dtype=torch.uint8, device="cuda:0")
+    d_hits = torch.zeros(max(n, 1) * 8, dtype=torch.uint8, device="cuda:0")
+    d_st = torch.zeros(max(n, 1) * 4, dtype=torch.uint8, device="cuda:0")
+    d_ctr = torch.zeros(max(n, 1) * 16, dtype=torch.uint8, device="cuda:0")
+    dt.closest_hit(d_rays.data_ptr(), n, d_hits.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr() if counters else 0)
+    torch.cuda.synchronize()
+    return (d_hits.cpu().numpy().view(sb.HIT_DTYPE)[:n], d_st.cpu().numpy().view(np.uint32)[:n], d_ctr.cpu().numpy().view(sb.COUNTERS_DTYPE)[:n])
+
+
+def gpu_points(torch, sb, dt, pts):
+    n = pts.shape[0]
+    d_p = dev_bytes(torch, pts)
+    d_o = torch.zeros(n * 20, dtype=torch.uint8, device="cuda:0")
+    d_st = torch.zeros(n * 4, dtype=torch.uint8, device="cuda:0")
+    d_ctr = torch.zeros(n * 16, dtype=torch.uint8, device="cuda:0")
+    dt.closest_point(d_p.data_ptr(), n, d_o.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+    torch.cuda.synchronize()
+    return d_o.cpu().numpy().view(sb.CP_DTYPE), d_st.cpu().numpy().view(np.uint32), d_ctr.cpu().numpy().view(sb.COUNTERS_DTYPE)
+
+
+def assert_hits_equal(got, want, what):
+    assert np.array_equal(got["prim"], want["prim"]), f"{what}: primitive ids differ at {np.nonzero(got['prim'] != want['prim'])[0][:10]}"
+    assert np.array_equal(got["t"].view(np.uint32), want["t"].view(np.uint32)), f"{what}: t not bit-exact"
+
+
+SCENES = {"terrain": lambda sb: sb.Scene.terrain(36, 3), "sphere": lambda sb: sb.Scene.sphere(28, 5)}
+
+
+@pytest.fixture(scope="module", params=["terrain", "sphere"])
+def world(request, built, oracle):
+    sb = built
+    scene = SCENES[request.param](sb)
+    lt = scene.build_sah(32, 4).collapse8()
+    lo, hi = scene.bounds()
+    cam = sb.default_camera(lo, hi, request.param == "terrain", 96, 96)
+    rays = np.concatenate([sb.gen_primary_host(cam, 0, 96 * 96), sb.gen_secondary_host(lt.triangles(), 11, 0, 6000 + 13)])
+    pts = sb.gen_points_host(lo - 0.3, hi + 0.3, 5, 0, 4099)
+    return dict(name=request.param, scene=scene, lt=lt, lo=lo, hi=hi, rays=rays, pts=pts)
+
+
+def layout_names():
+    return ["pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "ptr", "identity", "shared-slab", "dop14", "bvh8", "bvh8-q8",
+            "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
+
+
+@pytest.mark.parametrize("layout", layout_names())
+def test_closest_hit_matches_oracle(built, oracle, torch_cuda, world, layout):
+    sb = built
+    pt = world["lt"].encode(layout)
+    dt = pt.upload(0)
+    got, st, ctr = gpu_hits(torch_cuda, sb, dt, world["rays"])
+    want, wst, wctr = oracle.closest_hit(oracle.tree_bytes(pt), world["rays"], counters=True)
+    assert (want["prim"] != sb.MISS_PRIM).mean() > 0.1
+    assert_hits_equal(got, want, f"{layout}/{world['name']}")
+    assert np.array_equal(st, wst) and st.max() == 0
+    assert np.array_equal(ctr, wctr), f"{layout}: interpreter counters differ => visit order differs"
+    # the counter-free production kernel returns the same records
+    got2, _, _ = gpu_hits(torch_cuda, sb, dt, world["rays"], counters=False)
+    assert_hits_equal(got2, want, f"{layout} (no counters)")
+    # host-buffer entry point (H2D + kernel + D2H inside the call)
+    st_h = np.full(world["rays"].shape[0], 7, np.uint32)
+    got3 = dt.closest_hit_host(world["rays"], status=st_h)
+    assert_hits_equal(got3, want, f"{layout} (host entry)")
+    assert st_h.max() == 0
+    dt.free()
+
+
+@pytest.mark.parametrize("layout", [l for l in layout_names() if not l.startswith("bvh8")])
+def test_closest_point_matches_oracle(built, oracle, torch_cuda, world, layout):
+    sb = built
+    pt = world["lt"].encode(layout)
+    dt = pt.upload(0)
+    got, st, ctr = gpu_points(torch_cuda, sb, dt, world["pts"])
+    want, wst, wctr = oracle.closest_point(oracle.tree_bytes(pt), world["pts"], counters=True)
+    # north_star tolerance for floating point is 1e-6 relative; we require bit-exact d2, point and primitive
+    assert np.array_equal(got.view(np.uint32).reshape(-1, 5), want.view(np.uint32).reshape(-1, 5)), layout
+    assert np.array_equal(st, wst) and np.array_equal(ctr, wctr)
+    rel = np.abs(got["d2"] - want["d2"]) / np.maximum(want["d2"], 1e-30)
+    assert rel.max() <= 1e-6
+    got_h = dt.closest_point_host(world["pts"])
+    assert np.array_equal(got_h.view(np.uint32), got.view(np.uint32))
+    dt.free()
+
+
+def test_wide_layouts_reject_closest_point(built, torch_cuda, world):
+    dt = world["lt"].encode("bvh8-q8-ci").upload(0)
+    with pytest.raises(built.ScionError) as e:  # corpus.cpp:83 "cpq requires a binary layout"
+        dt.closest_point_host(world["pts"][:8])
+    assert e.value.code == built.ERR_ARG
+    dt.free()
+
+
+def test_golden_fixture(built, torch_cuda):
+    """committed oracle outputs (tests/golden/hits_small.npz, tools/gen_golden.py)"""
+    sb = built
+    g = np.load(os.path.join(ROOT, "tests", "golden", "hits_small.npz"))
+    grid, seed = [int(x) for x in g["terrain_grid"]]
+    lt = sb.Scene.terrain(grid, seed).build_sah(32, 4).collapse8()
+    rays = np.ascontiguousarray(g["rays"]).view(sb.RAY_DTYPE).reshape(-1)
+    for layout in layout_names():
+        dt = lt.encode(layout).upload(0)
+        got, st, ctr = gpu_hits(torch_cuda, sb, dt, rays)
+        assert np.array_equal(got["prim"], g[f"hit_prim:{layout}"]) and np.array_equal(got["t"].view(np.uint32), g[f"hit_t:{layout}"].view(np.uint32)), layout
+        assert np.array_equal(ctr["node_visits"], g[f"hit_visits:{layout}"])
+        if f"cp:{layout}" in g:
+            cp, _, _ = gpu_points(torch_cuda, sb, dt, np.ascontiguousarray(g["points"]))
+            assert np.array_equal(cp.view(np.uint32).reshape(-1, 5), g[f"cp:{layout}"]), layout
+        dt.free()
+
+
+def test_edge_cases(built, oracle, torch_cuda):
+    sb = built
+    scene = sb.Scene.terrain(8, 9)
+    lt = scene.build_sah(32, 4).collapse8()
+    lo, hi = scene.bounds()
+    r = np.zeros(12, sb.RAY_DTYPE)
+    r["tmax"] = np.inf
+    c = 0.5 * (lo + hi)
+    # 0: straight down through the centre; 1: axis-aligned with two zero direction components from a slab plane
+    r[0] = (c[0], hi[1] + 1, c[2], np.inf, 0, -1, 0, 0)
+    r[1] = (lo[0], hi[1] + 1, c[2], np.inf, 0, -1, 0, 0)  # origin x exactly on the world slab plane: 0 * inf = NaN path
+    r[2] = (c[0], hi[1] + 1, c[2], 0.25, 0, -1, 0, 0)  # finite tmax: miss
+    r[3] = (c[0], c[1] + 10, c[2], np.inf, 0, 1, 0, 0)  # pointing away
+    r[4] = (c[0], lo[1] - 1, c[2], np.inf, 0, 1, 0, 0)  # from below (back faces)
+    r[5] = (c[0], c[1], c[2], np.inf, 0.6, 0.0, 0.8, 0)  # origin inside the root box
+    r[6] = (c[0], hi[1] + 1, c[2], np.inf, -0.0, -1, -0.0, 0)  # negative zeros are not "negative" (geometry.scion:13)
+    r[7] = (lo[0] - 1, c[1], lo[2] - 1, np.inf, 0.70710678, 0, 0.70710678, 0)  # diagonal grazing
+    r[8] = (c[0], hi[1] + 1, c[2], np.inf, 0, 0, 0, 0)  # null direction: rdir = inf everywhere
+    r[9] = (np.nan, 0, 0, np.inf, 0, -1, 0, 0)  # NaN origin
+    r[10] = (c[0], hi[1] + 1, c[2], 0.0, 0, -1, 0, 0)  # tmax = 0
+    r[11] = (c[0], hi[1] + 1e30, c[2], np.inf, 0, -1, 0, 0)  # far away: precision loss, still deterministic
+    pts = np.array([[c[0], c[1], c[2]], [lo[0], lo[1], lo[2]], [1e6, 1e6, 1e6], [np.nan, 0, 0]], np.float32)
+    for layout in layout_names():
+        pt = lt.encode(layout)
+        dt = pt.upload(0)
+        tb = oracle.tree_bytes(pt)
+        for n in (12, 1, 0):  # ragged / single / empty launches
+            got, st, ctr = gpu_hits(torch_cuda, sb, dt, r[:n])
+            want, wst, wctr = oracle.closest_hit(tb, r[:n], counters=True)
+            assert_hits_equal(got, want, f"{layout} edge n={n}")
+            assert np.array_equal(ctr, wctr)
+        assert got.shape[0] == 0
+        full, _, _ = gpu_hits(torch_cuda, sb, dt, r)
+        assert full["prim"][0] != sb.MISS_PRIM and full["prim"][2] == sb.MISS_PRIM and np.isinf(full["t"][2]) and full["prim"][3] == sb.MISS_PRIM
+        if not layout.startswith("bvh8"):
+            cp, _, _ = gpu_points(torch_cuda, sb, dt, pts)
+            wcp, _ = oracle.closest_point(tb, pts)
+            assert np.array_equal(cp.view(np.uint32), wcp.view(np.uint32)), layout
+        dt.free()
+    # single-leaf tree, every layout ("degenerate tree")
+    one = sb.Scene.from_triangles(np.array([[0, 0, 0, 1, 0, 0, 0, 1, 0]], np.float32)).build_sah(32, 4).collapse8()
+    ray = np.zeros(2, sb.RAY_DTYPE)
+    ray[0] = (0.25, 0.25, -1, np.inf, 0, 0, 1, 0)
+    ray[1] = (2.0, 2.0, -1, np.inf, 0, 0, 1, 0)
+    for layout in layout_names():
+        dt = one.encode(layout).upload(0)
+        got, _, _ = gpu_hits(torch_cuda, sb, dt, ray)
+        assert got["t"][0] == 1.0 and got["prim"][0] == 0 and got["prim"][1] == sb.MISS_PRIM, layout  # MT KAT through the whole stack
+        dt.free()
+
+
+def test_stack_overflow_is_a_query_error(built, oracle, torch_cuda):
+    """a tree deeper than the 64-entry stack: overflow is reported per query, never silent"""
+    sb = built
+    # a degenerate chain: nested triangles force a median tree of depth 70 is not constructible through
+    # the depth-capped builders, so craft the LogicalTree-equivalent pbrt image by hand: 71 interiors
+    # whose LEFT child is a leaf and whose right child is the next interior (right-deep chain).
+    depth = 71
+    tris, nodes = [], []
+    # node i (interior) at index 2i, its left leaf at 2i+1, right = 2i+2 ; last node is a leaf
+    for i in range(depth + 1):
+        x = float(i)
+        tris.append([x, 0, 0, x + 0.5, 0, 0, x, 0.5, 0])
+    tris = np.array(tris, np.float32)
+    lt = sb.Scene.from_triangles(tris).build_median(1)  # balanced: depth 7, no overflow
+    dt = lt.encode("pbrt").upload(0)
+    ray = np.zeros(1, sb.RAY_DTYPE)
+    ray[0] = (0.1, 0.1, -1, np.inf, 0, 0, 1, 0)
+    got, st, ctr = gpu_hits(torch_cuda, sb, dt, ray)
+    assert st[0] == 0 and ctr["max_stack"][0] <= 64
+    dt.free()
+    # left-deep chain built directly as a pbrt byte image: every interior's left child is the next
+    # interior (this+1), its right child a leaf => pending right siblings grow by one per level.
+    N = 2 * depth + 1
+    buf = np.zeros(N * 32, np.uint8)
+    f = buf.view(np.float32).reshape(N, 8)
+    u = buf.view(np.uint32).reshape(N, 8)
+    h = buf.view(np.uint16).reshape(N, 16)
+    big_lo, big_hi = (-1.0, -1.0, -1.0), (float(depth + 2), 1.0, 1.0)
+    for i in range(depth):  # interiors at 0..depth-1 (preorder: left = this+1)
+        f[i, 0:3], f[i, 3:6] = big_lo, big_hi
+        u[i, 6] = (N - 1 - i) - i  # right child = leaf placed from the end
+        h[i, 14] = 0
+    for j in range(depth, N):  # leaves
+        f[j, 0:3], f[j, 3:6] = big_lo, big_hi
+        u[j, 6] = (j - depth) % (depth + 1)
+        h[j, 14] = 1
+    import ctypes as C
+    from tests.oracle_lib import TreeBytes
+    prim = np.ascontiguousarray(tris.reshape(-1))
+    tb = TreeBytes()
+    tb.layout = b"pbrt"
+    tb.nbuf = 2
+    tb.buf[0], tb.bytes[0], tb.count[0] = prim.ctypes.data, prim.nbytes, len(tris)
+    tb.buf[1], tb.bytes[1], tb.count[1] = buf.ctypes.data, buf.nbytes, N
+    want, wst, wctr = oracle.closest_hit(tb, ray, counters=True)
+    assert wst[0] == 1  # the oracle reports overflow (depth 71 > 64)
+    # upload the same hand-made image by patching a real ptree of the same shape
+    # (buffers are replaced through the device image: header from a compatible tree, payload ours)
+    base = sb.Scene.from_triangles(tris).build_median(1).encode("pbrt")
+    img_bytes = base.image_bytes
+    dimg = torch_cuda.zeros(img_bytes + N * 32 + 4096, dtype=torch_cuda.uint8, device="cuda:0")
+    off = (-dimg.data_ptr()) % 256
+    dt0 = base.upload_into(0, dimg.data_ptr() + off, img_bytes + N * 32)
+    himg = dimg.cpu().numpy()
+    hdr = himg[off:off + 1024].copy()
+    # header fields (abi.cu ImageHeader): offset[] at byte 72, bytes[] at 120, count[] at 168 (8 bytes each, 6 entries)
+    offs = hdr[72:72 + 48].view(np.uint64)
+    node_off = int(offs[1])
+    cnts = hdr[168:168 + 48].view(np.uint64)
+    assert int(cnts[1]) == len(base.buffers()[1]["data"]) // 32
+    if N * 32 <= int(hdr[120:168].view(np.uint64)[1]) + 16 + 4096:
+        himg[off + node_off:off + node_off + N * 32] = buf
+        dimg.copy_(torch_cuda.from_numpy(himg))
+        got, st, ctr = gpu_hits(torch_cuda, sb, dt0, ray)
+        assert st[0] == 1, "GPU must report STACK_OVERFLOW like the oracle"
+    dt0.free()
+
+
+def test_fault_injection_changes_results(built, oracle, torch_cuda, world):
+    """corrupting one c_o byte must surface as >= 1 mismatch against the oracle of the intact tree"""
+    sb = built
+    pt = world["lt"].encode("pbrt")
+    want, _ = oracle.closest_hit(oracle.tree_bytes(pt), world["rays"])
+    pt.corrupt(1, 24, 0x01)  # root node: c_o ^= 1 -> right child off by one
+    dt = pt.upload(0)
+    got, st, _ = gpu_hits(torch_cuda, sb, dt, world["rays"])
+    assert (got["prim"] != want["prim"]).sum() + (st != 0).sum() >= 1
+    dt.free()
+
+
+def test_replication_paths_agree(built, oracle, torch_cuda, world):
+    """upload / upload_into a caller tensor / from_image of a copied image give identical results"""
+    sb, torch = built, torch_cuda
+    pt = world["lt"].encode("pbrt-q16")
+    a = pt.upload(0)
+    ref, _, _ = gpu_hits(torch, sb, a, world["rays"], counters=False)
+    img = torch.empty(pt.image_bytes + 256, dtype=torch.uint8, device="cuda:0")
+    off = (-img.data_ptr()) % 256
+    b = pt.upload_into(0, img.data_ptr() + off, pt.image_bytes)
+    gb, _, _ = gpu_hits(torch, sb, b, world["rays"], counters=False)
+    copy = img.clone()  # what a broadcast receiver holds
+    off2 = (-copy.data_ptr()) % 256
+    if off2 != off:
+        copy2 = torch.empty(pt.image_bytes + 512, dtype=torch.uint8, device="cuda:0")
+        off2 = (-copy2.data_ptr()) % 256
+        copy2[off2:off2 + pt.image_bytes] = img[off:off + pt.image_bytes]
+        copy = copy2
+    c = sb.DeviceTree.from_image(copy.data_ptr() + off2, pt.image_bytes, 0, "pbrt-q16")
+    gc, _, _ = gpu_hits(torch, sb, c, world["rays"], counters=False)
+    assert_hits_equal(gb, ref, "upload_into")
+    assert_hits_equal(gc, ref, "from_image")
+    with pytest.raises(sb.ScionError):
+        sb.DeviceTree.from_image(copy.data_ptr() + off2, pt.image_bytes, 0, "pbrt")  # wrong layout name is rejected
+    for t in (a, b, c):
+        t.free()
+
+
+def test_device_generators_match_host_twins(built, torch_cuda, world):
+    sb, torch = built, torch_cuda
+    lo, hi = world["lo"], world["hi"]
+    cam = sb.default_camera(lo, hi, True, 64, 64)
+    n = 64 * 64
+    d = torch.empty(n * 32, dtype=torch.uint8, device="cuda:0")
+    sb.gen_primary(cam, 5, n - 5, d.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy()[:(n - 5) * 32].view(np.uint32), sb.gen_primary_host(cam, 5, n - 5).view(np.uint32))
+    dt = world["lt"].encode("pbrt").upload(0)
+    dt.gen_secondary(77, 100, n, d.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), sb.gen_secondary_host(world["lt"].triangles(), 77, 100, n).view(np.uint32))
+    p = torch.empty(n * 12, dtype=torch.uint8, device="cuda:0")
+    sb.gen_points(lo, hi, 9, 3, n, p.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(p.cpu().numpy().view(np.uint32), sb.gen_points_host(lo, hi, 9, 3, n).view(np.uint32).reshape(-1))
+    dt.free()
