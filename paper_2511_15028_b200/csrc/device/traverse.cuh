@@ -9,10 +9,17 @@
 // right child), because hit ids are only bit-exact when pruning sees the same `best` at the same
 // moment.
 //
-// Stack: the traversal stack lives in shared memory, laid out [entry][thread] so that any mix
-// of per-lane depths is bank-conflict free (lane l always hits bank l); the top of the tree walk
-// never touches it for the left child (implicit next node).  See DESIGN.md for the measured
-// comparison against a local-memory stack.
+// Execution model (justified by profiles/r1_ncu_v1_c5_q16_*: the first, one-warp-32-rays kernel
+// ran at 6.2 of 32 active threads per instruction, its triangle loop at 1 of 32):
+//   * persistent warps; every LANE is refilled with a new query as soon as its previous one
+//     retires (ballot + prefix popcount over a warp-private chunk of the global work counter);
+//   * the per-lane loop body is a small state machine — FETCH, NODE, PRIM — so that lanes in the
+//     same state execute the same instructions in the same iteration: all NODE lanes decode and
+//     test one node, then all PRIM lanes test one primitive;
+//   * the PRIM phase only runs when enough lanes wait in it (or nothing else can progress), which
+//     batches the expensive, rare Moeller-Trumbore evaluations.
+// Stack: first entries in shared memory laid out [entry][thread] (lane l always hits bank l, so
+// any mix of per-lane depths is conflict free), deeper entries in local memory.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -22,19 +29,13 @@
 namespace scion {
 
 constexpr int kBlockThreads = 128;
+constexpr unsigned kFullMask = 0xffffffffu;
+constexpr int kChunk = 256;     // queries a warp takes from the global counter at a time
+constexpr int kRefillMin = 4;   // refill when at least this many lanes are idle (or all of them)
+constexpr int kPrimMin = 8;     // run the PRIM phase when at least this many lanes wait in it
 
-// ------------------------------------------------------------------------------------------
-// work distribution: persistent CTAs; each warp grabs 32 queries at a time with one atomic
-// issued by an elected lane and broadcast by shuffle (warp-aggregated dynamic fetch).
-// ------------------------------------------------------------------------------------------
-struct WorkQueue {
-  unsigned long long* counter;  // device global, zeroed before launch
-};
-
-// Hybrid traversal stack: the first kSmem entries live in shared memory, laid out
-// [entry][thread] (lane l always hits bank l => conflict-free for any mix of per-lane depths);
-// deeper entries spill to a per-thread local-memory array that is only touched by the rare deep
-// paths.  kSmem is sized so that one CTA uses 16 KB of shared memory whatever the entry size.
+// Hybrid traversal stack (see header comment).  kSmem is sized so that one CTA uses 16 KB of
+// shared memory whatever the entry size.
 constexpr int kStackSmemBytesPerBlock = 16 * 1024;
 template <class Entry>
 struct HybridStack {
@@ -42,30 +43,62 @@ struct HybridStack {
                                    ? (kStackSmemBytesPerBlock / kBlockThreads / (int)sizeof(Entry))
                                    : SCION_STACK_DEPTH;
   static constexpr int kDeep = SCION_STACK_DEPTH - kSmem > 0 ? SCION_STACK_DEPTH - kSmem : 1;
-  Entry* base;  // &smem[threadIdx.x]; entry e lives at base[e * kBlockThreads]
   Entry deep[kDeep];
   int sp = 0;
-  SCION_DEV void push(const Entry& r) {
-    if (sp < kSmem) base[sp * kBlockThreads] = r;
+  SCION_DEV void push(Entry* smem, const Entry& r) {
+    if (sp < kSmem) smem[sp * kBlockThreads + threadIdx.x] = r;
     else deep[sp - kSmem] = r;
     sp++;
   }
-  SCION_DEV Entry pop() {
+  SCION_DEV Entry pop(Entry* smem) {
     sp--;
-    return sp < kSmem ? base[sp * kBlockThreads] : deep[sp - kSmem];
+    return sp < kSmem ? smem[sp * kBlockThreads + threadIdx.x] : deep[sp - kSmem];
   }
 };
 
 template <bool COUNT>
 struct Tally {
   uint32_t node_visits = 0, prim_tests = 0, cold_loads = 0, max_stack = 0;
+  SCION_DEV void reset() { node_visits = prim_tests = cold_loads = max_stack = 0; }
   SCION_DEV void visit() { if (COUNT) node_visits++; }
-  SCION_DEV void visits(uint32_t k) { if (COUNT) node_visits += k; }
   SCION_DEV void prim() { if (COUNT) prim_tests++; }
   SCION_DEV void cold(uint32_t k = 1) { if (COUNT) cold_loads += k; }
   SCION_DEV void stack(uint32_t occ) { if (COUNT) max_stack = occ > max_stack ? occ : max_stack; }
   SCION_DEV void store(scion_counters* out, uint64_t q) const {
     if (COUNT && out) out[q] = scion_counters{node_visits, prim_tests, cold_loads, max_stack};
+  }
+};
+
+// Warp-private window on the global work counter.  All 32 lanes call refill(); lanes that pass
+// want=true and for which work is left get a query index.  All members are warp-uniform.
+struct WorkFetcher {
+  unsigned long long chunk_base = 0;
+  unsigned chunk_left = 0;
+  bool exhausted = false;
+  SCION_DEV bool refill(bool want, unsigned long long* next, uint64_t n, uint64_t& q) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned lt = (1u << lane) - 1u;
+    bool got = false;
+    unsigned idle = __ballot_sync(kFullMask, want);
+    while (idle) {
+      if (chunk_left == 0) {
+        if (exhausted) break;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(next, (unsigned long long)kChunk);
+        base = __shfl_sync(kFullMask, base, 0);
+        if (base >= n) { exhausted = true; break; }
+        chunk_base = base;
+        chunk_left = (unsigned)(n - base < (uint64_t)kChunk ? n - base : (uint64_t)kChunk);
+      }
+      const unsigned rank = __popc(idle & lt);
+      if (want && !got && rank < chunk_left) { q = chunk_base + rank; got = true; }
+      const unsigned cnt = __popc(idle);
+      const unsigned taken = cnt < chunk_left ? cnt : chunk_left;
+      chunk_base += taken;
+      chunk_left -= taken;
+      idle = __ballot_sync(kFullMask, want && !got);
+    }
+    return got;
   }
 };
 
@@ -75,19 +108,16 @@ SCION_DEV RayCtx load_ray(const scion_ray* rays, uint64_t q) {
   return make_ray(a.x, a.y, a.z, a.w, b.x, b.y, b.z);
 }
 
-template <class L, class TallyT>
-SCION_DEV void leaf_triangles(const TreeView& T, const RayCtx& ray, const Slice& data, float& best_t, uint32_t& best_prim, TallyT& tally) {
+// one primitive: `if intersects(ray, t) && distmin(ray, t) < best[0] { best = (distmin(ray, t), t) }`
+template <class L>
+SCION_DEV void test_triangle(const TreeView& T, const RayCtx& ray, uint32_t i, float& best_t, uint32_t& best_prim) {
   static_assert(L::kStride_primitives == 36, "Triangle stride");
-  for (uint64_t i = data.begin; i < data.end; i++) {
-    float tri[9];
-    load_triangle36(T.buf[L::kBuf_primitives], i, tri);
-    float t;
-    tally.prim();
-    // `intersects(ray, t) && distmin(ray, t) < best[0]` then `best = (distmin(ray, t), t)`
-    if (ray_tri_mt(ray, tri, t) && t < best_t) {
-      best_t = t;
-      best_prim = (uint32_t)i;
-    }
+  float tri[9];
+  load_triangle36(T.buf[L::kBuf_primitives], i, tri);
+  float t;
+  if (ray_tri_mt(ray, tri, t) && t < best_t) {
+    best_t = t;
+    best_prim = i;
   }
 }
 
@@ -117,59 +147,98 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
   }
 }
 
+enum : int { kFetch = 0, kNode = 1, kPrim = 2 };
+
 // ------------------------------------------------------------------------------------------
 // closest_hit, binary + DOP-14 families
 // ------------------------------------------------------------------------------------------
 template <class L, bool COUNT>
 __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
-                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next) {
+                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ref* const sstack = reinterpret_cast<Ref*>(smem_raw);
   HybridStack<Ref> stack;
-  stack.base = reinterpret_cast<Ref*>(smem_raw) + threadIdx.x;
-  const unsigned lane = threadIdx.x & 31u;
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(next, 32ull);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= n) break;
-    const uint64_t q = base + lane;
-    if (q < n) {
-      const RayCtx ray = load_ray(rays, q);
-      float best_t = scion::inf();
-      uint32_t best_prim = SCION_MISS_PRIM;
-      uint32_t st = SCION_Q_OK;
-      Tally<COUNT> tally;
-      stack.sp = 0;
-      Ref cur = L::root(T);
-      for (;;) {
-        typename L::Node node;
-        L::decode(T, cur, node);
-        tally.visit();
-        float t_near;
-        const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
-        bool descend = false;
-        if (hit) {
-          if (node.variant == L::kLeaf) {
-            leaf_triangles<L>(T, ray, node.data, best_t, best_prim, tally);
-          } else if (t_near < best_t) {
-            // reference discipline: pop self, push right, push left => occupancy sp + 2
-            tally.stack((uint32_t)stack.sp + 2u);
-            if (stack.sp + 2 > SCION_STACK_DEPTH) { st = SCION_Q_STACK_OVERFLOW; break; }
-            stack.push(node.right);
-            cur = node.left;
-            descend = true;
-          }
-        }
-        if (!descend) {
-          if (stack.sp == 0) break;
-          cur = stack.pop();
-        }
-      }
+  WorkFetcher work;
+  const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
+  const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
+  Tally<COUNT> tally;
+  int mode = kFetch;
+  uint64_t q = 0;
+  RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
+  float best_t = 0;
+  uint32_t best_prim = 0, st = 0, prim_i = 0, prim_end = 0;
+  Ref cur = L::root(T);
+
+  // retire the lane's query or continue with the next pending subtree
+  auto pop_or_finish = [&]() {
+    if (stack.sp == 0 || st != SCION_Q_OK) {
       hits[q] = scion_hit{best_t, best_prim};
       if (status) status[q] = st;
       tally.store(counters, q);
+      mode = kFetch;
+    } else {
+      cur = stack.pop(sstack);
+      mode = kNode;
+    }
+  };
+
+  for (;;) {
+    // ---- FETCH: refill idle lanes
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    if (idle) {
+      if (__popc(idle) >= refill_min || idle == kFullMask || work.exhausted) {
+        uint64_t nq;
+        if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
+          q = nq;
+          ray = load_ray(rays, q);
+          best_t = scion::inf();
+          best_prim = SCION_MISS_PRIM;
+          st = SCION_Q_OK;
+          tally.reset();
+          stack.sp = 0;
+          cur = L::root(T);
+          mode = kNode;
+        }
+        if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
+      }
+    }
+    // ---- NODE: decode one node, test its bounds
+    if (mode == kNode) {
+      typename L::Node node;
+      L::decode(T, cur, node);
+      tally.visit();
+      float t_near;
+      const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
+      if (hit && node.variant == L::kLeaf) {
+        prim_i = (uint32_t)node.data.begin;
+        prim_end = (uint32_t)node.data.end;
+        if (prim_i < prim_end) mode = kPrim;
+        else pop_or_finish();
+      } else if (hit && t_near < best_t) {
+        // reference discipline: pop self, push right, push left => occupancy sp + 2
+        tally.stack((uint32_t)stack.sp + 2u);
+        if (stack.sp + 2 > SCION_STACK_DEPTH) {
+          st = SCION_Q_STACK_OVERFLOW;
+          pop_or_finish();
+        } else {
+          stack.push(sstack, node.right);
+          cur = node.left;
+        }
+      } else {
+        pop_or_finish();
+      }
+    }
+    // ---- PRIM: one primitive per waiting lane, batched
+    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    if (pmask) {
+      const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
+      if (run && mode == kPrim) {
+        tally.prim();
+        test_triangle<L>(T, ray, prim_i, best_t, best_prim);
+        if (++prim_i == prim_end) pop_or_finish();
+      }
     }
   }
 }
@@ -188,60 +257,99 @@ struct WideEntry {
 template <class L, bool COUNT>
 __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
-                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next) {
+                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   using Entry = WideEntry<Ref>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  Entry* const sstack = reinterpret_cast<Entry*>(smem_raw);
   HybridStack<Entry> stack;
-  stack.base = reinterpret_cast<Entry*>(smem_raw) + threadIdx.x;
-  const unsigned lane = threadIdx.x & 31u;
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(next, 32ull);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= n) break;
-    const uint64_t q = base + lane;
-    if (q < n) {
-      const RayCtx ray = load_ray(rays, q);
-      float best_t = scion::inf();
-      uint32_t best_prim = SCION_MISS_PRIM;
-      uint32_t st = SCION_Q_OK;
-      Tally<COUNT> tally;
-      stack.sp = 0;
-      Ref cur = L::root(T);
-      for (;;) {
-        typename L::Node node;
-        L::decode(T, cur, node);
-        if (node.variant == L::kLeaf) {
-          leaf_triangles<L>(T, ray, node.data, best_t, best_prim, tally);
-        } else {
-          tally.visit();
-          // test all eight child boxes; push the passing ones in reverse slot order
-          uint32_t mask = 0;
-          float tn[8];
-#pragma unroll
-          for (int k = 0; k < 8; k++) {
-            float t_far;
-            const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn[k], t_far);
-            if (interval_intersects(ray, some, tn[k], t_far) && tn[k] < best_t) mask |= 1u << k;
-          }
-          const int m = __popc(mask);
-          tally.stack((uint32_t)(stack.sp + m));
-          if (stack.sp + m > SCION_STACK_DEPTH) { st = SCION_Q_STACK_OVERFLOW; break; }
-#pragma unroll
-          for (int k = 7; k >= 0; k--)
-            if (mask & (1u << k)) stack.push(Entry{node.children[k], tn[k]});
-        }
-        bool found = false;
-        while (stack.sp > 0) {
-          const Entry e = stack.pop();
-          if (e.t_near < best_t) { cur = e.ref; found = true; break; }
-        }
-        if (!found) break;
+  WorkFetcher work;
+  const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
+  const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
+  Tally<COUNT> tally;
+  int mode = kFetch;
+  uint64_t q = 0;
+  RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
+  float best_t = 0;
+  uint32_t best_prim = 0, st = 0, prim_i = 0, prim_end = 0;
+  Ref cur = L::root(T);
+
+  auto pop_or_finish = [&]() {
+    bool found = false;
+    if (st == SCION_Q_OK) {
+      while (stack.sp > 0) {
+        const Entry e = stack.pop(sstack);
+        if (e.t_near < best_t) { cur = e.ref; found = true; break; }
       }
+    }
+    if (found) {
+      mode = kNode;
+    } else {
       hits[q] = scion_hit{best_t, best_prim};
       if (status) status[q] = st;
       tally.store(counters, q);
+      mode = kFetch;
+    }
+  };
+
+  for (;;) {
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    if (idle) {
+      if (__popc(idle) >= refill_min || idle == kFullMask || work.exhausted) {
+        uint64_t nq;
+        if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
+          q = nq;
+          ray = load_ray(rays, q);
+          best_t = scion::inf();
+          best_prim = SCION_MISS_PRIM;
+          st = SCION_Q_OK;
+          tally.reset();
+          stack.sp = 0;
+          cur = L::root(T);
+          mode = kNode;
+        }
+        if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
+      }
+    }
+    if (mode == kNode) {
+      typename L::Node node;
+      L::decode(T, cur, node);
+      if (node.variant == L::kLeaf) {
+        prim_i = (uint32_t)node.data.begin;
+        prim_end = (uint32_t)node.data.end;
+        if (prim_i < prim_end) mode = kPrim;
+        else pop_or_finish();
+      } else {
+        tally.visit();
+        // test all eight child boxes; push the passing ones in reverse slot order
+        uint32_t mask = 0;
+        float tn[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          float t_far;
+          const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn[k], t_far);
+          if (interval_intersects(ray, some, tn[k], t_far) && tn[k] < best_t) mask |= 1u << k;
+        }
+        const int m = __popc(mask);
+        tally.stack((uint32_t)(stack.sp + m));
+        if (stack.sp + m > SCION_STACK_DEPTH) {
+          st = SCION_Q_STACK_OVERFLOW;
+        } else {
+#pragma unroll
+          for (int k = 7; k >= 0; k--)
+            if (mask & (1u << k)) stack.push(sstack, Entry{node.children[k], tn[k]});
+        }
+        pop_or_finish();
+      }
+    }
+    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    if (pmask) {
+      const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
+      if (run && mode == kPrim) {
+        tally.prim();
+        test_triangle<L>(T, ray, prim_i, best_t, best_prim);
+        if (++prim_i == prim_end) pop_or_finish();
+      }
     }
   }
 }
@@ -264,66 +372,99 @@ SCION_DEV float cpq_node_distmin(const TreeView& T, const f32x3& p, const typena
 template <class L, bool COUNT>
 __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
                                                              scion_cp* __restrict__ out, uint32_t* __restrict__ status,
-                                                             scion_counters* __restrict__ counters, unsigned long long* __restrict__ next) {
+                                                             scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  Ref* const sstack = reinterpret_cast<Ref*>(smem_raw);
   HybridStack<Ref> stack;
-  stack.base = reinterpret_cast<Ref*>(smem_raw) + threadIdx.x;
-  const unsigned lane = threadIdx.x & 31u;
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(next, 32ull);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= n) break;
-    const uint64_t q = base + lane;
-    if (q < n) {
-      const f32x3 p{__ldcs(points + 3 * q), __ldcs(points + 3 * q + 1), __ldcs(points + 3 * q + 2)};
-      float best_d = scion::inf();
-      f32x3 best_p{0.0f, 0.0f, 0.0f};
-      uint32_t best_prim = SCION_MISS_PRIM;
-      uint32_t st = SCION_Q_OK;
-      Tally<COUNT> tally;
-      stack.sp = 0;
-      Ref cur = L::root(T);
-      for (;;) {
-        typename L::Node node;
-        const float d = cpq_node_distmin<L>(T, p, cur, node, tally);
-        bool descend = false;
-        if (d < best_d) {
-          if (node.variant == L::kLeaf) {
-            for (uint64_t i = node.data.begin; i < node.data.end; i++) {
-              float tri[9];
-              load_triangle36(T.buf[L::kBuf_primitives], i, tri);
-              const f32x3 c = closest_point_triangle(p, tri);
-              const f32x3 x = p - c;
-              const float d2 = dot(x, x);
-              tally.prim();
-              if (d2 < best_d) { best_d = d2; best_p = c; best_prim = (uint32_t)i; }
-            }
-          } else {
-            float ub;
-            if constexpr (L::kFamily == SCION_FAMILY_DOP14) ub = distmax_point_aabb(p, node.lo1, node.hi1);
-            else ub = distmax_point_aabb(p, node.low, node.high);
-            if (ub < best_d) best_d = ub;  // best = (upper_bound, best[1])
-            typename L::Node ln, rn;
-            const Ref left = node.left, right = node.right;
-            const float dl = cpq_node_distmin<L>(T, p, left, ln, tally);
-            const float dr = cpq_node_distmin<L>(T, p, right, rn, tally);
-            tally.stack((uint32_t)stack.sp + 2u);
-            if (stack.sp + 2 > SCION_STACK_DEPTH) { st = SCION_Q_STACK_OVERFLOW; break; }
-            if (dl < dr) { stack.push(right); cur = left; }
-            else { stack.push(left); cur = right; }
-            descend = true;
-          }
-        }
-        if (!descend) {
-          if (stack.sp == 0) break;
-          cur = stack.pop();
-        }
-      }
+  WorkFetcher work;
+  const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
+  const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
+  Tally<COUNT> tally;
+  int mode = kFetch;
+  uint64_t q = 0;
+  f32x3 p{0.0f, 0.0f, 0.0f}, best_p{0.0f, 0.0f, 0.0f};
+  float best_d = 0;
+  uint32_t best_prim = 0, st = 0, prim_i = 0, prim_end = 0;
+  Ref cur = L::root(T);
+
+  auto pop_or_finish = [&]() {
+    if (stack.sp == 0 || st != SCION_Q_OK) {
       out[q] = scion_cp{best_d, best_p.x, best_p.y, best_p.z, best_prim};
       if (status) status[q] = st;
       tally.store(counters, q);
+      mode = kFetch;
+    } else {
+      cur = stack.pop(sstack);
+      mode = kNode;
+    }
+  };
+
+  for (;;) {
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    if (idle) {
+      if (__popc(idle) >= refill_min || idle == kFullMask || work.exhausted) {
+        uint64_t nq;
+        if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
+          q = nq;
+          p = f32x3{__ldcs(points + 3 * q), __ldcs(points + 3 * q + 1), __ldcs(points + 3 * q + 2)};
+          best_d = scion::inf();
+          best_p = f32x3{0.0f, 0.0f, 0.0f};
+          best_prim = SCION_MISS_PRIM;
+          st = SCION_Q_OK;
+          tally.reset();
+          stack.sp = 0;
+          cur = L::root(T);
+          mode = kNode;
+        }
+        if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
+      }
+    }
+    if (mode == kNode) {
+      typename L::Node node;
+      const float d = cpq_node_distmin<L>(T, p, cur, node, tally);
+      if (!(d < best_d)) {
+        pop_or_finish();
+      } else if (node.variant == L::kLeaf) {
+        prim_i = (uint32_t)node.data.begin;
+        prim_end = (uint32_t)node.data.end;
+        if (prim_i < prim_end) mode = kPrim;
+        else pop_or_finish();
+      } else {
+        float ub;
+        if constexpr (L::kFamily == SCION_FAMILY_DOP14) ub = distmax_point_aabb(p, node.lo1, node.hi1);
+        else ub = distmax_point_aabb(p, node.low, node.high);
+        if (ub < best_d) best_d = ub;  // best = (upper_bound, best[1])
+        typename L::Node ln, rn;
+        const Ref left = node.left, right = node.right;
+        const float dl = cpq_node_distmin<L>(T, p, left, ln, tally);
+        const float dr = cpq_node_distmin<L>(T, p, right, rn, tally);
+        tally.stack((uint32_t)stack.sp + 2u);
+        if (stack.sp + 2 > SCION_STACK_DEPTH) {
+          st = SCION_Q_STACK_OVERFLOW;
+          pop_or_finish();
+        } else if (dl < dr) {
+          stack.push(sstack, right);
+          cur = left;
+        } else {
+          stack.push(sstack, left);
+          cur = right;
+        }
+      }
+    }
+    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    if (pmask) {
+      const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
+      if (run && mode == kPrim) {
+        float tri[9];
+        load_triangle36(T.buf[L::kBuf_primitives], prim_i, tri);
+        const f32x3 c = closest_point_triangle(p, tri);
+        const f32x3 x = p - c;
+        const float d2 = dot(x, x);
+        tally.prim();
+        if (d2 < best_d) { best_d = d2; best_p = c; best_prim = prim_i; }
+        if (++prim_i == prim_end) pop_or_finish();
+      }
     }
   }
 }

@@ -80,7 +80,38 @@ def timing(G, nrays, layouts):
             print(f"  {name:14s} {kind:9s} {nrays/ms/1e3:9.1f} Mrays/s  ({ms:.2f} ms)  encode {t4-t3:.2f}s bytes/prim {pt.node_bytes/lt.nprims:.1f}", flush=True)
         dt.free()
 
+def tune(G, nrays, layouts):
+    scene = sb.Scene.terrain(G, seed=3)
+    lt = scene.build_sah(32, 4).collapse8()
+    lo, hi = scene.bounds()
+    cam = sb.default_camera(lo, hi, True, 4096, 4096)
+    d_rays = dbuf(nrays * 32); d_hits = dbuf(nrays * 8)
+    for name in layouts:
+        dt = lt.encode(name).upload(0)
+        for kind in ("primary", "secondary"):
+            if kind == "primary": sb.gen_primary(cam, 0, nrays, d_rays.data_ptr())
+            else: dt.gen_secondary(77, 0, nrays, d_rays.data_ptr())
+            torch.cuda.synchronize()
+            res = []
+            for refill in (1, 4, 8, 16):
+                for prim in (1, 4, 8, 12, 16, 24):
+                    v = refill | (prim << 8)
+                    dt.closest_hit(d_rays.data_ptr(), nrays, d_hits.data_ptr(), variant=v)
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(2): dt.closest_hit(d_rays.data_ptr(), nrays, d_hits.data_ptr(), variant=v)
+                    e1.record(); torch.cuda.synchronize()
+                    res.append((nrays / (e0.elapsed_time(e1) / 2) / 1e3, refill, prim))
+            res.sort(reverse=True)
+            print(f"  {name:12s} {kind:9s} best: " + ", ".join(f"{m:.0f}(r{r},p{p})" for m, r, p in res[:5]) + " | worst: " + ", ".join(f"{m:.0f}(r{r},p{p})" for m, r, p in res[-3:]), flush=True)
+        dt.free()
+
 if __name__ == "__main__":
+    if "--tune" in sys.argv:
+        tune(708, 1 << 23, ["pbrt", "pbrt-q16", "bvh8-q8-ci"])
+        tune(2236, 1 << 23, ["pbrt-q16"])
+        sys.exit(0)
     print(torch.cuda.get_device_name(0))
     ok = parity(40, 128, 8192)
     print("PARITY", "OK" if ok else "FAILED", flush=True)
