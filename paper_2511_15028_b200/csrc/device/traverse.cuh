@@ -43,14 +43,16 @@ struct HybridStack {
                                    ? (kStackSmemBytesPerBlock / kBlockThreads / (int)sizeof(Entry))
                                    : SCION_STACK_DEPTH;
   static constexpr int kDeep = SCION_STACK_DEPTH - kSmem > 0 ? SCION_STACK_DEPTH - kSmem : 1;
+  // `sp` is deliberately NOT a member: the struct holds a dynamically indexed array and therefore
+  // lives in local memory; a member counter would be re-loaded / re-stored around every access
+  // (seen as STL/LDL pairs in profiles/r1_ncu_v2_c5_q16_*).
   Entry deep[kDeep];
-  int sp = 0;
-  SCION_DEV void push(Entry* smem, const Entry& r) {
+  SCION_DEV void push(Entry* smem, int& sp, const Entry& r) {
     if (sp < kSmem) smem[sp * kBlockThreads + threadIdx.x] = r;
     else deep[sp - kSmem] = r;
     sp++;
   }
-  SCION_DEV Entry pop(Entry* smem) {
+  SCION_DEV Entry pop(Entry* smem, int& sp) {
     sp--;
     return sp < kSmem ? smem[sp * kBlockThreads + threadIdx.x] : deep[sp - kSmem];
   }
@@ -121,6 +123,76 @@ SCION_DEV void test_triangle(const TreeView& T, const RayCtx& ray, uint32_t i, f
   }
 }
 
+// Warp-cooperative leaf processing.  Every lane with has=true owns a pending primitive range
+// [prim_i, prim_end) of its own ray; the (owner, primitive) pairs of ALL owners are spread over
+// the 32 lanes so that each lane runs one Moeller-Trumbore test per round for some owner's ray
+// (ray fetched by shuffle).  Owners then fold their results in ascending primitive order with the
+// reference's strict `t < best` rule, which is exactly the sequential foreach of chrt.scion:10-15
+// (each test is a pure function of (ray, triangle); only the fold depends on order).
+struct CoopScratch {
+  uint8_t owner[32];
+  uint8_t k[32];
+  float t[32];
+};
+template <class L>
+SCION_DEV uint32_t coop_triangles(const TreeView& T, bool has, const RayCtx& ray, uint32_t& prim_i, uint32_t prim_end, float& best_t,
+                                  uint32_t& best_prim, CoopScratch& sc) {
+  static_assert(L::kStride_primitives == 36, "Triangle stride");
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t tested = 0;
+  for (;;) {
+    const uint32_t remaining = has ? prim_end - prim_i : 0u;
+    if (__ballot_sync(kFullMask, remaining != 0u) == 0u) break;
+    const uint32_t c = remaining < 32u ? remaining : 32u;
+    uint32_t incl = c;  // inclusive prefix sum over lanes
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFullMask, incl, d);
+      if (lane >= (unsigned)d) incl += v;
+    }
+    const uint32_t excl = incl - c;
+    const uint32_t total = __shfl_sync(kFullMask, incl, 31);
+    const uint32_t take = excl >= 32u ? 0u : (c < 32u - excl ? c : 32u - excl);
+    for (uint32_t k = 0; k < take; k++) {
+      sc.owner[excl + k] = (uint8_t)lane;
+      sc.k[excl + k] = (uint8_t)k;
+    }
+    __syncwarp();
+    const bool work = lane < (total < 32u ? total : 32u);
+    const unsigned o = work ? sc.owner[lane] : 0u;
+    const uint32_t kk = work ? sc.k[lane] : 0u;
+    RayCtx r;
+    r.ox = __shfl_sync(kFullMask, ray.ox, o);
+    r.oy = __shfl_sync(kFullMask, ray.oy, o);
+    r.oz = __shfl_sync(kFullMask, ray.oz, o);
+    r.tmax = __shfl_sync(kFullMask, ray.tmax, o);
+    r.dx = __shfl_sync(kFullMask, ray.dx, o);
+    r.dy = __shfl_sync(kFullMask, ray.dy, o);
+    r.dz = __shfl_sync(kFullMask, ray.dz, o);
+    const uint32_t pi = __shfl_sync(kFullMask, prim_i, o) + kk;
+    float t = scion::inf();
+    if (work) {
+      float tri[9];
+      load_triangle36(T.buf[L::kBuf_primitives], pi, tri);
+      float th;
+      if (ray_tri_mt(r, tri, th)) t = th;
+      sc.t[lane] = t;
+    }
+    __syncwarp();
+    for (uint32_t k = 0; k < take; k++) {
+      const float th = sc.t[excl + k];
+      if (th < best_t) {  // a miss is +inf and never passes
+        best_t = th;
+        best_prim = prim_i + k;
+      }
+    }
+    prim_i += take;
+    tested += take;
+    __syncwarp();
+  }
+  return tested;
+}
+
 // bounds test of one binary / DOP node against the ray.  Loads the cold segment only when the
 // reference semantics would evaluate it (dop.scion:20-21 `if I {...}`).
 template <class L, class TallyT>
@@ -159,12 +231,14 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
   using Ref = typename L::Ref;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Ref* const sstack = reinterpret_cast<Ref*>(smem_raw);
+  __shared__ CoopScratch coop[kBlockThreads / 32];
   HybridStack<Ref> stack;
   WorkFetcher work;
   const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
   const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
   Tally<COUNT> tally;
   int mode = kFetch;
+  int sp = 0;
   uint64_t q = 0;
   RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
   float best_t = 0;
@@ -173,13 +247,13 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
 
   // retire the lane's query or continue with the next pending subtree
   auto pop_or_finish = [&]() {
-    if (stack.sp == 0 || st != SCION_Q_OK) {
+    if (sp == 0 || st != SCION_Q_OK) {
       hits[q] = scion_hit{best_t, best_prim};
       if (status) status[q] = st;
       tally.store(counters, q);
       mode = kFetch;
     } else {
-      cur = stack.pop(sstack);
+      cur = stack.pop(sstack, sp);
       mode = kNode;
     }
   };
@@ -197,7 +271,7 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
           best_prim = SCION_MISS_PRIM;
           st = SCION_Q_OK;
           tally.reset();
-          stack.sp = 0;
+          sp = 0;
           cur = L::root(T);
           mode = kNode;
         }
@@ -218,12 +292,12 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
         else pop_or_finish();
       } else if (hit && t_near < best_t) {
         // reference discipline: pop self, push right, push left => occupancy sp + 2
-        tally.stack((uint32_t)stack.sp + 2u);
-        if (stack.sp + 2 > SCION_STACK_DEPTH) {
+        tally.stack((uint32_t)sp + 2u);
+        if (sp + 2 > SCION_STACK_DEPTH) {
           st = SCION_Q_STACK_OVERFLOW;
           pop_or_finish();
         } else {
-          stack.push(sstack, node.right);
+          stack.push(sstack, sp, node.right);
           cur = node.left;
         }
       } else {
@@ -234,10 +308,11 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
     const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
     if (pmask) {
       const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
-      if (run && mode == kPrim) {
-        tally.prim();
-        test_triangle<L>(T, ray, prim_i, best_t, best_prim);
-        if (++prim_i == prim_end) pop_or_finish();
+      if (run) {  // warp-uniform
+        const bool own = mode == kPrim;
+        const uint32_t done = coop_triangles<L>(T, own, ray, prim_i, prim_end, best_t, best_prim, coop[threadIdx.x >> 5]);
+        if (COUNT) tally.prim_tests += done;
+        if (own) pop_or_finish();
       }
     }
   }
@@ -262,12 +337,14 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
   using Entry = WideEntry<Ref>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Entry* const sstack = reinterpret_cast<Entry*>(smem_raw);
+  __shared__ CoopScratch coop[kBlockThreads / 32];
   HybridStack<Entry> stack;
   WorkFetcher work;
   const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
   const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
   Tally<COUNT> tally;
   int mode = kFetch;
+  int sp = 0;
   uint64_t q = 0;
   RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
   float best_t = 0;
@@ -277,8 +354,8 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
   auto pop_or_finish = [&]() {
     bool found = false;
     if (st == SCION_Q_OK) {
-      while (stack.sp > 0) {
-        const Entry e = stack.pop(sstack);
+      while (sp > 0) {
+        const Entry e = stack.pop(sstack, sp);
         if (e.t_near < best_t) { cur = e.ref; found = true; break; }
       }
     }
@@ -304,7 +381,7 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
           best_prim = SCION_MISS_PRIM;
           st = SCION_Q_OK;
           tally.reset();
-          stack.sp = 0;
+          sp = 0;
           cur = L::root(T);
           mode = kNode;
         }
@@ -331,13 +408,13 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
           if (interval_intersects(ray, some, tn[k], t_far) && tn[k] < best_t) mask |= 1u << k;
         }
         const int m = __popc(mask);
-        tally.stack((uint32_t)(stack.sp + m));
-        if (stack.sp + m > SCION_STACK_DEPTH) {
+        tally.stack((uint32_t)(sp + m));
+        if (sp + m > SCION_STACK_DEPTH) {
           st = SCION_Q_STACK_OVERFLOW;
         } else {
 #pragma unroll
           for (int k = 7; k >= 0; k--)
-            if (mask & (1u << k)) stack.push(sstack, Entry{node.children[k], tn[k]});
+            if (mask & (1u << k)) stack.push(sstack, sp, Entry{node.children[k], tn[k]});
         }
         pop_or_finish();
       }
@@ -345,10 +422,11 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
     const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
     if (pmask) {
       const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
-      if (run && mode == kPrim) {
-        tally.prim();
-        test_triangle<L>(T, ray, prim_i, best_t, best_prim);
-        if (++prim_i == prim_end) pop_or_finish();
+      if (run) {  // warp-uniform
+        const bool own = mode == kPrim;
+        const uint32_t done = coop_triangles<L>(T, own, ray, prim_i, prim_end, best_t, best_prim, coop[threadIdx.x >> 5]);
+        if (COUNT) tally.prim_tests += done;
+        if (own) pop_or_finish();
       }
     }
   }
@@ -382,6 +460,7 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
   const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
   Tally<COUNT> tally;
   int mode = kFetch;
+  int sp = 0;
   uint64_t q = 0;
   f32x3 p{0.0f, 0.0f, 0.0f}, best_p{0.0f, 0.0f, 0.0f};
   float best_d = 0;
@@ -389,13 +468,13 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
   Ref cur = L::root(T);
 
   auto pop_or_finish = [&]() {
-    if (stack.sp == 0 || st != SCION_Q_OK) {
+    if (sp == 0 || st != SCION_Q_OK) {
       out[q] = scion_cp{best_d, best_p.x, best_p.y, best_p.z, best_prim};
       if (status) status[q] = st;
       tally.store(counters, q);
       mode = kFetch;
     } else {
-      cur = stack.pop(sstack);
+      cur = stack.pop(sstack, sp);
       mode = kNode;
     }
   };
@@ -413,7 +492,7 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
           best_prim = SCION_MISS_PRIM;
           st = SCION_Q_OK;
           tally.reset();
-          stack.sp = 0;
+          sp = 0;
           cur = L::root(T);
           mode = kNode;
         }
@@ -439,15 +518,15 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
         const Ref left = node.left, right = node.right;
         const float dl = cpq_node_distmin<L>(T, p, left, ln, tally);
         const float dr = cpq_node_distmin<L>(T, p, right, rn, tally);
-        tally.stack((uint32_t)stack.sp + 2u);
-        if (stack.sp + 2 > SCION_STACK_DEPTH) {
+        tally.stack((uint32_t)sp + 2u);
+        if (sp + 2 > SCION_STACK_DEPTH) {
           st = SCION_Q_STACK_OVERFLOW;
           pop_or_finish();
         } else if (dl < dr) {
-          stack.push(sstack, right);
+          stack.push(sstack, sp, right);
           cur = left;
         } else {
-          stack.push(sstack, left);
+          stack.push(sstack, sp, left);
           cur = right;
         }
       }
