@@ -39,22 +39,48 @@ constexpr int kPrimMin = 8;     // run the PRIM phase when at least this many la
 constexpr int kStackSmemBytesPerBlock = 16 * 1024;
 template <class Entry>
 struct HybridStack {
+  static_assert(sizeof(Entry) % 4 == 0, "stack entries are stored as 32-bit words");
+  static constexpr int kWords = (int)sizeof(Entry) / 4;
   static constexpr int kSmem = (kStackSmemBytesPerBlock / kBlockThreads / (int)sizeof(Entry)) < SCION_STACK_DEPTH
                                    ? (kStackSmemBytesPerBlock / kBlockThreads / (int)sizeof(Entry))
                                    : SCION_STACK_DEPTH;
   static constexpr int kDeep = SCION_STACK_DEPTH - kSmem > 0 ? SCION_STACK_DEPTH - kSmem : 1;
+  static constexpr uint32_t kEntryStride = kBlockThreads * (uint32_t)sizeof(Entry);  // bytes between entry e and e+1 of one thread
   // `sp` is deliberately NOT a member: the struct holds a dynamically indexed array and therefore
   // lives in local memory; a member counter would be re-loaded / re-stored around every access
-  // (seen as STL/LDL pairs in profiles/r1_ncu_v2_c5_q16_*).
+  // (seen as STL/LDL pairs in profiles/r1_ncu_v2_c5_q16.txt).  The shared-memory part is addressed
+  // through a precomputed 32-bit shared-space address + st.shared/ld.shared: the generic-pointer
+  // form re-derived the window base (S2R/LEA chain, 18 SASS instructions per push) every time.
   Entry deep[kDeep];
-  SCION_DEV void push(Entry* smem, int& sp, const Entry& r) {
-    if (sp < kSmem) smem[sp * kBlockThreads + threadIdx.x] = r;
-    else deep[sp - kSmem] = r;
+  uint32_t base;  // shared-space byte address of this thread's entry 0
+  SCION_DEV void init(void* smem_generic) {
+    base = (uint32_t)__cvta_generic_to_shared(smem_generic) + threadIdx.x * (uint32_t)sizeof(Entry);
+  }
+  SCION_DEV void push(int& sp, const Entry& r) {
+    if (sp < kSmem) {
+      uint32_t w[kWords];
+      memcpy(w, &r, sizeof(Entry));
+      const uint32_t a = base + (uint32_t)sp * kEntryStride;
+#pragma unroll
+      for (int i = 0; i < kWords; i++) asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + 4u * i), "r"(w[i]) : "memory");
+    } else {
+      deep[sp - kSmem] = r;
+    }
     sp++;
   }
-  SCION_DEV Entry pop(Entry* smem, int& sp) {
+  SCION_DEV Entry pop(int& sp) {
     sp--;
-    return sp < kSmem ? smem[sp * kBlockThreads + threadIdx.x] : deep[sp - kSmem];
+    Entry r;
+    if (sp < kSmem) {
+      uint32_t w[kWords];
+      const uint32_t a = base + (uint32_t)sp * kEntryStride;
+#pragma unroll
+      for (int i = 0; i < kWords; i++) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(a + 4u * i) : "memory");
+      memcpy(&r, w, sizeof(Entry));
+    } else {
+      r = deep[sp - kSmem];
+    }
+    return r;
   }
 };
 
@@ -220,6 +246,15 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
 }
 
 enum : int { kFetch = 0, kNode = 1, kPrim = 2 };
+constexpr uint32_t kFetchEvery = 2;  // look for idle lanes every kFetchEvery-th iteration
+constexpr uint32_t kPrimEvery = 4;   // look for waiting PRIM lanes every kPrimEvery-th iteration
+
+// keeps the result-store address arithmetic inside the (rare) retire branch instead of letting the
+// compiler hoist it into every loop iteration (9 SASS instructions per iteration in v3)
+SCION_DEV uint64_t opaque(uint64_t q) {
+  asm volatile("" : "+l"(q));
+  return q;
+}
 
 // ------------------------------------------------------------------------------------------
 // closest_hit, binary + DOP-14 families
@@ -230,12 +265,11 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Ref* const sstack = reinterpret_cast<Ref*>(smem_raw);
   __shared__ CoopScratch coop[kBlockThreads / 32];
   HybridStack<Ref> stack;
+  stack.init(smem_raw);
   WorkFetcher work;
-  const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
-  const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
+  (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
   int sp = 0;
@@ -248,21 +282,22 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
   // retire the lane's query or continue with the next pending subtree
   auto pop_or_finish = [&]() {
     if (sp == 0 || st != SCION_Q_OK) {
-      hits[q] = scion_hit{best_t, best_prim};
-      if (status) status[q] = st;
-      tally.store(counters, q);
+      const uint64_t qq = opaque(q);
+      hits[qq] = scion_hit{best_t, best_prim};
+      if (status) status[qq] = st;
+      tally.store(counters, qq);
       mode = kFetch;
     } else {
-      cur = stack.pop(sstack, sp);
+      cur = stack.pop(sp);
       mode = kNode;
     }
   };
 
-  for (;;) {
+  for (uint32_t it = 0;; it++) {
     // ---- FETCH: refill idle lanes
-    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    const unsigned idle = (it % kFetchEvery) == 0u ? __ballot_sync(kFullMask, mode == kFetch) : 0u;
     if (idle) {
-      if (__popc(idle) >= refill_min || idle == kFullMask || work.exhausted) {
+      if (__popc(idle) >= kRefillMin || idle == kFullMask || work.exhausted) {
         uint64_t nq;
         if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
           q = nq;
@@ -297,7 +332,7 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
           st = SCION_Q_STACK_OVERFLOW;
           pop_or_finish();
         } else {
-          stack.push(sstack, sp, node.right);
+          stack.push(sp, node.right);
           cur = node.left;
         }
       } else {
@@ -305,9 +340,9 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
       }
     }
     // ---- PRIM: one primitive per waiting lane, batched
-    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    const unsigned pmask = (it % kPrimEvery) == kPrimEvery - 1u ? __ballot_sync(kFullMask, mode == kPrim) : 0u;
     if (pmask) {
-      const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
+      const bool run = __popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u;
       if (run) {  // warp-uniform
         const bool own = mode == kPrim;
         const uint32_t done = coop_triangles<L>(T, own, ray, prim_i, prim_end, best_t, best_prim, coop[threadIdx.x >> 5]);
@@ -336,12 +371,11 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
   using Ref = typename L::Ref;
   using Entry = WideEntry<Ref>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Entry* const sstack = reinterpret_cast<Entry*>(smem_raw);
   __shared__ CoopScratch coop[kBlockThreads / 32];
   HybridStack<Entry> stack;
+  stack.init(smem_raw);
   WorkFetcher work;
-  const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
-  const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
+  (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
   int sp = 0;
@@ -355,24 +389,25 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
     bool found = false;
     if (st == SCION_Q_OK) {
       while (sp > 0) {
-        const Entry e = stack.pop(sstack, sp);
+        const Entry e = stack.pop(sp);
         if (e.t_near < best_t) { cur = e.ref; found = true; break; }
       }
     }
     if (found) {
       mode = kNode;
     } else {
-      hits[q] = scion_hit{best_t, best_prim};
-      if (status) status[q] = st;
-      tally.store(counters, q);
+      const uint64_t qq = opaque(q);
+      hits[qq] = scion_hit{best_t, best_prim};
+      if (status) status[qq] = st;
+      tally.store(counters, qq);
       mode = kFetch;
     }
   };
 
-  for (;;) {
-    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+  for (uint32_t it = 0;; it++) {
+    const unsigned idle = (it % kFetchEvery) == 0u ? __ballot_sync(kFullMask, mode == kFetch) : 0u;
     if (idle) {
-      if (__popc(idle) >= refill_min || idle == kFullMask || work.exhausted) {
+      if (__popc(idle) >= kRefillMin || idle == kFullMask || work.exhausted) {
         uint64_t nq;
         if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
           q = nq;
@@ -414,14 +449,14 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
         } else {
 #pragma unroll
           for (int k = 7; k >= 0; k--)
-            if (mask & (1u << k)) stack.push(sstack, sp, Entry{node.children[k], tn[k]});
+            if (mask & (1u << k)) stack.push(sp, Entry{node.children[k], tn[k]});
         }
         pop_or_finish();
       }
     }
-    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    const unsigned pmask = (it % kPrimEvery) == kPrimEvery - 1u ? __ballot_sync(kFullMask, mode == kPrim) : 0u;
     if (pmask) {
-      const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
+      const bool run = __popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u;
       if (run) {  // warp-uniform
         const bool own = mode == kPrim;
         const uint32_t done = coop_triangles<L>(T, own, ray, prim_i, prim_end, best_t, best_prim, coop[threadIdx.x >> 5]);
@@ -453,11 +488,10 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Ref* const sstack = reinterpret_cast<Ref*>(smem_raw);
   HybridStack<Ref> stack;
+  stack.init(smem_raw);
   WorkFetcher work;
-  const int refill_min = (tune & 0xff) ? (tune & 0xff) : kRefillMin;
-  const int prim_min = ((tune >> 8) & 0xff) ? ((tune >> 8) & 0xff) : kPrimMin;
+  (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
   int sp = 0;
@@ -469,20 +503,21 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
 
   auto pop_or_finish = [&]() {
     if (sp == 0 || st != SCION_Q_OK) {
-      out[q] = scion_cp{best_d, best_p.x, best_p.y, best_p.z, best_prim};
-      if (status) status[q] = st;
-      tally.store(counters, q);
+      const uint64_t qq = opaque(q);
+      out[qq] = scion_cp{best_d, best_p.x, best_p.y, best_p.z, best_prim};
+      if (status) status[qq] = st;
+      tally.store(counters, qq);
       mode = kFetch;
     } else {
-      cur = stack.pop(sstack, sp);
+      cur = stack.pop(sp);
       mode = kNode;
     }
   };
 
-  for (;;) {
-    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+  for (uint32_t it = 0;; it++) {
+    const unsigned idle = (it % kFetchEvery) == 0u ? __ballot_sync(kFullMask, mode == kFetch) : 0u;
     if (idle) {
-      if (__popc(idle) >= refill_min || idle == kFullMask || work.exhausted) {
+      if (__popc(idle) >= kRefillMin || idle == kFullMask || work.exhausted) {
         uint64_t nq;
         if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
           q = nq;
@@ -523,17 +558,17 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
           st = SCION_Q_STACK_OVERFLOW;
           pop_or_finish();
         } else if (dl < dr) {
-          stack.push(sstack, sp, right);
+          stack.push(sp, right);
           cur = left;
         } else {
-          stack.push(sstack, sp, left);
+          stack.push(sp, left);
           cur = right;
         }
       }
     }
-    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    const unsigned pmask = (it % kPrimEvery) == kPrimEvery - 1u ? __ballot_sync(kFullMask, mode == kPrim) : 0u;
     if (pmask) {
-      const bool run = __popc(pmask) >= prim_min || __ballot_sync(kFullMask, mode == kNode) == 0u;
+      const bool run = __popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u;
       if (run && mode == kPrim) {
         float tri[9];
         load_triangle36(T.buf[L::kBuf_primitives], prim_i, tri);
