@@ -204,12 +204,15 @@ def main():
         raise SystemExit("bench.py needs a CUDA device: the B200 backend has no CPU fallback (use --impl reference for the CPU arm)")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    force_dist = os.environ.get("SCION_FORCE_DIST") == "1"  # exercise the NCCL code path with a single rank (tests)
+    if world > 1 or force_dist:
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29511", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__ as g
     if rank == 0:
         g.build()
-    if world > 1:
+    if world > 1 or force_dist:
         dist.barrier()
     import paper_2511_15028_b200 as sb
     import paper_2511_15028_b200.workloads as W
@@ -221,7 +224,7 @@ def main():
     if rank == 0:
         _, _, wl, scene, ltree, lo, hi, build_s = build_host_side(args, args.workload)
         bounds = torch.tensor(list(lo) + list(hi), dtype=torch.float64, device=dev)
-    if world > 1:
+    if world > 1 or force_dist:
         dist.broadcast(bounds, 0)
     b = bounds.cpu().numpy().astype(np.float32)
     lo, hi = b[:3], b[3:]
@@ -239,7 +242,7 @@ def main():
             pt = ltree.encode(layout)
             nbytes[0] = pt.image_bytes
             enc_s = time.time() - t0
-        if world > 1:
+        if world > 1 or force_dist:
             dist.broadcast(nbytes, 0)
         img = torch.empty(int(nbytes.item()) + 256, dtype=torch.uint8, device=dev)
         off = (-img.data_ptr()) % 256
@@ -247,7 +250,7 @@ def main():
         tb0 = time.time()
         if rank == 0:
             dt = pt.upload_into(local_rank, ptr, int(nbytes.item()))
-        if world > 1:
+        if world > 1 or force_dist:
             dist.broadcast(img[off:off + int(nbytes.item())], 0)
             torch.cuda.synchronize()
         if rank != 0:
@@ -269,7 +272,7 @@ def main():
         for _ in range(warmup):
             run_step(dt)
         torch.cuda.synchronize()
-        if world > 1:
+        if world > 1 or force_dist:
             dist.barrier()
         torch.cuda.synchronize()
         if sampler:
@@ -283,10 +286,10 @@ def main():
         torch.cuda.synchronize()
         launches = sb.kernel_launches() - l0
         clocks = sampler.stop() if sampler else None
-        if world > 1:
+        if world > 1 or force_dist:
             dist.barrier()
         ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
-        if world > 1:
+        if world > 1 or force_dist:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item()), launches, clocks
 
@@ -300,7 +303,7 @@ def main():
         torch.cuda.synchronize()
         sums = d_ctr.view(-1, 4).sum(dim=0, dtype=torch.int64)
         errors = int((d_st != 0).sum().item())
-        if world > 1:
+        if world > 1 or force_dist:
             dist.all_reduce(sums)
         s = sums.cpu().numpy().astype(np.float64) / wl.total
         mean = np.zeros(1, sb.COUNTERS_DTYPE)
@@ -373,7 +376,7 @@ def main():
 
     # ---- gather of hit records: all ranks -> every rank, checksum of checksums
     gather = None
-    if world > 1:
+    if world > 1 or force_dist:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         sizes = [sb.partition(wl.total, r, world)[1] * r_bytes for r in range(world)]
@@ -416,7 +419,7 @@ def main():
         if gather:
             line["gather"] = gather
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or force_dist:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscion_b200.so")
+LIB_PATH = os.environ.get("SCION_B200_LIB", os.path.join(_HERE, "libscion_b200.so"))  # env override: kernel-variant experiments
 
 
 class ScionError(RuntimeError):

@@ -433,24 +433,23 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
         else pop_or_finish();
       } else {
         tally.visit();
-        // test all eight child boxes; push the passing ones in reverse slot order
-        uint32_t mask = 0;
-        float tn[8];
+        // test the eight child boxes from slot 7 down to slot 0 and push the passing ones as they
+        // are found: the stack then pops them in slot order (chrt8.scion:7 `foreach c in children`).
+        // Occupancy after the last push is sp + #passing, the same figure the all-at-once form checks.
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-          float t_far;
-          const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn[k], t_far);
-          if (interval_intersects(ray, some, tn[k], t_far) && tn[k] < best_t) mask |= 1u << k;
+        for (int k = 7; k >= 0; k--) {
+          float tn, t_far;
+          const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn, t_far);
+          if (interval_intersects(ray, some, tn, t_far) && tn < best_t && st == SCION_Q_OK) {
+            if (sp + 1 > SCION_STACK_DEPTH) {
+              st = SCION_Q_STACK_OVERFLOW;
+              tally.stack((uint32_t)sp + 1u);
+            } else {
+              stack.push(sp, Entry{node.children[k], tn});
+            }
+          }
         }
-        const int m = __popc(mask);
-        tally.stack((uint32_t)(sp + m));
-        if (sp + m > SCION_STACK_DEPTH) {
-          st = SCION_Q_STACK_OVERFLOW;
-        } else {
-#pragma unroll
-          for (int k = 7; k >= 0; k--)
-            if (mask & (1u << k)) stack.push(sp, Entry{node.children[k], tn[k]});
-        }
+        tally.stack((uint32_t)sp);
         pop_or_finish();
       }
     }
