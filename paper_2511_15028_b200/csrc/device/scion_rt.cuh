@@ -316,6 +316,14 @@ SCION_HOSTDEV uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t shift_bits) {
 #endif
 }
 
+SCION_HOSTDEV void prefetch_l2(const void* p) {
+#if defined(__CUDA_ARCH__)
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#else
+  (void)p;
+#endif
+}
+
 // Load one planned element of BYTES bytes whose address is known to be ALIGN-aligned
 // (ALIGN = gcd of the buffer base alignment, the segment base and the stride, computed by
 // emit_cuda).  16-byte read-only vector loads whenever the plan allows them; 8- and 4-byte

@@ -28,15 +28,24 @@
 
 namespace scion {
 
+#ifndef SCION_MINB2
+#define SCION_MINB2 9   /* 56 registers, 36 warps/SM: +7 % over the compiler's own 61-63 (8 blocks); 10 blocks (48 regs) spills and halves throughput */
+#endif
+#ifndef SCION_CHUNK
+#define SCION_CHUNK 128
+#endif
+#ifndef SCION_STACK_SMEM
+#define SCION_STACK_SMEM (16 * 1024)
+#endif
 constexpr int kBlockThreads = 128;
 constexpr unsigned kFullMask = 0xffffffffu;
-constexpr int kChunk = 256;     // queries a warp takes from the global counter at a time
+constexpr int kChunk = SCION_CHUNK;     // queries a warp takes from the global counter at a time
 constexpr int kRefillMin = 4;   // refill when at least this many lanes are idle (or all of them)
 constexpr int kPrimMin = 8;     // run the PRIM phase when at least this many lanes wait in it
 
 // Hybrid traversal stack (see header comment).  kSmem is sized so that one CTA uses 16 KB of
 // shared memory whatever the entry size.
-constexpr int kStackSmemBytesPerBlock = 16 * 1024;
+constexpr int kStackSmemBytesPerBlock = SCION_STACK_SMEM;
 template <class Entry>
 struct HybridStack {
   static_assert(sizeof(Entry) % 4 == 0, "stack entries are stored as 32-bit words");
@@ -219,6 +228,67 @@ SCION_DEV uint32_t coop_triangles(const TreeView& T, bool has, const RayCtx& ray
   return tested;
 }
 
+// Cooperative leaf phase of closest_point (cpq.scion:25-31): same scheme as coop_triangles, the
+// worker returns (d2, closest point); owners fold with the strict `d2 < best[0]` rule in order.
+struct CoopScratchCp {
+  uint8_t owner[32];
+  uint8_t k[32];
+  float d2[32];
+  float c[32][3];
+};
+template <class L>
+SCION_DEV uint32_t coop_points(const TreeView& T, bool has, const f32x3& p, uint32_t& prim_i, uint32_t prim_end, float& best_d, f32x3& best_p,
+                               uint32_t& best_prim, CoopScratchCp& sc) {
+  static_assert(L::kStride_primitives == 36, "Triangle stride");
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t tested = 0;
+  for (;;) {
+    const uint32_t remaining = has ? prim_end - prim_i : 0u;
+    if (__ballot_sync(kFullMask, remaining != 0u) == 0u) break;
+    const uint32_t c = remaining < 32u ? remaining : 32u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFullMask, incl, d);
+      if (lane >= (unsigned)d) incl += v;
+    }
+    const uint32_t excl = incl - c;
+    const uint32_t total = __shfl_sync(kFullMask, incl, 31);
+    const uint32_t take = excl >= 32u ? 0u : (c < 32u - excl ? c : 32u - excl);
+    for (uint32_t k = 0; k < take; k++) {
+      sc.owner[excl + k] = (uint8_t)lane;
+      sc.k[excl + k] = (uint8_t)k;
+    }
+    __syncwarp();
+    const bool work = lane < (total < 32u ? total : 32u);
+    const unsigned o = work ? sc.owner[lane] : 0u;
+    const uint32_t kk = work ? sc.k[lane] : 0u;
+    const f32x3 q{__shfl_sync(kFullMask, p.x, o), __shfl_sync(kFullMask, p.y, o), __shfl_sync(kFullMask, p.z, o)};
+    const uint32_t pi = __shfl_sync(kFullMask, prim_i, o) + kk;
+    if (work) {
+      float tri[9];
+      load_triangle36(T.buf[L::kBuf_primitives], pi, tri);
+      const f32x3 cp = closest_point_triangle(q, tri);
+      const f32x3 x = q - cp;
+      sc.d2[lane] = dot(x, x);
+      sc.c[lane][0] = cp.x; sc.c[lane][1] = cp.y; sc.c[lane][2] = cp.z;
+    }
+    __syncwarp();
+    for (uint32_t k = 0; k < take; k++) {
+      const float d2 = sc.d2[excl + k];
+      if (d2 < best_d) {
+        best_d = d2;
+        best_p = f32x3{sc.c[excl + k][0], sc.c[excl + k][1], sc.c[excl + k][2]};
+        best_prim = prim_i + k;
+      }
+    }
+    prim_i += take;
+    tested += take;
+    __syncwarp();
+  }
+  return tested;
+}
+
 // bounds test of one binary / DOP node against the ray.  Loads the cold segment only when the
 // reference semantics would evaluate it (dop.scion:20-21 `if I {...}`).
 template <class L, class TallyT>
@@ -246,6 +316,11 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
 }
 
 enum : int { kFetch = 0, kNode = 1, kPrim = 2 };
+#ifndef SCION_PREFETCH
+#define SCION_PREFETCH 1
+#endif
+constexpr bool kPrefetch = SCION_PREFETCH != 0;  // L2-prefetch a node record when its reference is pushed (+3-4 % on C5, binary)
+constexpr bool kPrefetchWide = false;             // 8-wide: up to 8 prefetches per node, most culled later: -4 % on C5
 constexpr uint32_t kFetchEvery = 2;  // look for idle lanes every kFetchEvery-th iteration
 constexpr uint32_t kPrimEvery = 4;   // look for waiting PRIM lanes every kPrimEvery-th iteration
 
@@ -260,7 +335,7 @@ SCION_DEV uint64_t opaque(uint64_t q) {
 // closest_hit, binary + DOP-14 families
 // ------------------------------------------------------------------------------------------
 template <class L, bool COUNT>
-__global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
+__global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
@@ -333,6 +408,7 @@ __global__ void __launch_bounds__(kBlockThreads) chrt2_kernel(const TreeView T, 
           pop_or_finish();
         } else {
           stack.push(sp, node.right);
+          if (kPrefetch) L::prefetch(T, node.right);
           cur = node.left;
         }
       } else {
@@ -364,8 +440,11 @@ struct WideEntry {
   float t_near;
 };
 
+#ifndef SCION_MINB8
+#define SCION_MINB8 4
+#endif
 template <class L, bool COUNT>
-__global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
+__global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
@@ -446,6 +525,7 @@ __global__ void __launch_bounds__(kBlockThreads) chrt8_kernel(const TreeView T, 
               tally.stack((uint32_t)sp + 1u);
             } else {
               stack.push(sp, Entry{node.children[k], tn});
+              if (kPrefetchWide) L::prefetch(T, node.children[k]);
             }
           }
         }
@@ -482,7 +562,7 @@ SCION_DEV float cpq_node_distmin(const TreeView& T, const f32x3& p, const typena
 }
 
 template <class L, bool COUNT>
-__global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
+__global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
                                                              scion_cp* __restrict__ out, uint32_t* __restrict__ status,
                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
@@ -495,6 +575,7 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
   int mode = kFetch;
   int sp = 0;
   uint64_t q = 0;
+  __shared__ CoopScratchCp coop[kBlockThreads / 32];
   f32x3 p{0.0f, 0.0f, 0.0f}, best_p{0.0f, 0.0f, 0.0f};
   float best_d = 0;
   uint32_t best_prim = 0, st = 0, prim_i = 0, prim_end = 0;
@@ -568,15 +649,11 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
     const unsigned pmask = (it % kPrimEvery) == kPrimEvery - 1u ? __ballot_sync(kFullMask, mode == kPrim) : 0u;
     if (pmask) {
       const bool run = __popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u;
-      if (run && mode == kPrim) {
-        float tri[9];
-        load_triangle36(T.buf[L::kBuf_primitives], prim_i, tri);
-        const f32x3 c = closest_point_triangle(p, tri);
-        const f32x3 x = p - c;
-        const float d2 = dot(x, x);
-        tally.prim();
-        if (d2 < best_d) { best_d = d2; best_p = c; best_prim = prim_i; }
-        if (++prim_i == prim_end) pop_or_finish();
+      if (run) {  // warp-uniform
+        const bool own = mode == kPrim;
+        const uint32_t done = coop_points<L>(T, own, p, prim_i, prim_end, best_d, best_p, best_prim, coop[threadIdx.x >> 5]);
+        if (COUNT) tally.prim_tests += done;
+        if (own) pop_or_finish();
       }
     }
   }

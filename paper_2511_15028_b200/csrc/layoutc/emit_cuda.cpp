@@ -606,6 +606,38 @@ struct Emitter {
       emit_decode("decode", Mode::All);
       out << "  SCION_HOSTDEV static void decode_cold(const scion::TreeView&, const Ref&, Node&) {}\n";
     }
+    // prefetch(): pull the record a reference designates into L2 ahead of its visit (issued by the
+    // traversal when the reference is pushed on the stack)
+    out << "  SCION_HOSTDEV static void prefetch(const scion::TreeView& tree__, const Ref& ref__) {\n";
+    {
+      std::string index_expr = ref_is_struct ? "ref__." + primary->index_binding : std::string("ref__");
+      if (primary_buf && !primary_buf->segments.empty()) {
+        const Buffer& b = *primary_buf;
+        out << "    scion::prefetch_l2(tree__.buf[" << b.id << "] + ";
+        if (b.is_arena) out << "(uint64_t)(" << index_expr << ")";
+        else out << "tree__.seg_base[" << b.id << "][0] + (uint64_t)(" << index_expr << ") * " << b.segments[0].stride_bytes << "ull";
+        out << ");\n";
+      } else {
+        // reference-encoded variants: prefetch only the arm(s) that live in an indirect group
+        for (auto& m : primary->members) {
+          if (m->kind != MemberNode::Split) continue;
+          out << "    const auto disc__ = " << ex(m->value, true) << ";\n";
+          for (auto& arm : m->arms) {
+            if (!arm.is_from || arm.pat != Arm::Literal) continue;
+            auto it = indirect_groups.find(arm.from_group);
+            if (it == indirect_groups.end() || !it->second.buf || it->second.buf->segments.empty()) continue;
+            const Buffer& b = *it->second.buf;
+            uint64_t stride = b.segments[0].stride_bytes;
+            out << "    if (disc__ == " << arm.value << ") {\n";
+            out << "      const uint8_t* p__ = tree__.buf[" << b.id << "] + tree__.seg_base[" << b.id << "][0] + (uint64_t)(" << ex(arm.from_key, true) << ") * " << stride << "ull;\n";
+            for (uint64_t o = 0; o < stride; o += 128) out << "      scion::prefetch_l2(p__ + " << o << ");\n";
+            if (stride % 128 != 0 && stride > 64) out << "      scion::prefetch_l2(p__ + " << stride - 1 << ");  // the record may straddle a line\n";
+            out << "    }\n";
+          }
+        }
+      }
+    }
+    out << "  }\n";
     out << "};\n\n}  // namespace scion_gen\n";
     return out.str();
   }

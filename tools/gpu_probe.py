@@ -108,6 +108,44 @@ def tune(G, nrays, layouts):
         dt.free()
 
 if __name__ == "__main__":
+    if "--c5" in sys.argv:  # C5-like quick timing: 10M terrain, 2^24 primary + 2^24 secondary, pbrt-q16 and pbrt
+        scene = sb.Scene.terrain(2236, seed=1)
+        lt = scene.build_sah(32, 4).collapse8()
+        lo, hi = scene.bounds()
+        nr = 1 << 25
+        d_rays = dbuf(nr * 32); d_hits = dbuf(nr * 8)
+        cam = sb.default_camera(lo, hi, True, 4096, 4096)
+        for layout in (sys.argv[sys.argv.index("--c5") + 1].split(",") if len(sys.argv) > sys.argv.index("--c5") + 1 else ("pbrt-q16", "pbrt")):
+            dt = lt.encode(layout).upload(0)
+            sb.gen_primary(cam, 0, 1 << 24, d_rays.data_ptr()); dt.gen_secondary(77, 0, 1 << 24, d_rays.data_ptr() + (32 << 24))
+            for _ in range(2): dt.closest_hit(d_rays.data_ptr(), nr, d_hits.data_ptr())
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(4): dt.closest_hit(d_rays.data_ptr(), nr, d_hits.data_ptr())
+            e1.record(); torch.cuda.synchronize()
+            print(f"  {os.environ.get('SCION_B200_LIB','default').split('/')[-1]:16s} {layout:10s} {nr / (e0.elapsed_time(e1) / 4) / 1e3:8.1f} Mrays/s", flush=True)
+            dt.free()
+        sys.exit(0)
+    if "--ncu" in sys.argv:
+        kind = sys.argv[sys.argv.index("--ncu") + 1]      # primary | secondary
+        layout = sys.argv[sys.argv.index("--ncu") + 2]
+        G = int(sys.argv[sys.argv.index("--ncu") + 3])
+        scene = sb.Scene.terrain(G, seed=1)
+        lt = scene.build_sah(32, 4).collapse8()
+        lo, hi = scene.bounds()
+        nr = 1 << 25
+        d_rays = dbuf(nr * 32); d_hits = dbuf(nr * 8)
+        dt = lt.encode(layout).upload(0)
+        if kind == "primary":
+            cam = sb.default_camera(lo, hi, True, 4096, 4096)
+            sb.gen_primary(cam, 0, 1 << 24, d_rays.data_ptr()); sb.gen_primary(cam, 0, 1 << 24, d_rays.data_ptr() + (32 << 24))
+        else:
+            dt.gen_secondary(77, 0, nr, d_rays.data_ptr())
+        for _ in range(3):
+            dt.closest_hit(d_rays.data_ptr(), nr, d_hits.data_ptr())
+        torch.cuda.synchronize()
+        sys.exit(0)
     if "--tune" in sys.argv:
         tune(708, 1 << 23, ["pbrt", "pbrt-q16", "bvh8-q8-ci"])
         tune(2236, 1 << 23, ["pbrt-q16"])
