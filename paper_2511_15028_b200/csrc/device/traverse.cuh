@@ -562,7 +562,7 @@ SCION_DEV float cpq_node_distmin(const TreeView& T, const f32x3& p, const typena
 }
 
 template <class L, bool COUNT>
-__global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
+__global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
                                                              scion_cp* __restrict__ out, uint32_t* __restrict__ status,
                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
