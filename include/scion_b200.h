@@ -172,6 +172,11 @@ void scion_scene_free(scion_scene* s);
 int scion_build_sah(const scion_scene* s, uint32_t bins, uint32_t max_leaf, uint32_t max_depth,
                     scion_ltree** out);
 int scion_build_median(const scion_scene* s, uint32_t max_leaf, scion_ltree** out);
+/* Import an externally built binary LogicalTree (the reference's `build-tree` artefact):
+ * any node order, root = node 0, leaves reference ranges of tris9.  The tree is re-flattened to
+ * preorder with primitives in left-first leaf order; bounds are taken as given.  No depth cap:
+ * trees deeper than the 64-entry stack make queries report SCION_Q_STACK_OVERFLOW. */
+int scion_ltree_from_arrays(const scion_lnode* nodes, uint64_t nnodes, const float* tris9, uint64_t ntris, scion_ltree** out);
 /* collapse_to_wide; idempotent, result cached inside the ltree. */
 int scion_ltree_collapse8(scion_ltree* t);
 

@@ -453,3 +453,34 @@ uint64_t oracle_check_encoding(const TreeBytes* T, const scion_lnode* lnodes, ui
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ decode entry points (tests of the
+// generated decoders): out_f = lo xyz, hi xyz, lo2 xyzw, hi2 xyzw, left.plo xyz, left.phi xyz (20 floats);
+// out_u = leaf, left, right, prim_begin, nprims
+extern "C" int oracle_decode2(const TreeBytes* T, uint64_t ref, const float* carried6, float* out_f, uint64_t* out_u) {
+  const LayoutDesc* d = find_layout(T->layout);
+  if (!d || d->family == SCION_FAMILY_BVH8) return 1;
+  Ref r;
+  r.r = ref;
+  r.plo = {carried6[0], carried6[1], carried6[2]};
+  r.phi = {carried6[3], carried6[4], carried6[5]};
+  Node2 n = decode2(*T, d->id, r);
+  const float f[20] = {n.box.lo.x, n.box.lo.y, n.box.lo.z, n.box.hi.x, n.box.hi.y, n.box.hi.z, n.lo2.x, n.lo2.y, n.lo2.z, n.lo2.w,
+                       n.hi2.x, n.hi2.y, n.hi2.z, n.hi2.w, n.left.plo.x, n.left.plo.y, n.left.plo.z, n.left.phi.x, n.left.phi.y, n.left.phi.z};
+  std::memcpy(out_f, f, sizeof(f));
+  out_u[0] = n.leaf; out_u[1] = n.left.r; out_u[2] = n.right.r; out_u[3] = n.prim_begin; out_u[4] = n.nprims;
+  return 0;
+}
+// out_f = 8 x (lo xyz, hi xyz); out_u = leaf, prim_begin, nprims, children[8]
+extern "C" int oracle_decode8(const TreeBytes* T, uint64_t ref, float* out_f, uint64_t* out_u) {
+  const LayoutDesc* d = find_layout(T->layout);
+  if (!d || d->family != SCION_FAMILY_BVH8) return 1;
+  Node8 n = decode8(*T, d->id, ref);
+  out_u[0] = n.leaf; out_u[1] = n.prim_begin; out_u[2] = n.nprims;
+  for (int k = 0; k < 8; k++) {
+    out_u[3 + k] = n.leaf ? 0 : n.children[k];
+    const float f[6] = {n.box[k].lo.x, n.box[k].lo.y, n.box[k].lo.z, n.box[k].hi.x, n.box[k].hi.y, n.box[k].hi.z};
+    std::memcpy(out_f + 6 * k, f, sizeof(f));
+  }
+  return 0;
+}

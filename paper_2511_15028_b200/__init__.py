@@ -86,6 +86,7 @@ def lib() -> C.CDLL:
         "scion_build_sah": (i32, [vp, u32, u32, u32, P(vp)]),
         "scion_build_median": (i32, [vp, u32, P(vp)]),
         "scion_ltree_collapse8": (i32, [vp]),
+        "scion_ltree_from_arrays": (i32, [vp, u64, vp, u64, P(vp)]),
         "scion_ltree_nnodes": (u64, [vp]),
         "scion_ltree_nodes": (vp, [vp]),
         "scion_ltree_nprims": (u64, [vp]),
@@ -275,6 +276,15 @@ class Scene:
 class LogicalTree:
     def __init__(self, handle):
         self._h = handle
+
+    @staticmethod
+    def from_arrays(nodes: np.ndarray, tris) -> "LogicalTree":
+        """Import an externally built binary LogicalTree (nodes: LNODE_DTYPE, root = node 0)."""
+        n = np.ascontiguousarray(nodes, dtype=LNODE_DTYPE)
+        t = np.ascontiguousarray(tris, dtype=np.float32).reshape(-1, 9)
+        h = C.c_void_p()
+        _check(lib().scion_ltree_from_arrays(n.ctypes.data, n.shape[0], t.ctypes.data, t.shape[0], C.byref(h)))
+        return LogicalTree(h)
 
     def collapse8(self) -> "LogicalTree":
         _check(lib().scion_ltree_collapse8(self._h))

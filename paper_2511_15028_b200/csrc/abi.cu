@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -232,6 +233,10 @@ int scion_build_median(const scion_scene* s, uint32_t max_leaf, scion_ltree** ou
   if (!s || !out) return fail(SCION_ERR_ARG, "null argument");
   SCION_TRY(auto* t = new scion_ltree(); try { scion::build_binary(*s, scion::Builder::Median, 2, max_leaf, 0, *t); } catch (...) { delete t; throw; } *out = t; return SCION_OK;)
 }
+int scion_ltree_from_arrays(const scion_lnode* nodes, uint64_t nnodes, const float* tris9, uint64_t ntris, scion_ltree** out) {
+  if (!out) return fail(SCION_ERR_ARG, "null out");
+  SCION_TRY(auto* t = new scion_ltree(); try { scion::import_binary(nodes, nnodes, tris9, ntris, *t); } catch (...) { delete t; throw; } *out = t; return SCION_OK;)
+}
 int scion_ltree_collapse8(scion_ltree* t) {
   if (!t) return fail(SCION_ERR_ARG, "null tree");
   SCION_TRY(scion::collapse8(*t); return SCION_OK;)
@@ -415,6 +420,29 @@ static int run_query(const scion_dtree* t, bool hit, const void* in, uint64_t n,
   a.variant = variant;
   a.grid = 0;
   CUDA_OK(cudaMemsetAsync(a.next, 0, sizeof(unsigned long long), a.stream));
+  // Experiment (SCION_L2_PERSIST=1): pin the node buffer in the persisting L2 carve-out.
+  static const bool l2_persist = [] { const char* e = getenv("SCION_L2_PERSIST"); return e && e[0] == '1'; }();
+  if (l2_persist && t->header.nbuf > 1) {
+    static bool limit_set = false;
+    if (!limit_set) {
+      cudaDeviceProp prop;
+      cudaGetDeviceProperties(&prop, t->device);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prop.persistingL2CacheMaxSize);
+      limit_set = true;
+    }
+    cudaStreamAttrValue attr;
+    memset(&attr, 0, sizeof(attr));
+    attr.accessPolicyWindow.base_ptr = (void*)t->view.buf[1];
+    size_t bytes = t->header.bytes[1];
+    int maxw = 0;
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, t->device);
+    if (maxw > 0 && bytes > (size_t)maxw) bytes = (size_t)maxw;
+    attr.accessPolicyWindow.num_bytes = bytes;
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(a.stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+  }
   CUDA_OK(fn(a));
   g_launches.fetch_add(1);
   return SCION_OK;

@@ -354,6 +354,28 @@ SCION_HOSTDEV void load_record(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
   }
 }
 
+// Staged prefix of a node array (see traverse.cuh): records [0, count) live at `base` (shared memory,
+// generic address).  load_record_generic uses plain generic loads so that one instruction serves
+// both the shared and the global window.
+struct Stage {
+  const uint8_t* base = nullptr;
+  uint32_t count = 0;
+};
+template <int BYTES, int ALIGN>
+SCION_HOSTDEV void load_record_generic(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
+  constexpr int NW = (BYTES + 3) / 4;
+  static_assert(ALIGN % 16 == 0 && BYTES % 16 == 0, "staging needs 16-byte records");
+#pragma unroll
+  for (int i = 0; i < NW; i += 4) {
+#if defined(__CUDA_ARCH__)
+    const uint4 v = *reinterpret_cast<const uint4*>(p + 4 * i);
+    r.w[i] = v.x; r.w[i + 1] = v.y; r.w[i + 2] = v.z; r.w[i + 3] = v.w;
+#else
+    memcpy(r.w + i, p + 4 * i, 16);
+#endif
+  }
+}
+
 // constant-offset field extraction: the inverse of write_bits_raw
 // (/root/reference/proj/src/bits.cpp:21-36), little-endian, LSB first
 template <int OFF, int W, int NW>

@@ -334,12 +334,45 @@ SCION_DEV uint64_t opaque(uint64_t q) {
 // ------------------------------------------------------------------------------------------
 // closest_hit, binary + DOP-14 families
 // ------------------------------------------------------------------------------------------
-template <class L, bool COUNT>
+// STAGE > 0 (experimental variant 2): the first STAGE node records of the array are copied into
+// shared memory with one TMA bulk copy (cp.async.bulk + mbarrier, SASS UBLKCP) at CTA start and
+// served from there by the emitted decode<true>().  In a preorder array that prefix is the root,
+// the left spine and the left-most subtrees.  Measured effect: see DESIGN.md §5.
+template <class L, bool COUNT, int STAGE = 0>
 __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Stage stage;
+  if constexpr (STAGE > 0) {
+    __shared__ __align__(8) unsigned long long mbar;
+    unsigned char* dst = smem_raw + kStackSmemBytesPerBlock;
+    const uint64_t have = T.count[L::kStageBuffer];
+    const uint32_t cnt = (uint32_t)(have < (uint64_t)STAGE ? have : (uint64_t)STAGE);
+    const uint32_t bytes = cnt * L::kStageStride;  // multiple of 16 (kCanStage)
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && bytes > 0) {
+      const uint8_t* src = T.buf[L::kStageBuffer] + T.seg_base[L::kStageBuffer][0];
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(dst)),
+                   "l"(src), "r"(bytes), "r"(mb)
+                   : "memory");
+    }
+    if (bytes > 0) {
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(mb), "r"(0u) : "memory");
+    }
+    stage.base = dst;
+    stage.count = cnt;
+  }
   __shared__ CoopScratch coop[kBlockThreads / 32];
   HybridStack<Ref> stack;
   stack.init(smem_raw);
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     // ---- NODE: decode one node, test its bounds
     if (mode == kNode) {
       typename L::Node node;
-      L::decode(T, cur, node);
+      L::template decode<(STAGE > 0)>(T, cur, node, stage);
       tally.visit();
       float t_near;
       const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);

@@ -301,6 +301,8 @@ inline float round_up(double s) {
 
 }  // namespace
 
+static void compute_dop(scion_ltree& out);
+
 void build_binary(const scion_scene& s, Builder kind, uint32_t bins, uint32_t max_leaf, uint32_t max_depth,
                   scion_ltree& out) {
   const uint64_t P = s.ntris();
@@ -337,8 +339,6 @@ void build_binary(const scion_scene& s, Builder kind, uint32_t bins, uint32_t ma
   // flatten to preorder; prims are already in left-first leaf order in idx[]
   out = scion_ltree();
   out.nodes.resize((size_t)N);
-  out.dop_lo2.assign((size_t)N * 4, 0.0f);
-  out.dop_hi2.assign((size_t)N * 4, 0.0f);
   out.prim_ids = idx;
   out.tris.resize(P * 9);
 #pragma omp parallel for schedule(static)
@@ -377,7 +377,14 @@ void build_binary(const scion_scene& s, Builder kind, uint32_t bins, uint32_t ma
   out.depth = maxd;
   if (outi != N) throw std::runtime_error("internal: node count mismatch");
 
-  // DOP-14 diagonal slabs, bottom-up (children have larger preorder index than parents)
+  compute_dop(out);
+}
+
+// DOP-14 diagonal slabs, bottom-up (children have larger preorder index than parents)
+static void compute_dop(scion_ltree& out) {
+  const int64_t N = (int64_t)out.nodes.size();
+  out.dop_lo2.assign((size_t)N * 4, 0.0f);
+  out.dop_hi2.assign((size_t)N * 4, 0.0f);
   for (int64_t i = N - 1; i >= 0; i--) {
     const scion_lnode& n = out.nodes[(size_t)i];
     float* lo2 = &out.dop_lo2[(size_t)i * 4];
@@ -402,6 +409,47 @@ void build_binary(const scion_scene& s, Builder kind, uint32_t bins, uint32_t ma
       for (int k = 0; k < 4; k++) { lo2[k] = std::min(l0[k], l1[k]); hi2[k] = std::max(h0[k], h1[k]); }
     }
   }
+}
+
+// Import of an externally built binary tree: re-flatten to preorder, primitives to leaf order.
+void import_binary(const scion_lnode* nodes, uint64_t nnodes, const float* tris9, uint64_t ntris, scion_ltree& out) {
+  if (!nodes || nnodes == 0 || !tris9 || ntris == 0) throw std::runtime_error("import: empty tree");
+  out = scion_ltree();
+  out.nodes.reserve(nnodes);
+  struct Item { int64_t src; int64_t parent; bool is_right; uint32_t depth; };
+  std::vector<Item> stack{{0, -1, false, 0}};
+  std::vector<uint8_t> seen(nnodes, 0);
+  uint32_t maxd = 0;
+  while (!stack.empty()) {
+    Item it = stack.back();
+    stack.pop_back();
+    if (it.src < 0 || (uint64_t)it.src >= nnodes || seen[(size_t)it.src]) throw std::runtime_error("import: child index out of range or node reached twice");
+    seen[(size_t)it.src] = 1;
+    const scion_lnode& s = nodes[it.src];
+    int64_t me = (int64_t)out.nodes.size();
+    out.nodes.push_back(s);
+    scion_lnode& n = out.nodes.back();
+    maxd = std::max(maxd, it.depth);
+    if (it.parent >= 0) {
+      if (it.is_right) out.nodes[(size_t)it.parent].right = (int32_t)me;
+      else out.nodes[(size_t)it.parent].left = (int32_t)me;
+    }
+    if (s.left < 0) {
+      if (s.nprims == 0 || (uint64_t)s.first_prim + s.nprims > ntris) throw std::runtime_error("import: leaf range out of bounds");
+      n.left = n.right = -1;
+      n.first_prim = (uint32_t)(out.tris.size() / 9);
+      for (uint32_t p = s.first_prim; p < s.first_prim + s.nprims; p++) {
+        out.tris.insert(out.tris.end(), tris9 + (size_t)p * 9, tris9 + (size_t)p * 9 + 9);
+        out.prim_ids.push_back(p);
+      }
+    } else {
+      n.first_prim = n.nprims = 0;
+      stack.push_back({s.right, me, true, it.depth + 1});
+      stack.push_back({s.left, me, false, it.depth + 1});
+    }
+  }
+  out.depth = maxd;
+  compute_dop(out);
 }
 
 // ---------------------------------------------------------------------------------

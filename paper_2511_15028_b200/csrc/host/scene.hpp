@@ -39,4 +39,5 @@ enum class Builder { SAH, Median };
 void build_binary(const scion_scene& s, Builder kind, uint32_t bins, uint32_t max_leaf, uint32_t max_depth,
                   scion_ltree& out);
 void collapse8(scion_ltree& t);
+void import_binary(const scion_lnode* nodes, uint64_t nnodes, const float* tris9, uint64_t ntris, scion_ltree& out);
 }  // namespace scion

@@ -315,17 +315,30 @@ struct Emitter {
   }
 
   // emits loads of every segment of `buf` that holds a wanted stored field
-  void emit_record_loads(const Buffer& buf, const std::string& index_expr, const std::string& tag, int ind, bool hot_only) {
+  // `stageable`: segment 0 of the primary index-referenced group may be served from a staged copy
+  // of the array's first records (TMA bulk copy into shared memory, device/traverse.cuh)
+  void emit_record_loads(const Buffer& buf, const std::string& index_expr, const std::string& tag, int ind, bool hot_only, bool stageable = false) {
     std::string pad((size_t)ind * 2, ' ');
     for (size_t s = 0; s < buf.segments.size(); s++) {
       if (hot_only && s > 0) break;
       uint64_t bytes = buf.segments[s].stride_bytes;
       std::string w = "w_" + tag + std::to_string(s);
       out << pad << "scion::Words<" << (bytes + 3) / 4 << "> " << w << ";\n";
-      out << pad << "scion::load_record<" << bytes << ", " << gcd_align(buf, (int)s) << ">(tree__.buf[" << buf.id << "] + ";
-      if (buf.is_arena) out << "(uint64_t)(" << index_expr << ")";
-      else out << "tree__.seg_base[" << buf.id << "][" << s << "] + (uint64_t)(" << index_expr << ") * " << bytes << "ull";
-      out << ", " << w << ");\n";
+      std::ostringstream addr;
+      addr << "tree__.buf[" << buf.id << "] + ";
+      if (buf.is_arena) addr << "(uint64_t)(" << index_expr << ")";
+      else addr << "tree__.seg_base[" << buf.id << "][" << s << "] + (uint64_t)(" << index_expr << ") * " << bytes << "ull";
+      if (stageable && s == 0 && !buf.is_arena) {
+        out << pad << "if constexpr (STAGED) {\n";
+        out << pad << "  const uint64_t i__ = (uint64_t)(" << index_expr << ");\n";
+        out << pad << "  const uint8_t* p__ = i__ < stage__.count ? stage__.base + i__ * " << bytes << "ull : " << addr.str() << ";\n";
+        out << pad << "  scion::load_record_generic<" << bytes << ", " << gcd_align(buf, (int)s) << ">(p__, " << w << ");\n";
+        out << pad << "} else {\n";
+        out << pad << "  scion::load_record<" << bytes << ", " << gcd_align(buf, (int)s) << ">(" << addr.str() << ", " << w << ");\n";
+        out << pad << "}\n";
+      } else {
+        out << pad << "scion::load_record<" << bytes << ", " << gcd_align(buf, (int)s) << ">(" << addr.str() << ", " << w << ");\n";
+      }
     }
   }
 
@@ -576,8 +589,15 @@ struct Emitter {
       out << "  }\n";
     }
     // decode
+    const bool can_stage = primary_buf && !primary_buf->segments.empty() && !primary_buf->is_arena && primary_buf->segments[0].stride_bytes % 16 == 0;
+    out << "  static constexpr bool kCanStage = " << (can_stage ? "true" : "false") << ";  // first records may be staged in shared memory\n";
+    out << "  static constexpr uint32_t kStageStride = " << (can_stage ? primary_buf->segments[0].stride_bytes : 0) << "u;\n";
+    out << "  static constexpr int kStageBuffer = " << (can_stage ? primary_buf->id : 0) << ";\n";
     auto emit_decode = [&](const char* name, Mode mode) {
-      out << "  SCION_HOSTDEV static void " << name << "(const scion::TreeView& tree__, const Ref& ref__, Node& node__) {\n";
+      const bool main = std::string(name) == "decode";
+      if (main) out << "  template <bool STAGED = false>\n";
+      out << "  SCION_HOSTDEV static void " << name << "(const scion::TreeView& tree__, const Ref& ref__, Node& node__"
+          << (main ? ", const scion::Stage& stage__ = scion::Stage()" : "") << ") {\n";
       // globals referenced by layout expressions
       std::set<std::string> ids;
       std::function<void(const std::vector<MemberP>&)> scan = [&](const std::vector<MemberP>& ms) {
@@ -595,7 +615,7 @@ struct Emitter {
         if (ids.count(plan.globals[g].name) && !plan.globals[g].inferred)
           out << "    const " << ctype(plan.globals[g].type) << " " << plan.globals[g].name << " = scion::glob<" << ctype(plan.globals[g].type) << ">(tree__, " << g << ");\n";
       std::string index_expr = ref_is_struct ? "ref__." + primary->index_binding : std::string("ref__");
-      if (primary_buf && !primary_buf->segments.empty()) emit_record_loads(*primary_buf, index_expr, "", 2, mode == Mode::Hot);
+      if (primary_buf && !primary_buf->segments.empty()) emit_record_loads(*primary_buf, index_expr, "", 2, mode == Mode::Hot, main && can_stage);
       emit_members(primary->members, primary_buf, "", 2, mode, {}, {}, nullptr, false);
       out << "  }\n";
     };

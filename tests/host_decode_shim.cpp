@@ -1,0 +1,87 @@
+// TEST-ONLY: compiles the GENERATED layout headers (csrc/gen/*.cuh) in the host mode of
+// device/scion_rt.cuh so that emit_cuda's output can be checked against the oracle's independent
+// decoders on a machine without a GPU.  Not part of the product library.
+#include <cstring>
+#include <string>
+
+#include "gen/bvh8.cuh"
+#include "gen/bvh8_q16.cuh"
+#include "gen/bvh8_q16_ci.cuh"
+#include "gen/bvh8_q8.cuh"
+#include "gen/bvh8_q8_ci.cuh"
+#include "gen/dop14.cuh"
+#include "gen/identity.cuh"
+#include "gen/pbrt.cuh"
+#include "gen/pbrt_align16.cuh"
+#include "gen/pbrt_post.cuh"
+#include "gen/pbrt_q16.cuh"
+#include "gen/pbrt_soa.cuh"
+#include "gen/ptr.cuh"
+#include "gen/sg_eq.cuh"
+#include "gen/sg_eq_align16.cuh"
+#include "gen/shared_slab.cuh"
+
+using scion::TreeView;
+namespace g = scion_gen;
+
+template <class R> R make_ref(uint64_t r, const float* c) {
+  if constexpr (sizeof(R) <= 8) return (R)r;
+  else { R x; x.P = r; x.plo = {c[0], c[1], c[2]}; x.phi = {c[3], c[4], c[5]}; return x; }
+}
+template <class R> uint64_t ref_id(const R& r) {
+  if constexpr (sizeof(R) <= 8) return (uint64_t)r;
+  else return r.P;
+}
+template <class L> int dec2(const TreeView* T, uint64_t ref, const float* carried, float* f, uint64_t* u) {
+  typename L::Node n{};
+  auto r = make_ref<typename L::Ref>(ref, carried);
+  L::decode(*T, r, n);
+  L::decode_cold(*T, r, n);
+  std::memset(f, 0, 20 * sizeof(float));
+  if constexpr (L::kFamily == 1) {
+    float v[14] = {n.lo1.x, n.lo1.y, n.lo1.z, n.hi1.x, n.hi1.y, n.hi1.z, n.lo2.x, n.lo2.y, n.lo2.z, n.lo2.w, n.hi2.x, n.hi2.y, n.hi2.z, n.hi2.w};
+    std::memcpy(f, v, sizeof(v));
+  } else {
+    float v[6] = {n.low.x, n.low.y, n.low.z, n.high.x, n.high.y, n.high.z};
+    std::memcpy(f, v, sizeof(v));
+  }
+  u[0] = n.variant == L::kLeaf;
+  u[1] = u[2] = u[3] = u[4] = 0;
+  if (n.variant == L::kLeaf) { u[3] = n.data.begin; u[4] = n.nprims; if (n.data.end - n.data.begin != n.nprims) return 2; }
+  else {
+    u[1] = ref_id(n.left); u[2] = ref_id(n.right);
+    if constexpr (sizeof(typename L::Ref) > 8) { float v[6] = {n.left.plo.x, n.left.plo.y, n.left.plo.z, n.left.phi.x, n.left.phi.y, n.left.phi.z}; std::memcpy(f + 14, v, sizeof(v)); }
+  }
+  return 0;
+}
+template <class L> int dec8(const TreeView* T, uint64_t ref, float* f, uint64_t* u) {
+  typename L::Node n{};
+  L::decode(*T, (typename L::Ref)ref, n);
+  std::memset(f, 0, 48 * sizeof(float));
+  std::memset(u, 0, 11 * sizeof(uint64_t));
+  u[0] = n.variant == L::kLeaf;
+  if (n.variant == L::kLeaf) { u[1] = n.data.begin; u[2] = n.nprims; return 0; }
+  for (int k = 0; k < 8; k++) {
+    u[3 + k] = (uint64_t)n.children[k];
+    float v[6] = {n.lo[k].x, n.lo[k].y, n.lo[k].z, n.hi[k].x, n.hi[k].y, n.hi[k].z};
+    std::memcpy(f + 6 * k, v, sizeof(v));
+  }
+  return 0;
+}
+
+extern "C" int host_decode2(const char* layout, const TreeView* T, uint64_t ref, const float* carried, float* f, uint64_t* u) {
+  std::string n = layout;
+#define L2(NAME, T_) if (n == NAME) return dec2<g::T_>(T, ref, carried, f, u);
+  L2("pbrt", L_pbrt) L2("pbrt-align16", L_pbrt_align16) L2("pbrt-soa", L_pbrt_soa) L2("pbrt-post", L_pbrt_post) L2("pbrt-q16", L_pbrt_q16)
+  L2("sg-eq", L_sg_eq) L2("sg-eq-align16", L_sg_eq_align16) L2("ptr", L_ptr) L2("identity", L_identity) L2("shared-slab", L_shared_slab) L2("dop14", L_dop14)
+#undef L2
+  return -1;
+}
+extern "C" int host_decode8(const char* layout, const TreeView* T, uint64_t ref, float* f, uint64_t* u) {
+  std::string n = layout;
+#define L8(NAME, T_) if (n == NAME) return dec8<g::T_>(T, ref, f, u);
+  L8("bvh8", L_bvh8) L8("bvh8-q8", L_bvh8_q8) L8("bvh8-q8-ci", L_bvh8_q8_ci) L8("bvh8-q16", L_bvh8_q16) L8("bvh8-q16-ci", L_bvh8_q16_ci)
+#undef L8
+  return -1;
+}
+extern "C" unsigned host_treeview_size() { return (unsigned)sizeof(TreeView); }

@@ -186,72 +186,70 @@ def test_edge_cases(built, oracle, torch_cuda):
         dt.free()
 
 
-def test_stack_overflow_is_a_query_error(built, oracle, torch_cuda):
-    """a tree deeper than the 64-entry stack: overflow is reported per query, never silent"""
+def deep_chain(sb, depth):
+    """left-deep chain: every interior's left child is the next interior, its right child a leaf, all boxes
+    identical => a ray through the box accumulates one pending right sibling per level"""
+    tri = lambda x: [x, 0, 0, x + 0.5, 0, 0, x, 0.5, 0]
+    tris = np.array([tri(float(i)) for i in range(depth + 1)], np.float32)
+    nodes = np.zeros(2 * depth + 1, sb.LNODE_DTYPE)
+    nodes["lo"][:] = (-1.0, -1.0, -1.0)
+    nodes["hi"][:] = (depth + 2.0, 1.0, 1.0)
+    for i in range(depth):  # interiors 0..depth-1, leaves depth..2*depth
+        nodes["left"][i] = i + 1 if i + 1 < depth else 2 * depth
+        nodes["right"][i] = depth + i
+    for j in range(depth, 2 * depth + 1):
+        nodes["left"][j] = nodes["right"][j] = -1
+        nodes["first_prim"][j] = j - depth
+        nodes["nprims"][j] = 1
+    return sb.LogicalTree.from_arrays(nodes, tris)
+
+
+@pytest.mark.parametrize("layout", ["pbrt", "pbrt-q16", "sg-eq", "dop14", "ptr", "bvh8-q8-ci"])
+def test_stack_overflow_is_a_query_error(built, oracle, torch_cuda, layout):
+    """a tree deeper than the 64-entry stack: overflow is reported per query, never silent (SPEC.md:289-292,
+    "tree of depth 70 with depth-64 stack -> overflow error"); shallower trees and rays that miss are fine"""
     sb = built
-    # a degenerate chain: nested triangles force a median tree of depth 70 is not constructible through
-    # the depth-capped builders, so craft the LogicalTree-equivalent pbrt image by hand: 71 interiors
-    # whose LEFT child is a leaf and whose right child is the next interior (right-deep chain).
-    depth = 71
-    tris, nodes = [], []
-    # node i (interior) at index 2i, its left leaf at 2i+1, right = 2i+2 ; last node is a leaf
-    for i in range(depth + 1):
-        x = float(i)
-        tris.append([x, 0, 0, x + 0.5, 0, 0, x, 0.5, 0])
-    tris = np.array(tris, np.float32)
-    lt = sb.Scene.from_triangles(tris).build_median(1)  # balanced: depth 7, no overflow
-    dt = lt.encode("pbrt").upload(0)
-    ray = np.zeros(1, sb.RAY_DTYPE)
-    ray[0] = (0.1, 0.1, -1, np.inf, 0, 0, 1, 0)
-    got, st, ctr = gpu_hits(torch_cuda, sb, dt, ray)
-    assert st[0] == 0 and ctr["max_stack"][0] <= 64
-    dt.free()
-    # left-deep chain built directly as a pbrt byte image: every interior's left child is the next
-    # interior (this+1), its right child a leaf => pending right siblings grow by one per level.
-    N = 2 * depth + 1
-    buf = np.zeros(N * 32, np.uint8)
-    f = buf.view(np.float32).reshape(N, 8)
-    u = buf.view(np.uint32).reshape(N, 8)
-    h = buf.view(np.uint16).reshape(N, 16)
-    big_lo, big_hi = (-1.0, -1.0, -1.0), (float(depth + 2), 1.0, 1.0)
-    for i in range(depth):  # interiors at 0..depth-1 (preorder: left = this+1)
-        f[i, 0:3], f[i, 3:6] = big_lo, big_hi
-        u[i, 6] = (N - 1 - i) - i  # right child = leaf placed from the end
-        h[i, 14] = 0
-    for j in range(depth, N):  # leaves
-        f[j, 0:3], f[j, 3:6] = big_lo, big_hi
-        u[j, 6] = (j - depth) % (depth + 1)
-        h[j, 14] = 1
-    import ctypes as C
-    from tests.oracle_lib import TreeBytes
-    prim = np.ascontiguousarray(tris.reshape(-1))
-    tb = TreeBytes()
-    tb.layout = b"pbrt"
-    tb.nbuf = 2
-    tb.buf[0], tb.bytes[0], tb.count[0] = prim.ctypes.data, prim.nbytes, len(tris)
-    tb.buf[1], tb.bytes[1], tb.count[1] = buf.ctypes.data, buf.nbytes, N
-    want, wst, wctr = oracle.closest_hit(tb, ray, counters=True)
-    assert wst[0] == 1  # the oracle reports overflow (depth 71 > 64)
-    # upload the same hand-made image by patching a real ptree of the same shape
-    # (buffers are replaced through the device image: header from a compatible tree, payload ours)
-    base = sb.Scene.from_triangles(tris).build_median(1).encode("pbrt")
-    img_bytes = base.image_bytes
-    dimg = torch_cuda.zeros(img_bytes + N * 32 + 4096, dtype=torch_cuda.uint8, device="cuda:0")
-    off = (-dimg.data_ptr()) % 256
-    dt0 = base.upload_into(0, dimg.data_ptr() + off, img_bytes + N * 32)
-    himg = dimg.cpu().numpy()
-    hdr = himg[off:off + 1024].copy()
-    # header fields (abi.cu ImageHeader): offset[] at byte 72, bytes[] at 120, count[] at 168 (8 bytes each, 6 entries)
-    offs = hdr[72:72 + 48].view(np.uint64)
-    node_off = int(offs[1])
-    cnts = hdr[168:168 + 48].view(np.uint64)
-    assert int(cnts[1]) == len(base.buffers()[1]["data"]) // 32
-    if N * 32 <= int(hdr[120:168].view(np.uint64)[1]) + 16 + 4096:
-        himg[off + node_off:off + node_off + N * 32] = buf
-        dimg.copy_(torch_cuda.from_numpy(himg))
-        got, st, ctr = gpu_hits(torch_cuda, sb, dt0, ray)
-        assert st[0] == 1, "GPU must report STACK_OVERFLOW like the oracle"
-    dt0.free()
+    ray = np.zeros(2, sb.RAY_DTYPE)
+    ray[0] = (0.1, 0.1, -1, np.inf, 0, 0, 1, 0)  # through the common box: descends the whole chain
+    ray[1] = (0.1, 5.0, -1, np.inf, 0, 0, 1, 0)  # misses the root
+    pts = np.array([[0.1, 0.1, 0.0]], np.float32)
+    for depth, expect in ((40, 0), (70, 1)):
+        lt = deep_chain(sb, depth).collapse8()
+        assert lt.depth == depth and lt.nnodes == 2 * depth + 1
+        pt = lt.encode(layout)
+        dt = pt.upload(0)
+        got, st, ctr = gpu_hits(torch_cuda, sb, dt, ray)
+        want, wst, wctr = oracle.closest_hit(oracle.tree_bytes(pt), ray, counters=True)
+        assert np.array_equal(st, wst), (layout, depth, st, wst)
+        assert st[1] == 0
+        if layout in ("pbrt", "pbrt-q16", "sg-eq", "ptr"):  # AABB chains: the ray passes every box (dop14's diagonal slabs prune it)
+            assert st[0] == expect
+        ok = st == 0
+        assert np.array_equal(got["prim"][ok], want["prim"][ok]) and np.array_equal(got["t"][ok].view(np.uint32), want["t"][ok].view(np.uint32))
+        if not layout.startswith("bvh8"):
+            cp, cst, _ = gpu_points(torch_cuda, sb, dt, pts)
+            wcp, wcst = oracle.closest_point(oracle.tree_bytes(pt), pts)
+            assert np.array_equal(cst, wcst)
+            if cst[0] == 0:
+                assert np.array_equal(cp.view(np.uint32), wcp.view(np.uint32))
+        dt.free()
+
+
+def test_staged_prefix_variant_is_identical(built, torch_cuda, world):
+    """experimental kernel variant 2 (TMA bulk copy of the node array's first records into shared memory,
+    served by decode<true>) must return exactly the default kernel's records"""
+    sb, torch = built, torch_cuda
+    n = world["rays"].shape[0]
+    d_rays = dev_bytes(torch, world["rays"])
+    for layout in ("pbrt", "pbrt-q16"):
+        dt = world["lt"].encode(layout).upload(0)
+        a = torch.zeros(n * 8, dtype=torch.uint8, device="cuda:0")
+        b = torch.zeros(n * 8, dtype=torch.uint8, device="cuda:0")
+        dt.closest_hit(d_rays.data_ptr(), n, a.data_ptr())
+        dt.closest_hit(d_rays.data_ptr(), n, b.data_ptr(), variant=2)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), layout
+        dt.free()
 
 
 def test_fault_injection_changes_results(built, oracle, torch_cuda, world):

@@ -127,6 +127,29 @@ if __name__ == "__main__":
             print(f"  {os.environ.get('SCION_B200_LIB','default').split('/')[-1]:16s} {layout:10s} {nr / (e0.elapsed_time(e1) / 4) / 1e3:8.1f} Mrays/s", flush=True)
             dt.free()
         sys.exit(0)
+    if "--stage" in sys.argv:  # TMA-staged prefix (variant 2) vs default: identical results? timing?
+        for G in (708, 2236):
+            scene = sb.Scene.terrain(G, seed=1)
+            lt = scene.build_sah(32, 4)
+            lo, hi = scene.bounds()
+            nr = 1 << 25
+            d_rays = dbuf(nr * 32); d_hits = dbuf(nr * 8); d_hits2 = dbuf(nr * 8)
+            cam = sb.default_camera(lo, hi, True, 4096, 4096)
+            for layout in ("pbrt-q16", "pbrt"):
+                dt = lt.encode(layout).upload(0)
+                sb.gen_primary(cam, 0, 1 << 24, d_rays.data_ptr()); dt.gen_secondary(77, 0, 1 << 24, d_rays.data_ptr() + (32 << 24))
+                res = {}
+                for v, out in ((0, d_hits), (2, d_hits2)):
+                    for _ in range(2): dt.closest_hit(d_rays.data_ptr(), nr, out.data_ptr(), variant=v)
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(4): dt.closest_hit(d_rays.data_ptr(), nr, out.data_ptr(), variant=v)
+                    e1.record(); torch.cuda.synchronize()
+                    res[v] = nr / (e0.elapsed_time(e1) / 4) / 1e3
+                print(f"  G={G} {layout:10s} default {res[0]:8.1f}  staged {res[2]:8.1f} Mrays/s  identical={bool(torch.equal(d_hits, d_hits2))}", flush=True)
+                dt.free()
+        sys.exit(0)
     if "--ncu" in sys.argv:
         kind = sys.argv[sys.argv.index("--ncu") + 1]      # primary | secondary
         layout = sys.argv[sys.argv.index("--ncu") + 2]
