@@ -85,10 +85,11 @@ struct scion_dtree {
   unsigned long long* counters = nullptr;  // kCounterSlots work-fetch counters
   std::atomic<uint32_t> next_slot{0};
   // staging for the host entry points
-  void* h2d[2] = {nullptr, nullptr};
-  void* d2h[2] = {nullptr, nullptr};
-  uint32_t* d_status[2] = {nullptr, nullptr};
-  cudaStream_t streams[2] = {nullptr, nullptr};
+  static constexpr int kSlots = 4;  // staging slots of the host entry points: H2D(k+1) || kernel(k) || D2H(k-1)
+  void* h2d[kSlots] = {};
+  void* d2h[kSlots] = {};
+  uint32_t* d_status[kSlots] = {};
+  cudaStream_t streams[kSlots] = {};
   uint64_t chunk = 0;
   std::mutex host_mutex;
 };
@@ -390,7 +391,7 @@ int scion_dtree_from_image(const char* layout, void* d_image, uint64_t bytes, in
 void scion_dtree_free(scion_dtree* t) {
   if (!t) return;
   cudaSetDevice(t->device);
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < scion_dtree::kSlots; i++) {
     if (t->streams[i]) { cudaStreamSynchronize(t->streams[i]); cudaStreamDestroy(t->streams[i]); }
     if (t->h2d[i]) cudaFree(t->h2d[i]);
     if (t->d2h[i]) cudaFree(t->d2h[i]);
@@ -462,9 +463,10 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
   std::lock_guard<std::mutex> lock(t->host_mutex);
   CUDA_OK(cudaSetDevice(t->device));
   const uint64_t in_sz = hit ? sizeof(scion_ray) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
-  const uint64_t kChunk = 1ull << 22;
+  const uint64_t kChunk = 1ull << 21;
+  constexpr int S = scion_dtree::kSlots;
   if (t->chunk == 0) {
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < S; i++) {
       CUDA_OK(cudaStreamCreateWithFlags(&t->streams[i], cudaStreamNonBlocking));
       CUDA_OK(cudaMalloc(&t->h2d[i], kChunk * sizeof(scion_ray)));
       CUDA_OK(cudaMalloc(&t->d2h[i], kChunk * sizeof(scion_cp)));
@@ -473,7 +475,7 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
     t->chunk = kChunk;
   }
   int k = 0;
-  for (uint64_t off = 0; off < n; off += kChunk, k ^= 1) {
+  for (uint64_t off = 0; off < n; off += kChunk, k = (k + 1) % S) {
     const uint64_t m = std::min(kChunk, n - off);
     cudaStream_t s = t->streams[k];
     CUDA_OK(cudaMemcpyAsync(t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s));
@@ -482,8 +484,7 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
     CUDA_OK(cudaMemcpyAsync((uint8_t*)h_out + off * out_sz, t->d2h[k], m * out_sz, cudaMemcpyDeviceToHost, s));
     if (h_status) CUDA_OK(cudaMemcpyAsync(h_status + off, t->d_status[k], m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   }
-  CUDA_OK(cudaStreamSynchronize(t->streams[0]));
-  CUDA_OK(cudaStreamSynchronize(t->streams[1]));
+  for (int i = 0; i < S; i++) CUDA_OK(cudaStreamSynchronize(t->streams[i]));
   return SCION_OK;
 }
 int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64_t n, scion_hit* h_hits, uint32_t* h_status) {

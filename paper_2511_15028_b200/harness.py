@@ -1,0 +1,163 @@
+"""Command-line harness of the B200 backend — the slice of the reference CLI (`layoutc check | footprint |
+compile --emit-c | bench`) that belongs to the traversal path.
+
+  python -m paper_2511_15028_b200.harness check                      # every registered layout plans + emits
+  python -m paper_2511_15028_b200.harness footprint --layout L --scene terrain:224
+  python -m paper_2511_15028_b200.harness emit-cuda --layout L [-o file]
+  python -m paper_2511_15028_b200.harness bench --layout L[,L2..] --alg chrt|cpq --scene terrain:708 --queries 4194304 --rays secondary
+
+`bench` follows the paper's protocol: 1 warm-up + 9 runs, drop the 2 lowest
+and 2 highest, report the mean of the remaining 5, one CSV row per (layout, algorithm, scene, nGPU).
+Exit codes as the reference CLI: 0 pass, 1 diagnostics/mismatch, 2 usage.  `verify` (which needs the CPU
+oracle) lives in tests/verify_cli.py because only test infrastructure may touch oracle/.
+"""
+import argparse
+import json
+import sys
+
+import numpy as np
+
+import paper_2511_15028_b200 as sb
+
+
+def parse_scene(spec: str) -> "sb.Scene":
+    kind, _, arg = spec.partition(":")
+    n = int(arg or 64)
+    if kind == "terrain":
+        return sb.Scene.terrain(n, sb.seed_from_env(1))
+    if kind == "sphere":
+        return sb.Scene.sphere(n, sb.seed_from_env(1))
+    if kind == "cloud":
+        return sb.Scene.cloud(n, sb.seed_from_env(1))
+    raise SystemExit(2)
+
+
+def cmd_check(_):
+    ok = True
+    for l in sb.layouts():
+        try:
+            plan = sb.layout_plan(l["name"])
+            text = sb.emit_cuda(l["name"])
+            assert "static void decode(" in text
+            print(f"{l['name']:14s} ok   family={('bvh2', 'dop14', 'bvh8')[l['family']]} node_stride={l['node_stride']} segments={l['n_segments']} slots={len(plan['slots'])}")
+        except Exception as e:  # noqa: BLE001
+            ok = False
+            print(f"{l['name']:14s} FAILED {e}", file=sys.stderr)
+    return 0 if ok else 1
+
+
+def cmd_footprint(a):
+    scene = parse_scene(a.scene)
+    lt = scene.build_sah(32, a.max_leaf).collapse8()
+    pt = lt.encode(a.layout)
+    rep = {"layout": a.layout, "scene": a.scene, "primitives": lt.nprims, "total_bytes": pt.total_bytes, "node_bytes": pt.node_bytes,
+           "bvh_bytes_per_prim": pt.node_bytes / lt.nprims,
+           "buffers": [{"name": b["name"], "bytes": b["bytes"], "count": b["count"], "segment_bases": b["seg_bases"]} for b in pt.buffers()],
+           "node_stride": sb.layout_info(a.layout)["node_stride"]}
+    print(json.dumps(rep, indent=1))
+    return 0
+
+
+def cmd_emit(a):
+    text = sb.emit_cuda(a.layout)
+    if a.output:
+        open(a.output, "w").write(text)
+    else:
+        sys.stdout.write(text)
+    return 0
+
+
+def cmd_bench(a):
+    import torch
+    if not torch.cuda.is_available():
+        print("bench needs a CUDA device (no CPU fallback)", file=sys.stderr)
+        return 1
+    scene = parse_scene(a.scene)
+    lt = scene.build_sah(32, a.max_leaf).collapse8()
+    lo, hi = scene.bounds()
+    n = a.queries
+    dev = "cuda:0"
+    print("layout,algorithm,scene,n_gpus,queries,kind,mean_ms,mqueries_per_s,bvh_bytes_per_prim,node_visits,prim_tests,bytes_per_query,achieved_gbs")
+    for layout in a.layout.split(","):
+        pt = lt.encode(layout)
+        dt = pt.upload(0)
+        if a.alg == "chrt":
+            d_q = torch.empty(n * 32, dtype=torch.uint8, device=dev)
+            d_r = torch.empty(n * 8, dtype=torch.uint8, device=dev)
+            if a.rays == "primary":
+                side = int(np.sqrt(n))
+                cam = sb.default_camera(lo, hi, scene_is_terrain(a.scene), side, side)
+                sb.gen_primary(cam, 0, n, d_q.data_ptr())
+            else:
+                dt.gen_secondary(sb.seed_from_env(7), 0, n, d_q.data_ptr())
+            run = lambda ctr=0, st=0: dt.closest_hit(d_q.data_ptr(), n, d_r.data_ptr(), st, ctr)
+        else:
+            d_q = torch.empty(n * 12, dtype=torch.uint8, device=dev)
+            d_r = torch.empty(n * 20, dtype=torch.uint8, device=dev)
+            sb.gen_points(lo, hi, sb.seed_from_env(7), 0, n, d_q.data_ptr())
+            run = lambda ctr=0, st=0: dt.closest_point(d_q.data_ptr(), n, d_r.data_ptr(), st, ctr)
+        times = []
+        for i in range(10):  # 1 warm-up + 9 runs
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run()
+            e1.record()
+            torch.cuda.synchronize()
+            if i:
+                times.append(e0.elapsed_time(e1))
+        ms = float(np.mean(sorted(times)[2:-2]))  # drop 2 lowest + 2 highest, mean of 5
+        d_ctr = torch.zeros(n * 4, dtype=torch.int32, device=dev)
+        d_st = torch.zeros(n, dtype=torch.int32, device=dev)
+        run(d_ctr.data_ptr(), d_st.data_ptr())
+        torch.cuda.synchronize()
+        c = d_ctr.view(-1, 4).sum(dim=0, dtype=torch.int64).cpu().numpy() / n
+        plan = sb.layout_plan(layout)
+        seg = [s["stride_bytes"] for b in plan["buffers"] if b["name"] == plan["node_group"] for s in b["segments"]]
+        q_io = 40 if a.alg == "chrt" else 32
+        bpq = c[0] * (seg[0] if seg else 0) + c[2] * sum(seg[1:]) + c[1] * 36 + q_io
+        print(f"{layout},{a.alg},{a.scene},1,{n},{a.rays if a.alg == 'chrt' else 'points'},{ms:.4f},{n / ms / 1e3:.2f},{pt.node_bytes / lt.nprims:.3f},{c[0]:.2f},{c[1]:.2f},{bpq:.1f},{bpq * n / ms / 1e6:.1f}")
+        if int((d_st != 0).sum()) != 0:
+            print(f"{layout}: query errors reported", file=sys.stderr)
+            return 1
+        dt.free()
+    return 0
+
+
+def scene_is_terrain(spec):
+    return spec.startswith("terrain")
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(prog="paper_2511_15028_b200.harness")
+    sub = ap.add_subparsers(dest="cmd")
+    sub.add_parser("check")
+    p = sub.add_parser("footprint")
+    p.add_argument("--layout", required=True)
+    p.add_argument("--scene", default="terrain:64")
+    p.add_argument("--max-leaf", type=int, default=4)
+    p = sub.add_parser("emit-cuda")
+    p.add_argument("--layout", required=True)
+    p.add_argument("-o", "--output")
+    p = sub.add_parser("bench")
+    p.add_argument("--layout", required=True)
+    p.add_argument("--alg", default="chrt", choices=["chrt", "cpq"])
+    p.add_argument("--scene", default="terrain:224")
+    p.add_argument("--queries", type=int, default=1 << 20)
+    p.add_argument("--rays", default="primary", choices=["primary", "secondary"])
+    p.add_argument("--max-leaf", type=int, default=4)
+    try:
+        a = ap.parse_args(argv)
+    except SystemExit:
+        return 2
+    if a.cmd is None:
+        ap.print_usage(sys.stderr)
+        return 2
+    try:
+        return {"check": cmd_check, "footprint": cmd_footprint, "emit-cuda": cmd_emit, "bench": cmd_bench}[a.cmd](a)
+    except sb.ScionError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 2 if e.code == sb.ERR_ARG else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
