@@ -77,6 +77,18 @@ struct HybridStack {
     }
     sp++;
   }
+  // store entry r at absolute position `pos` iff `on` — no branch on the common (shared-memory) path, so
+  // eight conditional pushes of an 8-wide node issue as straight-line predicated code
+  SCION_DEV void store_if(bool on, int pos, const Entry& r) {
+    uint32_t w[kWords];
+    memcpy(w, &r, sizeof(Entry));
+    const uint32_t a = base + (uint32_t)pos * kEntryStride;
+    const uint32_t p = (on && pos < kSmem) ? 1u : 0u;
+#pragma unroll
+    for (int i = 0; i < kWords; i++)
+      asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.b32 [%0], %1; }" ::"r"(a + 4u * i), "r"(w[i]), "r"(p) : "memory");
+    if (on && pos >= kSmem) deep[pos - kSmem] = r;
+  }
   SCION_DEV Entry pop(int& sp) {
     sp--;
     Entry r;
@@ -545,24 +557,27 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const
         else pop_or_finish();
       } else {
         tally.visit();
-        // test the eight child boxes from slot 7 down to slot 0 and push the passing ones as they
-        // are found: the stack then pops them in slot order (chrt8.scion:7 `foreach c in children`).
-        // Occupancy after the last push is sp + #passing, the same figure the all-at-once form checks.
+        // test the eight child boxes, then store the passing ones at their final stack positions:
+        // slot k lands above every passing slot with a larger index, so the stack pops in slot order
+        // (chrt8.scion:7 `foreach c in children`).  Positional predicated stores instead of eight
+        // divergent push blocks (profiles/r1_ncu_v5_c5_q8ci.txt: 8 x 14 SASS instructions at 3/32 lanes).
+        uint32_t mask = 0;
+        float tn[8];
 #pragma unroll
-        for (int k = 7; k >= 0; k--) {
-          float tn, t_far;
-          const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn, t_far);
-          if (interval_intersects(ray, some, tn, t_far) && tn < best_t && st == SCION_Q_OK) {
-            if (sp + 1 > SCION_STACK_DEPTH) {
-              st = SCION_Q_STACK_OVERFLOW;
-              tally.stack((uint32_t)sp + 1u);
-            } else {
-              stack.push(sp, Entry{node.children[k], tn});
-              if (kPrefetchWide) L::prefetch(T, node.children[k]);
-            }
-          }
+        for (int k = 0; k < 8; k++) {
+          float t_far;
+          const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn[k], t_far);
+          if (interval_intersects(ray, some, tn[k], t_far) && tn[k] < best_t) mask |= 1u << k;
         }
-        tally.stack((uint32_t)sp);
+        const int m = __popc(mask);
+        tally.stack((uint32_t)(sp + m));
+        if (sp + m > SCION_STACK_DEPTH) {
+          st = SCION_Q_STACK_OVERFLOW;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; k++) stack.store_if((mask >> k) & 1u, sp + __popc(mask >> (k + 1)), Entry{node.children[k], tn[k]});
+          sp += m;
+        }
         pop_or_finish();
       }
     }
