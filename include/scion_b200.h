@@ -212,6 +212,10 @@ int scion_ptree_global(const scion_ptree* p, int i, const char** name, uint8_t r
 int scion_ptree_root(const scion_ptree* p, uint64_t* ref0, float* carried6);
 uint64_t scion_ptree_total_bytes(const scion_ptree* p); /* footprint().total_bytes */
 uint64_t scion_ptree_node_bytes(const scion_ptree* p);  /* all buffers except primitives */
+/* PhysicalTree container file ("versioned container file = header (magic, version, layout
+ * name, global slots) + raw little-endian buffers"; read by the `run` subcommand) */
+int scion_ptree_save(const scion_ptree* p, const char* path);
+int scion_ptree_load(const char* path, scion_ptree** out);
 /* fault injection for verify tests: xor one byte of a buffer */
 int scion_ptree_corrupt(scion_ptree* p, int buffer, uint64_t byte_offset, uint8_t xor_mask);
 void scion_ptree_free(scion_ptree* p);

@@ -112,6 +112,8 @@ def lib() -> C.CDLL:
         "scion_ptree_total_bytes": (u64, [vp]),
         "scion_ptree_node_bytes": (u64, [vp]),
         "scion_ptree_corrupt": (i32, [vp, i32, u64, C.c_uint8]),
+        "scion_ptree_save": (i32, [vp, cp]),
+        "scion_ptree_load": (i32, [cp, P(vp)]),
         "scion_ptree_free": (None, [vp]),
         "scion_device_count": (i32, [P(i32)]),
         "scion_dtree_upload": (i32, [vp, i32, P(vp)]),
@@ -378,6 +380,16 @@ class PhysicalTree:
     @property
     def node_bytes(self) -> int:
         return lib().scion_ptree_node_bytes(self._h)
+
+    def save(self, path: str):
+        """Write the PhysicalTree container file."""
+        _check(lib().scion_ptree_save(self._h, path.encode()))
+
+    @staticmethod
+    def load(path: str) -> "PhysicalTree":
+        h = C.c_void_p()
+        _check(lib().scion_ptree_load(path.encode(), C.byref(h)))
+        return PhysicalTree(h)
 
     def corrupt(self, buffer: int, byte_offset: int, xor_mask: int = 0xFF):
         _check(lib().scion_ptree_corrupt(self._h, buffer, byte_offset, xor_mask))

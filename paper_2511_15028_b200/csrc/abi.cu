@@ -5,8 +5,10 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -146,6 +148,23 @@ unsigned long long* take_counter(const scion_dtree* t) {
   return m->counters + (m->next_slot.fetch_add(1) % kCounterSlots);
 }
 
+}  // namespace
+
+namespace {
+struct FileW {
+  FILE* f;
+  bool ok = true;
+  void raw(const void* p, size_t n) { if (n && fwrite(p, 1, n, f) != n) ok = false; }
+  template <class T> void val(T v) { raw(&v, sizeof(T)); }
+  void str(const std::string& s) { val<uint32_t>((uint32_t)s.size()); raw(s.data(), s.size()); }
+};
+struct FileR {
+  FILE* f;
+  bool ok = true;
+  void raw(void* p, size_t n) { if (n && fread(p, 1, n, f) != n) ok = false; }
+  template <class T> T val() { T v{}; raw(&v, sizeof(T)); return v; }
+  std::string str() { uint32_t n = val<uint32_t>(); if (!ok || n > 4096) { ok = false; return ""; } std::string s(n, 0); raw(s.data(), n); return s; }
+};
 }  // namespace
 
 namespace scion {
@@ -304,6 +323,86 @@ uint64_t scion_ptree_node_bytes(const scion_ptree* p) {
   for (size_t b = 0; b < p->buffers.size(); b++)
     if (!p->plan->buffers[b].is_global_array) s += p->buffers[b].size();
   return s;
+}
+// ---- container file: "SCIONPT1" | u32 version | u32 name_len | name | u64 nprims | u64 root0 | 6 x f32 carried |
+//      u32 nglob | nglob x { u32 len, name, 16 raw bytes } | u32 nbuf | nbuf x { u32 len, name, u64 count, u64 bytes,
+//      u32 nseg, nseg x u64 base } | raw buffers, each padded to 16 bytes.  Little-endian throughout.
+int scion_ptree_save(const scion_ptree* p, const char* path) {
+  if (!p || !path) return fail(SCION_ERR_ARG, "null argument");
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(SCION_ERR_ARG, std::string("cannot open ") + path);
+  FileW w{f};
+  w.raw("SCIONPT1", 8);
+  w.val<uint32_t>(1);
+  w.str(p->layout);
+  w.val<uint64_t>(p->nprims);
+  w.val<uint64_t>(p->root0);
+  w.raw(p->carried, sizeof(p->carried));
+  w.val<uint32_t>((uint32_t)p->globals.size());
+  for (size_t g = 0; g < p->globals.size(); g++) { w.str(p->plan->globals[g].name); w.raw(p->globals[g].data(), 16); }
+  w.val<uint32_t>((uint32_t)p->buffers.size());
+  for (size_t b = 0; b < p->buffers.size(); b++) {
+    w.str(p->plan->buffers[b].name);
+    w.val<uint64_t>(p->counts[b]);
+    w.val<uint64_t>(p->buffers[b].size());
+    w.val<uint32_t>((uint32_t)p->seg_bases[b].size());
+    for (uint64_t x : p->seg_bases[b]) w.val<uint64_t>(x);
+  }
+  static const char zeros[16] = {0};
+  for (auto& b : p->buffers) { w.raw(b.data(), b.size()); w.raw(zeros, (16 - b.size() % 16) % 16); }
+  bool ok = w.ok;
+  if (fclose(f) != 0) ok = false;
+  return ok ? SCION_OK : fail(SCION_ERR_ARG, std::string("write failed: ") + path);
+}
+int scion_ptree_load(const char* path, scion_ptree** out) {
+  if (!path || !out) return fail(SCION_ERR_ARG, "null argument");
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(SCION_ERR_ARG, std::string("cannot open ") + path);
+  FileR r{f};
+  auto bail = [&](const std::string& why) { fclose(f); return fail(SCION_ERR_ARG, std::string(path) + ": " + why); };
+  char magic[8];
+  r.raw(magic, 8);
+  if (!r.ok || memcmp(magic, "SCIONPT1", 8) != 0) return bail("not a scion PhysicalTree container");
+  if (r.val<uint32_t>() != 1) return bail("unsupported container version");
+  std::string layout = r.str();
+  SCION_TRY(
+    const scion::LayoutEntry* e = scion::find_layout(layout);
+    if (!e) return bail("container names unknown layout '" + layout + "'");
+    auto p = std::make_unique<scion_ptree>();
+    p->layout = layout;
+    p->plan = e->plan.get();
+    p->nprims = r.val<uint64_t>();
+    p->root0 = r.val<uint64_t>();
+    r.raw(p->carried, sizeof(p->carried));
+    uint32_t ng = r.val<uint32_t>();
+    if (!r.ok || ng != p->plan->globals.size()) return bail("global slot table does not match the layout's plan");
+    p->globals.resize(ng);
+    for (uint32_t g = 0; g < ng; g++) { if (r.str() != p->plan->globals[g].name) return bail("global slot name mismatch"); r.raw(p->globals[g].data(), 16); }
+    uint32_t nb = r.val<uint32_t>();
+    if (!r.ok || nb != p->plan->buffers.size()) return bail("buffer table does not match the layout's plan");
+    p->buffers.resize(nb); p->counts.resize(nb); p->seg_bases.resize(nb);
+    std::vector<uint64_t> sizes(nb);
+    for (uint32_t b = 0; b < nb; b++) {
+      if (r.str() != p->plan->buffers[b].name) return bail("buffer name mismatch");
+      p->counts[b] = r.val<uint64_t>();
+      sizes[b] = r.val<uint64_t>();
+      uint32_t ns = r.val<uint32_t>();
+      if (!r.ok || ns > 8) return bail("corrupt segment table");
+      for (uint32_t s = 0; s < ns; s++) p->seg_bases[b].push_back(r.val<uint64_t>());
+      const scion::lc::Buffer& pb = p->plan->buffers[b];
+      if (!pb.is_arena && sizes[b] != pb.bytes(p->counts[b])) return bail("buffer size disagrees with footprint() for its count");
+    }
+    for (uint32_t b = 0; b < nb; b++) {
+      p->buffers[b].resize(sizes[b]);
+      r.raw(p->buffers[b].data(), sizes[b]);
+      char pad[16];
+      r.raw(pad, (16 - sizes[b] % 16) % 16);
+    }
+    if (!r.ok) return bail("truncated container");
+    fclose(f);
+    *out = p.release();
+    return SCION_OK;
+  )
 }
 int scion_ptree_corrupt(scion_ptree* p, int buffer, uint64_t byte_offset, uint8_t xor_mask) {
   if (!p || buffer < 0 || buffer >= (int)p->buffers.size() || byte_offset >= p->buffers[(size_t)buffer].size()) return fail(SCION_ERR_ARG, "corrupt: out of range");

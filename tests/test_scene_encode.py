@@ -159,3 +159,26 @@ def test_counters_sg_eq_visits_at_least_pbrt(built, oracle, small):
     _, _, c_p = oracle.closest_hit(oracle.tree_bytes(lt.encode("pbrt")), rays, counters=True)
     _, _, c_s = oracle.closest_hit(oracle.tree_bytes(lt.encode("sg-eq")), rays, counters=True)
     assert c_s["node_visits"].sum() >= c_p["node_visits"].sum()
+
+
+def test_container_file_round_trip(built, oracle, small, tmp_path):
+    """PhysicalTree container: save -> load is byte-identical for every layout; foreign or
+    truncated files are rejected with a diagnostic, never half-loaded"""
+    _, lt = small
+    for l in built.layouts():
+        pt = lt.encode(l["name"])
+        path = str(tmp_path / (l["name"] + ".scionpt"))
+        pt.save(path)
+        back = built.PhysicalTree.load(path)
+        assert back.layout == pt.layout and back.root() == pt.root() and back.total_bytes == pt.total_bytes
+        for a, b in zip(pt.buffers(), back.buffers()):
+            assert a["name"] == b["name"] and a["count"] == b["count"] and a["seg_bases"] == b["seg_bases"] and np.array_equal(a["data"], b["data"])
+        assert [g["raw"] for g in pt.globals()] == [g["raw"] for g in back.globals()]
+        assert oracle.check_encoding(back, lt)[0] == 0
+    raw = open(path, "rb").read()
+    open(path, "wb").write(raw[: len(raw) // 2])
+    with pytest.raises(built.ScionError):
+        built.PhysicalTree.load(path)
+    open(path, "wb").write(b"NOTSCION" + raw[8:])
+    with pytest.raises(built.ScionError):
+        built.PhysicalTree.load(path)
