@@ -252,6 +252,26 @@ int scion_closest_hit(const scion_dtree* t, const scion_ray* d_rays, uint64_t n,
                       int variant, void* stream);
 int scion_closest_point(const scion_dtree* t, const float* d_points_xyz, uint64_t n, scion_cp* d_out,
                         uint32_t* d_status, scion_counters* d_counters, int variant, void* stream);
+/* collision_detection(bvh1, bvh2, r: mut set[(Triangle, Triangle)]) — corpus/alg/cd.scion:2-31,
+ * cd_dop14.scion (binary layouts only, corpus.cpp:86).  Both trees must use the same layout and live on the
+ * same device (the same tree twice = self-collision).  The result is a SET: up to `capacity` pairs
+ * (primitive index in tree a, primitive index in tree b) are written to d_out in unspecified order and
+ * *out_count receives the true set size (> capacity means the caller must retry with a larger buffer).
+ * Synchronous (level-synchronous frontier expansion).  Frontier exhaustion is an error, never silent. */
+typedef struct scion_pair {
+  uint32_t a, b;
+} scion_pair;
+typedef struct scion_cd_stats {
+  uint64_t node_pairs; /* node pairs tested (= recursive calls of the DSL) */
+  uint64_t tri_tests;  /* SAT tests */
+  uint64_t levels;
+  uint64_t max_frontier;
+} scion_cd_stats;
+int scion_collision_detection(const scion_dtree* a, const scion_dtree* b, scion_pair* d_out, uint64_t capacity, uint64_t* out_count,
+                              scion_cd_stats* stats /* nullable */, uint64_t frontier_capacity /* 0 = default 2^24 */, void* stream);
+/* host-buffer form: pairs copied back (D2H) */
+int scion_collision_detection_host(const scion_dtree* a, const scion_dtree* b, scion_pair* h_out, uint64_t capacity, uint64_t* out_count,
+                                   scion_cd_stats* stats);
 /* Host-buffer entry points (the reference-facing call: host in, host out). H2D copy,
  * kernel, D2H copy, stream sync; chunked + double-buffered over two streams. */
 int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64_t n, scion_hit* h_hits,

@@ -484,3 +484,81 @@ extern "C" int oracle_decode8(const TreeBytes* T, uint64_t ref, float* out_f, ui
   }
   return 0;
 }
+
+
+// ------------------------------------------------------------------ collision detection
+// /root/reference/proj/corpus/alg/cd.scion:2-31 and cd_dop14.scion:2-31, kept recursive like the DSL
+// ([recursive], depth guard 10^4 frames).  Result = set of (triangle index in tree 1,
+// triangle index in tree 2); returned sorted so that set equality is a plain comparison.
+namespace {
+struct CdRun {
+  const TreeBytes& A;
+  const TreeBytes& B;
+  int id, family;
+  std::vector<uint64_t> pairs;
+  uint64_t node_pairs = 0, tri_tests = 0;
+  bool too_deep = false;
+  void rec(const Ref& ra, const Ref& rb, int depth) {
+    if (depth > 10000) { too_deep = true; return; }
+    Node2 a = decode_any2(A, id, ra), b = decode_any2(B, id, rb);
+    node_pairs++;
+    const bool hit = family == SCION_FAMILY_DOP14 ? dop_overlap(a.box, a.lo2, a.hi2, b.box, b.lo2, b.hi2) : aabb_overlap(a.box, b.box);
+    if (!hit) return;
+    if (!a.leaf && !b.leaf) {
+      rec(a.left, b.left, depth + 1); rec(a.left, b.right, depth + 1);
+      rec(a.right, b.left, depth + 1); rec(a.right, b.right, depth + 1);
+    } else if (!a.leaf) {
+      rec(a.left, rb, depth + 1); rec(a.right, rb, depth + 1);
+    } else if (!b.leaf) {
+      rec(ra, b.left, depth + 1); rec(ra, b.right, depth + 1);
+    } else {
+      for (uint64_t i = a.prim_begin; i < a.prim_begin + a.nprims; i++)
+        for (uint64_t j = b.prim_begin; j < b.prim_begin + b.nprims; j++) {
+          tri_tests++;
+          if (sat_triangles(load_tri(A, i), load_tri(B, j))) pairs.push_back((i << 32) | j);
+        }
+    }
+  }
+};
+}  // namespace
+
+extern "C" {
+// returns the number of colliding pairs (written sorted, up to `capacity`), or -1 on error
+int64_t oracle_collision_detection(const TreeBytes* A, const TreeBytes* B, uint64_t* out_pairs, uint64_t capacity, uint64_t* stats3) {
+  int id, family, id2, family2;
+  if (resolve(A->layout, &id, &family) || resolve(B->layout, &id2, &family2) || id != id2 || family == SCION_FAMILY_BVH8) return -1;
+  CdRun run{*A, *B, id, family};
+  run.rec(id >= 100 ? Ref{A->root0} : root_ref(*A, (LayoutId)id), id >= 100 ? Ref{B->root0} : root_ref(*B, (LayoutId)id), 0);
+  if (run.too_deep) return -2;
+  std::sort(run.pairs.begin(), run.pairs.end());
+  for (size_t i = 0; i < run.pairs.size() && i < capacity; i++) out_pairs[i] = run.pairs[i];
+  if (stats3) { stats3[0] = run.node_pairs; stats3[1] = run.tri_tests; stats3[2] = run.pairs.size(); }
+  return (int64_t)run.pairs.size();
+}
+// O(n*m) SAT brute force
+int64_t oracle_brute_collisions(const float* tris_a, uint64_t na, const float* tris_b, uint64_t nb, uint64_t* out_pairs, uint64_t capacity) {
+  std::vector<std::vector<uint64_t>> per((size_t)omp_get_max_threads());
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < (int64_t)na; i++) {
+    Tri a;
+    std::memcpy(&a, tris_a + 9 * i, 36);
+    auto& v = per[(size_t)omp_get_thread_num()];
+    for (uint64_t j = 0; j < nb; j++) {
+      Tri b;
+      std::memcpy(&b, tris_b + 9 * j, 36);
+      if (sat_triangles(a, b)) v.push_back(((uint64_t)i << 32) | j);
+    }
+  }
+  std::vector<uint64_t> all;
+  for (auto& v : per) all.insert(all.end(), v.begin(), v.end());
+  std::sort(all.begin(), all.end());
+  for (size_t i = 0; i < all.size() && i < capacity; i++) out_pairs[i] = all[i];
+  return (int64_t)all.size();
+}
+int oracle_sat(const float* a9, const float* b9) {
+  Tri a, b;
+  std::memcpy(&a, a9, 36);
+  std::memcpy(&b, b9, 36);
+  return sat_triangles(a, b) ? 1 : 0;
+}
+}

@@ -236,4 +236,58 @@ inline float distmin_dop_point(V3 p, V3 lo1, V3 hi1, V4 lo2, V4 hi2) {
   return fmaxf(base, fmaxf(fmaxf(d0, d1), fmaxf(d2, d3)));
 }
 
+// ------------------------------------------------------------------ geometry.scion:112-157 (collision detection)
+// project6 (:112-118)
+inline int project6(V3 ax, V3 p1, V3 p2, V3 p3, V3 q1, V3 q2, V3 q3) {
+  float P1 = dot(ax, p1), P2 = dot(ax, p2), P3 = dot(ax, p3);
+  float Q1 = dot(ax, q1), Q2 = dot(ax, q2), Q3 = dot(ax, q3);
+  float mn1 = fminf(fminf(P1, P2), P3), mx2 = fmaxf(fmaxf(Q1, Q2), Q3);
+  if (mn1 > mx2) return 0;
+  float mx1 = fmaxf(fmaxf(P1, P2), P3), mn2 = fminf(fminf(Q1, Q2), Q3);
+  if (mn2 > mx1) return 0;
+  return 1;
+}
+// SAT_triangle_intersection over the 17 candidate axes (:120-154)
+inline bool sat_triangles(const Tri& A, const Tri& B) {
+  V3 p1{0.0f, 0.0f, 0.0f}, p2 = sub(A.p1, A.p0), p3 = sub(A.p2, A.p0);
+  V3 q1 = sub(B.p0, A.p0), q2 = sub(B.p1, A.p0), q3 = sub(B.p2, A.p0);
+  V3 e1 = sub(p2, p1), e2 = sub(p3, p2), n1 = cross(e1, e2);
+  if (project6(n1, p1, p2, p3, q1, q2, q3) == 0) return false;
+  V3 f1 = sub(q2, q1), f2 = sub(q3, q2), m1 = cross(f1, f2);
+  if (project6(m1, p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e1, f1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e1, f2), p1, p2, p3, q1, q2, q3) == 0) return false;
+  V3 f3 = sub(q1, q3);
+  if (project6(cross(e1, f3), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e2, f1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e2, f2), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e2, f3), p1, p2, p3, q1, q2, q3) == 0) return false;
+  V3 e3 = sub(p1, p3);
+  if (project6(cross(e3, f1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e3, f2), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e3, f3), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e1, n1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e2, n1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(e3, n1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(f1, m1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(f2, m1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  if (project6(cross(f3, m1), p1, p2, p3, q1, q2, q3) == 0) return false;
+  return true;
+}
+// intersects(AABB, AABB) (:158-160)
+inline bool aabb_overlap(const Box& a, const Box& b) {
+  V3 low{fmaxf(a.lo.x, b.lo.x), fmaxf(a.lo.y, b.lo.y), fmaxf(a.lo.z, b.lo.z)};
+  V3 high{fminf(a.hi.x, b.hi.x), fminf(a.hi.y, b.hi.y), fminf(a.hi.z, b.hi.z)};
+  return low.x <= high.x && low.y <= high.y && low.z <= high.z;
+}
+// intersects_dop_dop (dop.scion:81-90)
+inline bool dop_overlap(const Box& a, V4 alo2, V4 ahi2, const Box& b, V4 blo2, V4 bhi2) {
+  if (!aabb_overlap(a, b)) return false;
+  if (alo2.x > bhi2.x || blo2.x > ahi2.x) return false;
+  if (alo2.y > bhi2.y || blo2.y > ahi2.y) return false;
+  if (alo2.z > bhi2.z || blo2.z > ahi2.z) return false;
+  if (alo2.w > bhi2.w || blo2.w > ahi2.w) return false;
+  return true;
+}
+
 }  // namespace oracle

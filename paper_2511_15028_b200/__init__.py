@@ -46,6 +46,13 @@ class LayoutInfo(C.Structure):
                 ("n_segments", C.c_uint32), ("ref_bits", C.c_uint32), ("max_leaf", C.c_uint32), ("has_cpq", C.c_int)]
 
 
+class CdStats(C.Structure):
+    _fields_ = [("node_pairs", C.c_uint64), ("tri_tests", C.c_uint64), ("levels", C.c_uint64), ("max_frontier", C.c_uint64)]
+
+
+PAIR_DTYPE = np.dtype([("a", "u4"), ("b", "u4")])
+
+
 class Camera(C.Structure):
     _fields_ = [("eye", C.c_float * 3), ("target", C.c_float * 3), ("up", C.c_float * 3), ("fov_y_deg", C.c_float), ("width", C.c_uint32), ("height", C.c_uint32)]
 
@@ -125,6 +132,8 @@ def lib() -> C.CDLL:
         "scion_dtree_free": (None, [vp]),
         "scion_closest_hit": (i32, [vp, vp, u64, vp, vp, vp, i32, vp]),
         "scion_closest_point": (i32, [vp, vp, u64, vp, vp, vp, i32, vp]),
+        "scion_collision_detection": (i32, [vp, vp, vp, u64, P(u64), P(CdStats), u64, vp]),
+        "scion_collision_detection_host": (i32, [vp, vp, vp, u64, P(u64), P(CdStats)]),
         "scion_closest_hit_host": (i32, [vp, vp, u64, vp, vp]),
         "scion_closest_point_host": (i32, [vp, vp, u64, vp, vp]),
         "scion_camera_default": (None, [P(C.c_float * 3), P(C.c_float * 3), i32, u32, u32, P(Camera)]),
@@ -171,11 +180,13 @@ def _f3(v):
     return (C.c_float * 3)(*[float(x) for x in v])
 
 
-def _np_view(ptr, count, dtype):
+def _np_view(ptr, count, dtype, owner=None):
+    """Zero-copy numpy view of library-owned memory; the view keeps `owner` (the Python handle object) alive."""
     if not ptr or count == 0:
         return np.zeros(0, dtype=dtype)
     nbytes = int(count) * np.dtype(dtype).itemsize
     buf = (C.c_uint8 * nbytes).from_address(ptr)
+    buf._owner = owner  # numpy array -> ctypes buffer -> owner
     return np.frombuffer(buf, dtype=dtype)
 
 
@@ -252,7 +263,7 @@ class Scene:
         return lib().scion_scene_ntris(self._h)
 
     def triangles(self) -> np.ndarray:
-        return _np_view(lib().scion_scene_triangles(self._h), self.ntris * 9, np.float32).reshape(-1, 9)
+        return _np_view(lib().scion_scene_triangles(self._h), self.ntris * 9, np.float32, self).reshape(-1, 9)
 
     def bounds(self):
         lo, hi = (C.c_float * 3)(), (C.c_float * 3)()
@@ -305,24 +316,24 @@ class LogicalTree:
         return lib().scion_ltree_depth(self._h)
 
     def nodes(self) -> np.ndarray:
-        return _np_view(lib().scion_ltree_nodes(self._h), self.nnodes, LNODE_DTYPE)
+        return _np_view(lib().scion_ltree_nodes(self._h), self.nnodes, LNODE_DTYPE, self)
 
     def triangles(self) -> np.ndarray:
-        return _np_view(lib().scion_ltree_triangles(self._h), self.nprims * 9, np.float32).reshape(-1, 9)
+        return _np_view(lib().scion_ltree_triangles(self._h), self.nprims * 9, np.float32, self).reshape(-1, 9)
 
     def prim_ids(self) -> np.ndarray:
-        return _np_view(lib().scion_ltree_prim_ids(self._h), self.nprims, np.uint32)
+        return _np_view(lib().scion_ltree_prim_ids(self._h), self.nprims, np.uint32, self)
 
     def dop(self):
         n = self.nnodes
-        return (_np_view(lib().scion_ltree_dop_lo2(self._h), n * 4, np.float32).reshape(-1, 4),
-                _np_view(lib().scion_ltree_dop_hi2(self._h), n * 4, np.float32).reshape(-1, 4))
+        return (_np_view(lib().scion_ltree_dop_lo2(self._h), n * 4, np.float32, self).reshape(-1, 4),
+                _np_view(lib().scion_ltree_dop_hi2(self._h), n * 4, np.float32, self).reshape(-1, 4))
 
     def wnodes(self) -> np.ndarray:
-        return _np_view(lib().scion_ltree_wnodes(self._h), lib().scion_ltree_nwnodes(self._h), WNODE_DTYPE)
+        return _np_view(lib().scion_ltree_wnodes(self._h), lib().scion_ltree_nwnodes(self._h), WNODE_DTYPE, self)
 
     def wleaves(self) -> np.ndarray:
-        return _np_view(lib().scion_ltree_wleaves(self._h), lib().scion_ltree_nwleaves(self._h), WLEAF_DTYPE)
+        return _np_view(lib().scion_ltree_wleaves(self._h), lib().scion_ltree_nwleaves(self._h), WLEAF_DTYPE, self)
 
     @property
     def wroot(self) -> int:
@@ -356,7 +367,7 @@ class PhysicalTree:
             _check(lib().scion_ptree_buffer(self._h, i, C.byref(name), C.byref(data), C.byref(nbytes), C.byref(count)))
             bases = (C.c_uint64 * 4)()
             ns = lib().scion_ptree_segment_bases(self._h, i, bases, 4)
-            out.append(dict(name=name.value.decode(), data=_np_view(data.value, nbytes.value, np.uint8), ptr=data.value, bytes=nbytes.value,
+            out.append(dict(name=name.value.decode(), data=_np_view(data.value, nbytes.value, np.uint8, self), ptr=data.value, bytes=nbytes.value,
                             count=count.value, seg_bases=list(bases[:ns])))
         return out
 
@@ -467,6 +478,20 @@ class DeviceTree:
             out = np.empty(n, CP_DTYPE)
         _check(lib().scion_closest_point_host(self._h, pts.ctypes.data, n, out.ctypes.data, status.ctypes.data if status is not None else None))
         return out
+
+    def collide_host(self, other: "DeviceTree", capacity: int = 1 << 20):
+        """collision_detection(self, other): returns (pairs sorted as a set, true count, stats dict)."""
+        out = np.empty(capacity, PAIR_DTYPE)
+        n, st = C.c_uint64(), CdStats()
+        _check(lib().scion_collision_detection_host(self._h, other._h, out.ctypes.data, capacity, C.byref(n), C.byref(st)))
+        m = min(n.value, capacity)
+        keys = np.sort((out["a"][:m].astype(np.uint64) << np.uint64(32)) | out["b"][:m].astype(np.uint64))
+        return keys, n.value, dict(node_pairs=st.node_pairs, tri_tests=st.tri_tests, levels=st.levels, max_frontier=st.max_frontier)
+
+    def collide(self, other: "DeviceTree", d_out: int, capacity: int, frontier_capacity: int = 0, stream: int = 0):
+        n, st = C.c_uint64(), CdStats()
+        _check(lib().scion_collision_detection(self._h, other._h, d_out, capacity, C.byref(n), C.byref(st), frontier_capacity, stream or None))
+        return n.value, dict(node_pairs=st.node_pairs, tri_tests=st.tri_tests, levels=st.levels, max_frontier=st.max_frontier)
 
     def gen_secondary(self, seed: int, first: int, n: int, d_rays: int, stream: int = 0):
         _check(lib().scion_gen_secondary(self._h, seed, first, n, d_rays, stream or None))

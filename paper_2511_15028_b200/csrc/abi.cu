@@ -554,6 +554,36 @@ int scion_closest_point(const scion_dtree* t, const float* d_points, uint64_t n,
   return run_query(t, false, d_points, n, d_out, d_status, d_counters, variant, stream);
 }
 
+int scion_collision_detection(const scion_dtree* a, const scion_dtree* b, scion_pair* d_out, uint64_t capacity, uint64_t* out_count,
+                              scion_cd_stats* stats, uint64_t frontier_capacity, void* stream) {
+  if (!a || !b || (!d_out && capacity) || !out_count) return fail(SCION_ERR_ARG, "null argument");
+  if (a->layout != b->layout) return fail(SCION_ERR_ARG, "collision_detection needs two trees of the same layout");
+  if (a->device != b->device) return fail(SCION_ERR_ARG, "collision_detection needs both trees on the same device");
+  if (!a->kernels->collide) return fail(SCION_ERR_ARG, "cd requires a binary layout (corpus.cpp:86)");
+  CUDA_OK(cudaSetDevice(a->device));
+  scion::CdArgs args{a->view, b->view, d_out, capacity, frontier_capacity, out_count, stats, (cudaStream_t)stream};
+  int overflow = 0;
+  CUDA_OK(a->kernels->collide(args, &overflow));
+  g_launches.fetch_add(1);
+  if (overflow) return fail(SCION_ERR_QUERY, "collision_detection: node-pair frontier exceeded its capacity (pass a larger frontier_capacity)");
+  return SCION_OK;
+}
+int scion_collision_detection_host(const scion_dtree* a, const scion_dtree* b, scion_pair* h_out, uint64_t capacity, uint64_t* out_count,
+                                   scion_cd_stats* stats) {
+  if (!a || (!h_out && capacity) || !out_count) return fail(SCION_ERR_ARG, "null argument");
+  CUDA_OK(cudaSetDevice(a->device));
+  scion_pair* d = nullptr;
+  CUDA_OK(cudaMalloc(&d, (capacity ? capacity : 1) * sizeof(scion_pair)));
+  int rc = scion_collision_detection(a, b, d, capacity, out_count, stats, 0, nullptr);
+  if (rc == SCION_OK) {
+    uint64_t m = *out_count < capacity ? *out_count : capacity;
+    cudaError_t e = m ? cudaMemcpy(h_out, d, m * sizeof(scion_pair), cudaMemcpyDeviceToHost) : cudaSuccess;
+    if (e != cudaSuccess) rc = fail(SCION_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(d);
+  return rc;
+}
+
 // Host entry points: chunked, double-buffered over two streams so that the H2D copy of chunk
 // k+1 and the D2H copy of chunk k-1 overlap the traversal of chunk k.
 static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uint64_t n, void* h_out, uint32_t* h_status) {

@@ -22,6 +22,17 @@ struct LaunchArgs {
 };
 
 typedef cudaError_t (*launch_fn)(const LaunchArgs&);
+
+struct CdArgs {  // collision detection: two trees of the same layout on the same device
+  TreeView a, b;
+  scion_pair* out;
+  uint64_t capacity;
+  uint64_t frontier_capacity;
+  uint64_t* out_count;      // host
+  scion_cd_stats* stats;    // host, nullable
+  cudaStream_t stream;
+};
+typedef cudaError_t (*cd_fn)(const CdArgs&, int* overflow_bits);
 typedef cudaError_t (*occupancy_fn)(int* blocks_per_sm, int* regs, size_t* smem);
 
 struct KernelEntry {
@@ -29,6 +40,7 @@ struct KernelEntry {
   launch_fn closest_hit;
   launch_fn closest_point;  // null for 8-wide layouts (corpus.cpp:83)
   occupancy_fn hit_occupancy;
+  cd_fn collide;  // null for 8-wide layouts (corpus.cpp:86)
 };
 
 const KernelEntry* find_kernels(const char* layout);

@@ -47,6 +47,11 @@ class Oracle:
         L.oracle_distmax_point_aabb.argtypes = [vp, vp, vp]
         L.oracle_distmax_point_aabb.restype = f32
         L.oracle_quantize_roundtrip.argtypes = [i32, vp, vp, vp, vp, vp, vp]
+        L.oracle_collision_detection.argtypes = [C.POINTER(TreeBytes), C.POINTER(TreeBytes), vp, u64, vp]
+        L.oracle_collision_detection.restype = C.c_int64
+        L.oracle_brute_collisions.argtypes = [vp, u64, vp, u64, vp, u64]
+        L.oracle_brute_collisions.restype = C.c_int64
+        L.oracle_sat.argtypes = [vp, vp]
 
     # ------------------------------------------------------------------ tree marshalling
     def tree_bytes(self, ptree: "sb.PhysicalTree"):
@@ -139,3 +144,23 @@ class Oracle:
         bad = self.lib.oracle_check_encoding(C.byref(tb), nodes.ctypes.data, nodes.shape[0], lo2.ctypes.data, hi2.ctypes.data,
                                              wn.ctypes.data if wn.size else None, wl.ctypes.data if wl.size else None, ltree.wroot, msg, 256, C.byref(loose))
         return bad, msg.value.decode(), loose.value
+
+    # ------------------------------------------------------------------ collision detection
+    def collide(self, tb_a, tb_b, capacity=1 << 22):
+        out = np.empty(capacity, np.uint64)
+        stats = np.zeros(3, np.uint64)
+        n = self.lib.oracle_collision_detection(C.byref(tb_a), C.byref(tb_b), out.ctypes.data, capacity, stats.ctypes.data)
+        assert 0 <= n <= capacity, n
+        return out[:n].copy(), dict(node_pairs=int(stats[0]), tri_tests=int(stats[1]))
+
+    def brute_collisions(self, tris_a, tris_b, capacity=1 << 22):
+        a = np.ascontiguousarray(tris_a, np.float32).reshape(-1, 9)
+        b = np.ascontiguousarray(tris_b, np.float32).reshape(-1, 9)
+        out = np.empty(capacity, np.uint64)
+        n = self.lib.oracle_brute_collisions(a.ctypes.data, a.shape[0], b.ctypes.data, b.shape[0], out.ctypes.data, capacity)
+        assert 0 <= n <= capacity
+        return out[:n].copy()
+
+    def sat(self, a9, b9):
+        a, b = np.ascontiguousarray(a9, np.float32), np.ascontiguousarray(b9, np.float32)
+        return bool(self.lib.oracle_sat(a.ctypes.data, b.ctypes.data))
