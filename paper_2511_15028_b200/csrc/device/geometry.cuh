@@ -12,7 +12,7 @@ struct RayCtx {
   float ox, oy, oz, tmax;
   float dx, dy, dz;
   float rdx, rdy, rdz;  // 1.0 / direction, hoisted (pure, geometry.scion:13)
-  bool nx, ny, nz;      // direction < 0.0 per axis (-0.0 is not negative)
+  uint32_t neg;         // bit a set iff direction[a] < 0.0 (-0.0 is not negative); one register instead of three flags
 };
 
 SCION_DEV RayCtx make_ray(float ox, float oy, float oz, float tmax, float dx, float dy, float dz) {
@@ -20,15 +20,16 @@ SCION_DEV RayCtx make_ray(float ox, float oy, float oz, float tmax, float dx, fl
   r.ox = ox; r.oy = oy; r.oz = oz; r.tmax = tmax;
   r.dx = dx; r.dy = dy; r.dz = dz;
   r.rdx = 1.0f / dx; r.rdy = 1.0f / dy; r.rdz = 1.0f / dz;
-  r.nx = dx < 0.0f; r.ny = dy < 0.0f; r.nz = dz < 0.0f;
+  r.neg = (dx < 0.0f ? 1u : 0u) | (dy < 0.0f ? 2u : 0u) | (dz < 0.0f ? 4u : 0u);
   return r;
 }
 
 // intersectsp_ray_aabb, geometry.scion:12-22.  Returns `some`; t_near/t_far are the interval.
 SCION_DEV bool ray_aabb(const RayCtx& r, const f32x3& lo, const f32x3& hi, float& t_near, float& t_far) {
-  const float nx = r.nx ? hi.x : lo.x, fx = r.nx ? lo.x : hi.x;
-  const float ny = r.ny ? hi.y : lo.y, fy = r.ny ? lo.y : hi.y;
-  const float nz = r.nz ? hi.z : lo.z, fz = r.nz ? lo.z : hi.z;
+  const bool sx = (r.neg & 1u) != 0u, sy = (r.neg & 2u) != 0u, sz = (r.neg & 4u) != 0u;
+  const float nx = sx ? hi.x : lo.x, fx = sx ? lo.x : hi.x;
+  const float ny = sy ? hi.y : lo.y, fy = sy ? lo.y : hi.y;
+  const float nz = sz ? hi.z : lo.z, fz = sz ? lo.z : hi.z;
   const float t_nx = (nx - r.ox) * r.rdx, t_fx = (fx - r.ox) * r.rdx;
   const float t_ny = (ny - r.oy) * r.rdy, t_fy = (fy - r.oy) * r.rdy;
   const float t_nz = (nz - r.oz) * r.rdz, t_fz = (fz - r.oz) * r.rdz;

@@ -327,14 +327,19 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
   }
 }
 
-enum : int { kFetch = 0, kNode = 1, kPrim = 2 };
+// lane modes; "stepping" lanes are those with mode >= kNode
+enum : int { kFetch = 0, kPrim = 1, kNode = 2, kPop = 3 };
 #ifndef SCION_PREFETCH
 #define SCION_PREFETCH 1
 #endif
+#ifndef SCION_INNER
+#define SCION_INNER 4
+#endif
 constexpr bool kPrefetch = SCION_PREFETCH != 0;  // L2-prefetch a node record when its reference is pushed (+3-4 % on C5, binary)
 constexpr bool kPrefetchWide = false;             // 8-wide: up to 8 prefetches per node, most culled later: -4 % on C5
-constexpr uint32_t kFetchEvery = 2;  // look for idle lanes every kFetchEvery-th iteration
-constexpr uint32_t kPrimEvery = 4;   // look for waiting PRIM lanes every kPrimEvery-th iteration
+constexpr int kInner = SCION_INNER;  // node steps between two looks at the warp (idle lanes to refill, lanes waiting with a leaf)
+constexpr uint32_t kFetchEvery = 2;  // (8-wide / CPQ kernels) look for idle lanes every kFetchEvery-th iteration
+constexpr uint32_t kPrimEvery = 4;   // (8-wide / CPQ kernels) look for waiting PRIM lanes every kPrimEvery-th iteration
 
 // keeps the result-store address arithmetic inside the (rare) retire branch instead of letting the
 // compiler hoist it into every loop iteration (9 SASS instructions per iteration in v3)
@@ -344,17 +349,135 @@ SCION_DEV uint64_t opaque(uint64_t q) {
 }
 
 // ------------------------------------------------------------------------------------------
-// closest_hit, binary + DOP-14 families
+// Lane-private LIFO addressed by ONE register (kernel v6).  `top` is the shared-space byte address
+// of the slot the next push writes: window + 4*tid + depth*kSlot; word w of an entry lives at
+// +w*4*kBlockThreads, so every 32-bit access of a warp hits 32 different banks whatever the mix of
+// depths.  Depth tests compare (top - window) with constants (4*tid < kSlot), so neither the depth
+// nor the thread's base address occupies a register.  Entries beyond the shared-memory share go
+// to a local array (rare: the window holds the first 32 references of a 4-byte-reference layout).
 // ------------------------------------------------------------------------------------------
+template <class Entry>
+struct LaneStack {
+  static_assert(sizeof(Entry) % 4 == 0, "stack entries are stored as 32-bit words");
+  static constexpr int kWords = (int)sizeof(Entry) / 4;
+  static constexpr uint32_t kSlot = (uint32_t)kBlockThreads * 4u * (uint32_t)kWords;
+  static constexpr int kFit = (int)((uint32_t)kStackSmemBytesPerBlock / kSlot);
+  static constexpr int kSmem = kFit < SCION_STACK_DEPTH ? kFit : SCION_STACK_DEPTH;
+  static_assert(kSmem >= 1, "the shared-memory window must hold at least one entry per thread");
+  static constexpr int kDeep = SCION_STACK_DEPTH - kSmem > 0 ? SCION_STACK_DEPTH - kSmem : 1;
+  static constexpr uint32_t kSmemBytes = (uint32_t)kSmem * kSlot;
+
+  SCION_DEV static void store(uint32_t a, const Entry& e) {
+    uint32_t w[kWords];
+    memcpy(w, &e, sizeof(Entry));
+#pragma unroll
+    for (int i = 0; i < kWords; i++) asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + (uint32_t)(i * 4 * kBlockThreads)), "r"(w[i]));
+  }
+  SCION_DEV static void load(uint32_t a, Entry& e) {
+    uint32_t w[kWords];
+#pragma unroll
+    for (int i = 0; i < kWords; i++) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(a + (uint32_t)(i * 4 * kBlockThreads)));
+    memcpy(&e, w, sizeof(Entry));
+  }
+};
+
+// Warp-cooperative leaf phase, v6.  Same contract as coop_triangles (owners fold the results of
+// their own range in ascending primitive order with the strict `t < best` rule = the sequential
+// foreach of chrt.scion:10-15), cheaper bookkeeping: an owner publishes only the FIRST slot of its
+// run (one byte store) and the OR of the start bits (one REDUX); a worker finds its run with one
+// FLO over the start mask.  The owner's direction comes from the per-thread stash in shared
+// memory (it is not needed by the node phase, so it does not occupy registers there).
+struct CoopScratch2 {
+  float t[32];
+  uint8_t owner[32];
+};
+struct alignas(16) RayStash {
+  float dx, dy, dz;
+  uint32_t pad;
+};
+template <class L>
+SCION_DEV uint32_t coop_triangles2(const TreeView& T, bool own, float ox, float oy, float oz, float tmax, const RayStash* __restrict__ warp_stash,
+                                   uint32_t& prim_i, uint32_t prim_end, float& best_t, uint32_t& best_prim, CoopScratch2& sc) {
+  static_assert(L::kStride_primitives == 36, "Triangle stride");
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t tested = 0;
+  for (;;) {
+    const uint32_t remaining = own ? prim_end - prim_i : 0u;
+    if (__ballot_sync(kFullMask, remaining != 0u) == 0u) break;
+    const uint32_t c = remaining < 32u ? remaining : 32u;
+    uint32_t incl = c;  // inclusive prefix sum over lanes
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFullMask, incl, d);
+      if (lane >= (unsigned)d) incl += v;
+    }
+    const uint32_t excl = incl - c;
+    const bool starts_run = c != 0u && excl < 32u;
+    const uint32_t take = starts_run ? (c < 32u - excl ? c : 32u - excl) : 0u;
+    if (starts_run) sc.owner[excl] = (uint8_t)lane;
+    const unsigned starts = __reduce_or_sync(kFullMask, starts_run ? (1u << excl) : 0u);
+    const uint32_t total = __shfl_sync(kFullMask, incl, 31);
+    __syncwarp();
+    const bool work = lane < total;  // total may exceed 32; lanes are 0..31
+    // the run that covers slot `lane` starts at the highest start bit at or below it
+    const unsigned below = starts & (0xffffffffu >> (31u - lane));
+    const unsigned first = 31u - (unsigned)__clz((int)(below | 1u));
+    const unsigned o = sc.owner[first];
+    const uint32_t kk = lane - first;
+    RayCtx r;
+    r.ox = __shfl_sync(kFullMask, ox, o);
+    r.oy = __shfl_sync(kFullMask, oy, o);
+    r.oz = __shfl_sync(kFullMask, oz, o);
+    r.tmax = __shfl_sync(kFullMask, tmax, o);
+    const uint32_t pi = __shfl_sync(kFullMask, prim_i, o) + kk;
+    float t = scion::inf();
+    if (work) {
+      const RayStash d = warp_stash[o];
+      r.dx = d.dx; r.dy = d.dy; r.dz = d.dz;
+      float tri[9];
+      load_triangle36(T.buf[L::kBuf_primitives], pi, tri);
+      float th;
+      if (ray_tri_mt(r, tri, th)) t = th;
+    }
+    sc.t[lane] = t;
+    __syncwarp();
+    for (uint32_t k = 0; k < take; k++) {
+      const float th = sc.t[excl + k];
+      if (th < best_t) {  // a miss is +inf and never passes
+        best_t = th;
+        best_prim = prim_i + k;
+      }
+    }
+    prim_i += take;
+    tested += take;
+    __syncwarp();
+  }
+  return tested;
+}
+
+// ------------------------------------------------------------------------------------------
+// closest_hit, binary + DOP-14 families (kernel v6)
+//
+// Per-lane state machine.  A *step* (lanes in kNode / kPop) is: [kPop: take the next pending
+// reference off the stack, or retire the query when the stack is empty] -> decode one node ->
+// bounds test -> interior hit: push right, continue with left (kNode) | leaf hit: park the
+// primitive range (kPrim) | otherwise kPop.  Deferring the pop to the start of the next step puts
+// the push and the pop on the same straight-line path (predicated STS / LDS) instead of two
+// divergent branches that each ran at ~12/32 lanes in v5 (profiles/r1_ncu_v5_c5_q16.txt).
+// kInner steps run back to back; only then does the warp look for idle lanes (refill) and for
+// lanes waiting with a leaf (cooperative PRIM phase).
+//
 // STAGE > 0 (experimental variant 2): the first STAGE node records of the array are copied into
 // shared memory with one TMA bulk copy (cp.async.bulk + mbarrier, SASS UBLKCP) at CTA start and
 // served from there by the emitted decode<true>().  In a preorder array that prefix is the root,
 // the left spine and the left-most subtrees.  Measured effect: see DESIGN.md §5.
+// ------------------------------------------------------------------------------------------
 template <class L, bool COUNT, int STAGE = 0>
 __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
+  using LS = LaneStack<Ref>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Stage stage;
   if constexpr (STAGE > 0) {
@@ -370,7 +493,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     }
     __syncthreads();
     if (threadIdx.x == 0 && bytes > 0) {
-      const uint8_t* src = T.buf[L::kStageBuffer] + T.seg_base[L::kStageBuffer][0];
+      const uint8_t* src = T.buf[L::kStageBuffer];
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                        (uint32_t)__cvta_generic_to_shared(dst)),
@@ -385,91 +508,110 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     stage.base = dst;
     stage.count = cnt;
   }
-  __shared__ CoopScratch coop[kBlockThreads / 32];
-  HybridStack<Ref> stack;
-  stack.init(smem_raw);
+  __shared__ CoopScratch2 coop[kBlockThreads / 32];
+  __shared__ RayStash stash[kBlockThreads];          // ray direction: only the leaf phase needs it
+  __shared__ unsigned long long stash_q[kBlockThreads];  // query index: only the retire path needs it
+  Ref deep[LS::kDeep];
+  uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  asm volatile("" : "+r"(window));  // opaque: kept in a register instead of being re-derived (S2R CgaCtaId + 3) at every push and pop
+  uint32_t top = window + threadIdx.x * 4u;
   WorkFetcher work;
   (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
-  int sp = 0;
-  uint64_t q = 0;
   RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
   float best_t = 0;
-  uint32_t best_prim = 0, st = 0, prim_i = 0, prim_end = 0;
+  uint32_t best_prim = 0, prim_i = 0, prim_end = 0;
   Ref cur = L::root(T);
 
-  // retire the lane's query or continue with the next pending subtree
-  auto pop_or_finish = [&]() {
-    if (sp == 0 || st != SCION_Q_OK) {
-      const uint64_t qq = opaque(q);
-      hits[qq] = scion_hit{best_t, best_prim};
-      if (status) status[qq] = st;
-      tally.store(counters, qq);
-      mode = kFetch;
-    } else {
-      cur = stack.pop(sp);
+  auto retire = [&](uint32_t st) {
+    const uint64_t qq = opaque(stash_q[threadIdx.x]);
+    hits[qq] = scion_hit{best_t, best_prim};
+    if (status) status[qq] = st;
+    tally.store(counters, qq);
+    mode = kFetch;
+  };
+
+  auto step = [&]() {
+    if (mode == kPop) {
+      const uint32_t rel = top - window;  // depth * kSlot + 4 * tid, 4 * tid < kSlot
+      if (rel - LS::kSlot < LS::kSmemBytes) {  // 1 <= depth <= kSmem: the entry is in shared memory
+        top -= LS::kSlot;
+        LS::load(top, cur);
+      } else if (rel < LS::kSlot) {  // empty: the query is done
+        retire(SCION_Q_OK);
+        return;
+      } else {
+        top -= LS::kSlot;
+        cur = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+      }
+    }
+    typename L::Node node;
+    L::template decode<(STAGE > 0)>(T, cur, node, stage);
+    tally.visit();
+    float t_near;
+    const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
+    const bool leaf = node.variant == L::kLeaf;
+    mode = kPop;
+    if (hit && leaf) {
+      const uint32_t b = (uint32_t)node.data.begin, e = (uint32_t)node.data.end;
+      if (b < e) {
+        prim_i = b;
+        prim_end = e;
+        mode = kPrim;
+      }
+    } else if (hit && t_near < best_t) {
+      // reference discipline: pop self, push right, push left => occupancy depth + 2
+      const uint32_t rel = top - window;
+      if (COUNT) tally.stack(rel / LS::kSlot + 2u);
+      if (rel < LS::kSmemBytes) {
+        LS::store(top, node.right);
+      } else {
+        const uint32_t depth = rel / LS::kSlot;
+        if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
+          retire(SCION_Q_STACK_OVERFLOW);
+          return;
+        }
+        deep[depth - (uint32_t)LS::kSmem] = node.right;
+      }
+      top += LS::kSlot;
+      if (kPrefetch) L::prefetch(T, node.right);
+      cur = node.left;
       mode = kNode;
     }
   };
 
-  for (uint32_t it = 0;; it++) {
+  for (;;) {
+    // ---- NODE: kInner steps per lane without looking at the rest of the warp
+#pragma unroll 1
+    for (int k = 0; k < kInner; k++) {
+      if (mode >= kNode) step();
+    }
     // ---- FETCH: refill idle lanes
-    const unsigned idle = (it % kFetchEvery) == 0u ? __ballot_sync(kFullMask, mode == kFetch) : 0u;
-    if (idle) {
-      if (__popc(idle) >= kRefillMin || idle == kFullMask || work.exhausted) {
-        uint64_t nq;
-        if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
-          q = nq;
-          ray = load_ray(rays, q);
-          best_t = scion::inf();
-          best_prim = SCION_MISS_PRIM;
-          st = SCION_Q_OK;
-          tally.reset();
-          sp = 0;
-          cur = L::root(T);
-          mode = kNode;
-        }
-        if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    if (idle && (__popc(idle) >= kRefillMin || work.exhausted)) {
+      uint64_t nq;
+      if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
+        ray = load_ray(rays, nq);
+        stash[threadIdx.x] = RayStash{ray.dx, ray.dy, ray.dz, 0u};
+        stash_q[threadIdx.x] = nq;
+        best_t = scion::inf();
+        best_prim = SCION_MISS_PRIM;
+        tally.reset();
+        top = window + threadIdx.x * 4u;
+        cur = L::root(T);
+        mode = kNode;
       }
+      if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
     }
-    // ---- NODE: decode one node, test its bounds
-    if (mode == kNode) {
-      typename L::Node node;
-      L::template decode<(STAGE > 0)>(T, cur, node, stage);
-      tally.visit();
-      float t_near;
-      const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
-      if (hit && node.variant == L::kLeaf) {
-        prim_i = (uint32_t)node.data.begin;
-        prim_end = (uint32_t)node.data.end;
-        if (prim_i < prim_end) mode = kPrim;
-        else pop_or_finish();
-      } else if (hit && t_near < best_t) {
-        // reference discipline: pop self, push right, push left => occupancy sp + 2
-        tally.stack((uint32_t)sp + 2u);
-        if (sp + 2 > SCION_STACK_DEPTH) {
-          st = SCION_Q_STACK_OVERFLOW;
-          pop_or_finish();
-        } else {
-          stack.push(sp, node.right);
-          if (kPrefetch) L::prefetch(T, node.right);
-          cur = node.left;
-        }
-      } else {
-        pop_or_finish();
-      }
-    }
-    // ---- PRIM: one primitive per waiting lane, batched
-    const unsigned pmask = (it % kPrimEvery) == kPrimEvery - 1u ? __ballot_sync(kFullMask, mode == kPrim) : 0u;
-    if (pmask) {
-      const bool run = __popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u;
-      if (run) {  // warp-uniform
-        const bool own = mode == kPrim;
-        const uint32_t done = coop_triangles<L>(T, own, ray, prim_i, prim_end, best_t, best_prim, coop[threadIdx.x >> 5]);
-        if (COUNT) tally.prim_tests += done;
-        if (own) pop_or_finish();
-      }
+    // ---- PRIM: all 32 lanes test the parked (owner, triangle) pairs
+    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    if (pmask && (__popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode >= kNode) == 0u)) {
+      const bool own = mode == kPrim;
+      const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, prim_end, best_t,
+                                               best_prim, coop[threadIdx.x >> 5]);
+      if (COUNT) tally.prim_tests += done;
+      if (own) mode = kPop;
     }
   }
 }
@@ -494,7 +636,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   using Entry = WideEntry<Ref>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CoopScratch coop[kBlockThreads / 32];
   HybridStack<Entry> stack;
   stack.init(smem_raw);
@@ -614,7 +756,7 @@ __global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, c
                                                              scion_cp* __restrict__ out, uint32_t* __restrict__ status,
                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   HybridStack<Ref> stack;
   stack.init(smem_raw);
   WorkFetcher work;

@@ -327,6 +327,7 @@ struct Emitter {
       std::ostringstream addr;
       addr << "tree__.buf[" << buf.id << "] + ";
       if (buf.is_arena) addr << "(uint64_t)(" << index_expr << ")";
+      else if (s == 0) addr << "(uint64_t)(" << index_expr << ") * " << bytes << "ull";  // segment 0 starts at the buffer base (plan.cpp:333-347)
       else addr << "tree__.seg_base[" << buf.id << "][" << s << "] + (uint64_t)(" << index_expr << ") * " << bytes << "ull";
       if (stageable && s == 0 && !buf.is_arena) {
         out << pad << "if constexpr (STAGED) {\n";
@@ -635,7 +636,7 @@ struct Emitter {
         const Buffer& b = *primary_buf;
         out << "    scion::prefetch_l2(tree__.buf[" << b.id << "] + ";
         if (b.is_arena) out << "(uint64_t)(" << index_expr << ")";
-        else out << "tree__.seg_base[" << b.id << "][0] + (uint64_t)(" << index_expr << ") * " << b.segments[0].stride_bytes << "ull";
+        else out << "(uint64_t)(" << index_expr << ") * " << b.segments[0].stride_bytes << "ull";
         out << ");\n";
       } else {
         // reference-encoded variants: prefetch only the arm(s) that live in an indirect group
@@ -649,7 +650,7 @@ struct Emitter {
             const Buffer& b = *it->second.buf;
             uint64_t stride = b.segments[0].stride_bytes;
             out << "    if (disc__ == " << arm.value << ") {\n";
-            out << "      const uint8_t* p__ = tree__.buf[" << b.id << "] + tree__.seg_base[" << b.id << "][0] + (uint64_t)(" << ex(arm.from_key, true) << ") * " << stride << "ull;\n";
+            out << "      const uint8_t* p__ = tree__.buf[" << b.id << "] + (uint64_t)(" << ex(arm.from_key, true) << ") * " << stride << "ull;\n";
             for (uint64_t o = 0; o < stride; o += 128) out << "      scion::prefetch_l2(p__ + " << o << ");\n";
             if (stride % 128 != 0 && stride > 64) out << "      scion::prefetch_l2(p__ + " << stride - 1 << ");  // the record may straddle a line\n";
             out << "    }\n";
