@@ -40,8 +40,14 @@ namespace scion {
 constexpr int kBlockThreads = 128;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kChunk = SCION_CHUNK;     // queries a warp takes from the global counter at a time
-constexpr int kRefillMin = 4;   // refill when at least this many lanes are idle (or all of them)
-constexpr int kPrimMin = 8;     // run the PRIM phase when at least this many lanes wait in it
+#ifndef SCION_REFILL_MIN
+#define SCION_REFILL_MIN 4
+#endif
+#ifndef SCION_PRIM_MIN
+#define SCION_PRIM_MIN 6
+#endif
+constexpr int kRefillMin = SCION_REFILL_MIN;   // refill when at least this many lanes are idle (or all of them)
+constexpr int kPrimMin = SCION_PRIM_MIN;       // run the PRIM phase when at least this many lanes wait in it
 
 // Hybrid traversal stack (see header comment).  kSmem is sized so that one CTA uses 16 KB of
 // shared memory whatever the entry size.
@@ -327,8 +333,7 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
   }
 }
 
-// lane modes; "stepping" lanes are those with mode >= kNode
-enum : int { kFetch = 0, kPrim = 1, kNode = 2, kPop = 3 };
+enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
 #ifndef SCION_PREFETCH
 #define SCION_PREFETCH 1
 #endif
@@ -458,12 +463,12 @@ SCION_DEV uint32_t coop_triangles2(const TreeView& T, bool own, float ox, float 
 // ------------------------------------------------------------------------------------------
 // closest_hit, binary + DOP-14 families (kernel v6)
 //
-// Per-lane state machine.  A *step* (lanes in kNode / kPop) is: [kPop: take the next pending
-// reference off the stack, or retire the query when the stack is empty] -> decode one node ->
-// bounds test -> interior hit: push right, continue with left (kNode) | leaf hit: park the
-// primitive range (kPrim) | otherwise kPop.  Deferring the pop to the start of the next step puts
-// the push and the pop on the same straight-line path (predicated STS / LDS) instead of two
-// divergent branches that each ran at ~12/32 lanes in v5 (profiles/r1_ncu_v5_c5_q16.txt).
+// Per-lane state machine.  A *step* (lanes in kNode) is: decode one node -> bounds test ->
+// interior hit: push right, continue with left | leaf hit: park the primitive range (kPrim) |
+// otherwise pop the next pending reference.  Push and pop are predicated STS / LDS on ONE
+// straight-line path; in v5 they were two divergent branches that each ran at ~12/32 lanes
+// (profiles/r1_ncu_v5_c5_q16.txt).  Retiring a query, entries beyond the shared-memory window
+// and overflow share one rarely taken branch.
 // kInner steps run back to back; only then does the warp look for idle lanes (refill) and for
 // lanes waiting with a leaf (cooperative PRIM phase).
 //
@@ -532,52 +537,66 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     mode = kFetch;
   };
 
-  auto step = [&]() {
-    if (mode == kPop) {
-      const uint32_t rel = top - window;  // depth * kSlot + 4 * tid, 4 * tid < kSlot
-      if (rel - LS::kSlot < LS::kSmemBytes) {  // 1 <= depth <= kSmem: the entry is in shared memory
-        top -= LS::kSlot;
-        LS::load(top, cur);
-      } else if (rel < LS::kSlot) {  // empty: the query is done
-        retire(SCION_Q_OK);
-        return;
-      } else {
-        top -= LS::kSlot;
-        cur = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
-      }
+  // next pending reference, or retire the query when the stack is empty (used after a leaf phase
+  // and on the rare paths of step())
+  auto pop_or_retire = [&]() {
+    const uint32_t rel = top - window;  // depth * kSlot + 4 * tid, 4 * tid < kSlot
+    if (rel - LS::kSlot < LS::kSmemBytes) {  // 1 <= depth <= kSmem: the entry is in shared memory
+      top -= LS::kSlot;
+      LS::load(top, cur);
+      mode = kNode;
+    } else if (rel < LS::kSlot) {  // empty: the query is done
+      retire(SCION_Q_OK);
+    } else {
+      top -= LS::kSlot;
+      cur = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+      mode = kNode;
     }
+  };
+
+  auto step = [&]() {
     typename L::Node node;
     L::template decode<(STAGE > 0)>(T, cur, node, stage);
     tally.visit();
     float t_near;
     const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
     const bool leaf = node.variant == L::kLeaf;
-    mode = kPop;
-    if (hit && leaf) {
-      const uint32_t b = (uint32_t)node.data.begin, e = (uint32_t)node.data.end;
-      if (b < e) {
-        prim_i = b;
-        prim_end = e;
-        mode = kPrim;
-      }
-    } else if (hit && t_near < best_t) {
-      // reference discipline: pop self, push right, push left => occupancy depth + 2
-      const uint32_t rel = top - window;
-      if (COUNT) tally.stack(rel / LS::kSlot + 2u);
-      if (rel < LS::kSmemBytes) {
-        LS::store(top, node.right);
-      } else {
+    const uint32_t pb = leaf ? (uint32_t)node.data.begin : 0u, pe = leaf ? (uint32_t)node.data.end : 0u;
+    const bool p_prim = hit && leaf && pb < pe;
+    const bool p_push = hit && !leaf && t_near < best_t;
+    const uint32_t rel = top - window;
+    // the common push (depth < kSmem) and pop (1 <= depth <= kSmem) are straight-line predicated
+    // code; everything else (empty stack = retire, entries beyond the shared-memory window,
+    // overflow) is one rarely taken branch
+    const bool fast = p_push ? rel < LS::kSmemBytes : rel - LS::kSlot < LS::kSmemBytes;
+    if (COUNT && p_push) tally.stack(rel / LS::kSlot + 2u);  // reference discipline: pop self, push right, push left
+    if (!(fast || p_prim)) {
+      if (p_push) {
         const uint32_t depth = rel / LS::kSlot;
         if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
           retire(SCION_Q_STACK_OVERFLOW);
-          return;
+        } else {
+          deep[depth - (uint32_t)LS::kSmem] = node.right;
+          top += LS::kSlot;
+          cur = node.left;
         }
-        deep[depth - (uint32_t)LS::kSmem] = node.right;
+      } else {
+        pop_or_retire();
       }
-      top += LS::kSlot;
+      return;
+    }
+    if (p_prim) {
+      prim_i = pb;
+      prim_end = pe;
+      mode = kPrim;
+    } else if (p_push) {
+      LS::store(top, node.right);
       if (kPrefetch) L::prefetch(T, node.right);
+      top += LS::kSlot;
       cur = node.left;
-      mode = kNode;
+    } else {
+      top -= LS::kSlot;
+      LS::load(top, cur);
     }
   };
 
@@ -585,7 +604,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     // ---- NODE: kInner steps per lane without looking at the rest of the warp
 #pragma unroll 1
     for (int k = 0; k < kInner; k++) {
-      if (mode >= kNode) step();
+      if (mode == kNode) step();
     }
     // ---- FETCH: refill idle lanes
     const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
@@ -606,12 +625,12 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     }
     // ---- PRIM: all 32 lanes test the parked (owner, triangle) pairs
     const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
-    if (pmask && (__popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode >= kNode) == 0u)) {
+    if (pmask && (__popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u)) {
       const bool own = mode == kPrim;
       const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, prim_end, best_t,
                                                best_prim, coop[threadIdx.x >> 5]);
       if (COUNT) tally.prim_tests += done;
-      if (own) mode = kPop;
+      if (own) pop_or_retire();
     }
   }
 }
