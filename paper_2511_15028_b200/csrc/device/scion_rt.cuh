@@ -316,9 +316,11 @@ SCION_HOSTDEV uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t shift_bits) {
 #endif
 }
 
-SCION_HOSTDEV void prefetch_l2(const void* p) {
+template <int LEVEL>
+SCION_HOSTDEV void prefetch_to(const void* p) {
 #if defined(__CUDA_ARCH__)
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  if constexpr (LEVEL == 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  else asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 #else
   (void)p;
 #endif

@@ -23,6 +23,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "geometry.cuh"
 #include "scion_b200.h"
 
@@ -35,7 +37,10 @@ namespace scion {
 #define SCION_CHUNK 128
 #endif
 #ifndef SCION_STACK_SMEM
-#define SCION_STACK_SMEM (16 * 1024)
+// Shared memory and L1 share 256 KB per SM: at 9 CTAs/SM a 16 KB window leaves ~60 KB of L1, 12 KB
+// ~92 KB, 8 KB ~124 KB.  Measured (C5 probe, pbrt-q16, kernel v7): 20 KB 1265, 16 KB 2106, 12 KB
+// 2178, 10 KB 2183, 8 KB 2176, 6 KB 1979, 4 KB 1747 Mrays/s (small windows send pushes to local memory).
+#define SCION_STACK_SMEM (12 * 1024)
 #endif
 constexpr int kBlockThreads = 128;
 constexpr unsigned kFullMask = 0xffffffffu;
@@ -337,6 +342,9 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
 #ifndef SCION_PREFETCH
 #define SCION_PREFETCH 1
 #endif
+#ifndef SCION_PF_NEXT
+#define SCION_PF_NEXT 0
+#endif
 #ifndef SCION_INNER
 #define SCION_INNER 4
 #endif
@@ -557,6 +565,9 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
   auto step = [&]() {
     typename L::Node node;
     L::template decode<(STAGE > 0)>(T, cur, node, stage);
+#if SCION_PF_NEXT
+    if constexpr (std::is_integral<Ref>::value) L::template prefetch<1>(T, (Ref)(cur + 1));
+#endif
     tally.visit();
     float t_near;
     const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);

@@ -629,12 +629,13 @@ struct Emitter {
     }
     // prefetch(): pull the record a reference designates into L2 ahead of its visit (issued by the
     // traversal when the reference is pushed on the stack)
+    out << "  template <int LEVEL = 2>  // 2: into L2 (a reference that was pushed); 1: into L1 (a record about to be visited)\n";
     out << "  SCION_HOSTDEV static void prefetch(const scion::TreeView& tree__, const Ref& ref__) {\n";
     {
       std::string index_expr = ref_is_struct ? "ref__." + primary->index_binding : std::string("ref__");
       if (primary_buf && !primary_buf->segments.empty()) {
         const Buffer& b = *primary_buf;
-        out << "    scion::prefetch_l2(tree__.buf[" << b.id << "] + ";
+        out << "    scion::prefetch_to<LEVEL>(tree__.buf[" << b.id << "] + ";
         if (b.is_arena) out << "(uint64_t)(" << index_expr << ")";
         else out << "(uint64_t)(" << index_expr << ") * " << b.segments[0].stride_bytes << "ull";
         out << ");\n";
@@ -651,8 +652,8 @@ struct Emitter {
             uint64_t stride = b.segments[0].stride_bytes;
             out << "    if (disc__ == " << arm.value << ") {\n";
             out << "      const uint8_t* p__ = tree__.buf[" << b.id << "] + (uint64_t)(" << ex(arm.from_key, true) << ") * " << stride << "ull;\n";
-            for (uint64_t o = 0; o < stride; o += 128) out << "      scion::prefetch_l2(p__ + " << o << ");\n";
-            if (stride % 128 != 0 && stride > 64) out << "      scion::prefetch_l2(p__ + " << stride - 1 << ");  // the record may straddle a line\n";
+            for (uint64_t o = 0; o < stride; o += 128) out << "      scion::prefetch_to<LEVEL>(p__ + " << o << ");\n";
+            if (stride % 128 != 0 && stride > 64) out << "      scion::prefetch_to<LEVEL>(p__ + " << stride - 1 << ");  // the record may straddle a line\n";
             out << "    }\n";
           }
         }
