@@ -6,6 +6,10 @@
 #pragma once
 #include "scion_rt.cuh"
 
+#ifndef SCION_TRI_LDG32
+#define SCION_TRI_LDG32 0
+#endif
+
 namespace scion {
 
 struct RayCtx {
@@ -149,7 +153,11 @@ SCION_DEV f32x3 closest_point_triangle(const f32x3& p, const float* t) {
 // loads instead of nine 4-byte ones — and re-aligned in registers.  Device buffers carry 16
 // bytes of slack so the covering read of the last triangle stays inside the allocation.
 SCION_DEV void load_triangle36(const uint8_t* prims, uint64_t index, float (&v)[9]) {
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && SCION_TRI_LDG32
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(prims + index * 36ull);
+#pragma unroll
+  for (int j = 0; j < 9; j++) v[j] = u2f(__ldg(q + j));
+#elif defined(__CUDA_ARCH__)
   const uint64_t addr = (uint64_t)prims + index * 36ull;
   const uint4* q = reinterpret_cast<const uint4*>(addr & ~15ull);
   const uint32_t s = (uint32_t)(addr >> 2) & 3u;

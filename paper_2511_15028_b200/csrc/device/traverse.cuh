@@ -660,108 +660,182 @@ struct WideEntry {
 #ifndef SCION_MINB8
 #define SCION_MINB8 4
 #endif
+#ifndef SCION_INNER8
+#define SCION_INNER8 1
+#endif
+#ifndef SCION_PRIM_MIN8
+#define SCION_PRIM_MIN8 6
+#endif
+#ifndef SCION_REFILL_MIN8
+#define SCION_REFILL_MIN8 4
+#endif
+// 8-wide kernel v7.  Same lane state machine as chrt2_kernel with three differences that follow from
+// the shape of an 8-wide visit (one ~500-instruction interior step instead of ~100):
+//   * a step only ever decodes INTERIOR records: where the variant is encoded in the reference
+//     (every 8-wide layout of the corpus, L::kVariantInRef) a leaf reference is recognised when it is
+//     popped and the lane parks its primitive range at once, instead of spending a whole step slot on it;
+//   * the first passing child is continued with directly (registers); only the other passing children
+//     are stored, at their final positions, so that they pop in slot order (chrt8.scion:7);
+//   * the warp looks for idle / parked lanes after every step (SCION_INNER8 = 1): a waiting lane costs
+//     1/32 of a 500-instruction step.
 template <class L, bool COUNT>
 __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   using Entry = WideEntry<Ref>;
+  using LS = LaneStack<Entry>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ CoopScratch coop[kBlockThreads / 32];
-  HybridStack<Entry> stack;
-  stack.init(smem_raw);
+  __shared__ CoopScratch2 coop[kBlockThreads / 32];
+  __shared__ RayStash stash[kBlockThreads];
+  __shared__ unsigned long long stash_q[kBlockThreads];
+  Entry deep[LS::kDeep];
+  uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  asm volatile("" : "+r"(window));
+  uint32_t top = window + threadIdx.x * 4u;
   WorkFetcher work;
   (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
-  int sp = 0;
-  uint64_t q = 0;
   RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
   float best_t = 0;
-  uint32_t best_prim = 0, st = 0, prim_i = 0, prim_end = 0;
+  uint32_t best_prim = 0, prim_i = 0, prim_end = 0;
   Ref cur = L::root(T);
 
-  auto pop_or_finish = [&]() {
-    bool found = false;
-    if (st == SCION_Q_OK) {
-      while (sp > 0) {
-        const Entry e = stack.pop(sp);
-        if (e.t_near < best_t) { cur = e.ref; found = true; break; }
+  auto retire = [&](uint32_t st) {
+    const uint64_t qq = opaque(stash_q[threadIdx.x]);
+    hits[qq] = scion_hit{best_t, best_prim};
+    if (status) status[qq] = st;
+    tally.store(counters, qq);
+    mode = kFetch;
+  };
+  // `cur` was just chosen: park it if the reference itself says it is a leaf
+  auto enter = [&]() {
+    mode = kNode;
+    if constexpr (L::kVariantInRef) {
+      if (L::ref_variant(cur) == L::kLeaf) {
+        typename L::Node leaf;
+        L::decode(T, cur, leaf);  // reference-only arm: no memory access
+        prim_i = (uint32_t)leaf.data.begin;
+        prim_end = (uint32_t)leaf.data.end;
+        if (prim_i < prim_end) mode = kPrim;
+        else mode = -1;  // empty leaf: nothing to do, take the next entry
       }
     }
-    if (found) {
-      mode = kNode;
-    } else {
-      const uint64_t qq = opaque(q);
-      hits[qq] = scion_hit{best_t, best_prim};
-      if (status) status[qq] = st;
-      tally.store(counters, qq);
-      mode = kFetch;
+  };
+  // next pending entry whose deferred cull `t_near < best` still passes, or retire
+  auto pop_next = [&]() {
+    for (;;) {
+      const uint32_t rel = top - window;
+      Entry e;
+      if (rel - LS::kSlot < LS::kSmemBytes) {
+        top -= LS::kSlot;
+        LS::load(top, e);
+      } else if (rel < LS::kSlot) {
+        retire(SCION_Q_OK);
+        return;
+      } else {
+        top -= LS::kSlot;
+        e = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+      }
+      if (e.t_near < best_t) {
+        cur = e.ref;
+        enter();
+        if (mode >= 0) return;
+      }
     }
   };
 
-  for (uint32_t it = 0;; it++) {
-    const unsigned idle = (it % kFetchEvery) == 0u ? __ballot_sync(kFullMask, mode == kFetch) : 0u;
-    if (idle) {
-      if (__popc(idle) >= kRefillMin || idle == kFullMask || work.exhausted) {
-        uint64_t nq;
-        if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
-          q = nq;
-          ray = load_ray(rays, q);
-          best_t = scion::inf();
-          best_prim = SCION_MISS_PRIM;
-          st = SCION_Q_OK;
-          tally.reset();
-          sp = 0;
-          cur = L::root(T);
-          mode = kNode;
-        }
-        if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
-      }
-    }
-    if (mode == kNode) {
-      typename L::Node node;
-      L::decode(T, cur, node);
+  auto step = [&]() {
+    typename L::Node node;
+    L::decode(T, cur, node);
+    if constexpr (!L::kVariantInRef) {
       if (node.variant == L::kLeaf) {
         prim_i = (uint32_t)node.data.begin;
         prim_end = (uint32_t)node.data.end;
         if (prim_i < prim_end) mode = kPrim;
-        else pop_or_finish();
-      } else {
-        tally.visit();
-        // test the eight child boxes, then store the passing ones at their final stack positions:
-        // slot k lands above every passing slot with a larger index, so the stack pops in slot order
-        // (chrt8.scion:7 `foreach c in children`).  Positional predicated stores instead of eight
-        // divergent push blocks (profiles/r1_ncu_v5_c5_q8ci.txt: 8 x 14 SASS instructions at 3/32 lanes).
-        uint32_t mask = 0;
-        float tn[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          float t_far;
-          const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn[k], t_far);
-          if (interval_intersects(ray, some, tn[k], t_far) && tn[k] < best_t) mask |= 1u << k;
-        }
-        const int m = __popc(mask);
-        tally.stack((uint32_t)(sp + m));
-        if (sp + m > SCION_STACK_DEPTH) {
-          st = SCION_Q_STACK_OVERFLOW;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; k++) stack.store_if((mask >> k) & 1u, sp + __popc(mask >> (k + 1)), Entry{node.children[k], tn[k]});
-          sp += m;
-        }
-        pop_or_finish();
+        else pop_next();
+        return;
       }
     }
-    const unsigned pmask = (it % kPrimEvery) == kPrimEvery - 1u ? __ballot_sync(kFullMask, mode == kPrim) : 0u;
-    if (pmask) {
-      const bool run = __popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u;
-      if (run) {  // warp-uniform
-        const bool own = mode == kPrim;
-        const uint32_t done = coop_triangles<L>(T, own, ray, prim_i, prim_end, best_t, best_prim, coop[threadIdx.x >> 5]);
-        if (COUNT) tally.prim_tests += done;
-        if (own) pop_or_finish();
+    tally.visit();
+    uint32_t mask = 0;
+    float tn[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      float t_far;
+      const bool some = ray_aabb(ray, node.lo[k], node.hi[k], tn[k], t_far);
+      if (interval_intersects(ray, some, tn[k], t_far) && tn[k] < best_t) mask |= 1u << k;
+    }
+    if (mask == 0u) {
+      pop_next();
+      return;
+    }
+    const uint32_t m = (uint32_t)__popc(mask);
+    const uint32_t rel = top - window;
+    const uint32_t depth = rel / LS::kSlot;
+    if (COUNT) tally.stack(depth + m);
+    if (depth + m > (uint32_t)SCION_STACK_DEPTH) {  // the reference would hold all m passing children at once
+      retire(SCION_Q_STACK_OVERFLOW);
+      return;
+    }
+    // slot k1 = lowest passing slot is visited next; the others are stored so that they pop in slot
+    // order: slot k lands above every passing slot with a larger index
+    const uint32_t rest = mask & (mask - 1u);
+    if (rel + (m - 1u) * LS::kSlot <= LS::kSmemBytes) {  // all stores land in the shared-memory window
+#pragma unroll
+      for (int k = 1; k < 8; k++) {
+        if ((rest >> k) & 1u) LS::store(top + (uint32_t)__popc(mask >> (k + 1)) * LS::kSlot, Entry{node.children[k], tn[k]});
       }
+    } else {
+#pragma unroll
+      for (int k = 1; k < 8; k++) {
+        if ((rest >> k) & 1u) {
+          const uint32_t pos = depth + (uint32_t)__popc(mask >> (k + 1));
+          if (pos < (uint32_t)LS::kSmem) LS::store(window + threadIdx.x * 4u + pos * LS::kSlot, Entry{node.children[k], tn[k]});
+          else deep[pos - (uint32_t)LS::kSmem] = Entry{node.children[k], tn[k]};
+        }
+      }
+    }
+    top += (m - 1u) * LS::kSlot;
+    Ref first = node.children[0];
+#pragma unroll
+    for (int k = 7; k >= 0; k--)
+      if ((mask >> k) & 1u) first = node.children[k];
+    cur = first;
+    enter();
+    if (mode < 0) pop_next();
+  };
+
+  for (;;) {
+#pragma unroll 1
+    for (int k = 0; k < SCION_INNER8; k++) {
+      if (mode == kNode) step();
+    }
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    if (idle && (__popc(idle) >= SCION_REFILL_MIN8 || work.exhausted)) {
+      uint64_t nq;
+      if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
+        ray = load_ray(rays, nq);
+        stash[threadIdx.x] = RayStash{ray.dx, ray.dy, ray.dz, 0u};
+        stash_q[threadIdx.x] = nq;
+        best_t = scion::inf();
+        best_prim = SCION_MISS_PRIM;
+        tally.reset();
+        top = window + threadIdx.x * 4u;
+        cur = L::root(T);
+        enter();
+        if (mode < 0) retire(SCION_Q_OK);  // the root is an empty leaf
+      }
+      if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
+    }
+    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    if (pmask && (__popc(pmask) >= SCION_PRIM_MIN8 || __ballot_sync(kFullMask, mode == kNode) == 0u)) {
+      const bool own = mode == kPrim;
+      const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, prim_end, best_t,
+                                               best_prim, coop[threadIdx.x >> 5]);
+      if (COUNT) tally.prim_tests += done;
+      if (own) pop_next();
     }
   }
 }

@@ -579,6 +579,43 @@ struct Emitter {
       out << "    return (Ref)tree__.root0;\n";
     }
     out << "  }\n";
+    // ref_variant(): where the primary split discriminates on the reference alone (reference-encoded
+    // variants, e.g. every 8-wide layout of the corpus) the traversal can tell a leaf reference from an
+    // interior one without touching memory
+    {
+      const MemberNode* split = nullptr;
+      for (auto& m : primary->members)
+        if (m->kind == MemberNode::Split && !split) split = m.get();
+      bool in_ref = split != nullptr;
+      if (split) {
+        std::set<std::string> ids;
+        collect_idents(split->value, ids);
+        for (auto& id : ids)
+          if (!ref_names.count(id)) in_ref = false;
+      }
+      out << "  static constexpr bool kVariantInRef = " << (in_ref ? "true" : "false") << ";\n";
+      out << "  SCION_HOSTDEV static int ref_variant(const Ref& ref__) {\n";
+      if (in_ref) {
+        out << "    const auto disc__ = " << ex(split->value, true) << ";\n";
+        for (size_t a = 0; a < split->arms.size(); a++) {
+          const Arm& arm = split->arms[a];
+          std::string test;
+          switch (arm.pat) {
+            case Arm::Literal: test = "disc__ == " + std::to_string(arm.value); break;
+            case Arm::Gt: test = "disc__ > " + std::to_string(arm.value); break;
+            case Arm::Lt: test = "disc__ < " + std::to_string(arm.value); break;
+            case Arm::Ge: test = "disc__ >= " + std::to_string(arm.value); break;
+            case Arm::Le: test = "disc__ <= " + std::to_string(arm.value); break;
+            case Arm::Wildcard: test = ""; break;
+          }
+          if (a + 1 == split->arms.size() || test.empty()) { out << "    return " << variant_index(arm.variant) << ";  // " << arm.variant << "\n"; break; }
+          out << "    if (" << test << ") return " << variant_index(arm.variant) << ";  // " << arm.variant << "\n";
+        }
+      } else {
+        out << "    (void)ref__;\n    return -1;  // the variant is stored in the node record\n";
+      }
+      out << "  }\n";
+    }
     // helper funcs
     for (auto& fn : func_order) {
       const Func* f = find_func(fn);

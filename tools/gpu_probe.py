@@ -127,6 +127,36 @@ if __name__ == "__main__":
             print(f"  {os.environ.get('SCION_B200_LIB','default').split('/')[-1]:16s} {layout:10s} {nr / (e0.elapsed_time(e1) / 4) / 1e3:8.1f} Mrays/s", flush=True)
             dt.free()
         sys.exit(0)
+    if "--c5split" in sys.argv:  # primary-only vs secondary-only throughput on the 10M scene
+        scene = sb.Scene.terrain(2236, seed=1)
+        lt = scene.build_sah(32, 4).collapse8()
+        lo, hi = scene.bounds()
+        nr = 1 << 25
+        d_rays = dbuf(nr * 32); d_hits = dbuf(nr * 8)
+        cam = sb.default_camera(lo, hi, True, 4096, 4096)
+        for layout in sys.argv[sys.argv.index("--c5split") + 1].split(","):
+            dt = lt.encode(layout).upload(0)
+            for kind in ("primary", "secondary"):
+                if kind == "primary":
+                    sb.gen_primary(cam, 0, 1 << 24, d_rays.data_ptr()); sb.gen_primary(cam, 0, 1 << 24, d_rays.data_ptr() + (32 << 24))
+                else:
+                    dt.gen_secondary(77, 0, nr, d_rays.data_ptr())
+                for _ in range(2): dt.closest_hit(d_rays.data_ptr(), nr, d_hits.data_ptr())
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(4): dt.closest_hit(d_rays.data_ptr(), nr, d_hits.data_ptr())
+                e1.record(); torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / 4
+                nc = 1 << 22
+                d_ctr = dbuf(nc * 16)
+                dt.closest_hit(d_rays.data_ptr(), nc, d_hits.data_ptr(), 0, d_ctr.data_ptr())
+                torch.cuda.synchronize()
+                ctr = d_ctr.cpu().numpy().view(sb.COUNTERS_DTYPE)
+                nv, npt = ctr["node_visits"].mean(), ctr["prim_tests"].mean()
+                print(f"  {layout:10s} {kind:9s} {nr / ms / 1e3:8.1f} Mrays/s  visits/ray {nv:.1f} tris/ray {npt:.1f} maxstack {ctr['max_stack'].max()} mean stack {ctr['max_stack'].mean():.1f} -> {nr * nv / ms / 1e6:.1f} Gvisits/s", flush=True)
+            dt.free()
+        sys.exit(0)
     if "--stage" in sys.argv:  # TMA-staged prefix (variant 2) vs default: identical results? timing?
         for G in (708, 2236):
             scene = sb.Scene.terrain(G, seed=1)
