@@ -855,100 +855,222 @@ SCION_DEV float cpq_node_distmin(const TreeView& T, const f32x3& p, const typena
   else return sqdist_point_aabb(p, n.low, n.high);
 }
 
+// Cooperative leaf phase of closest_point (cpq.scion:25-31), v7: same run bookkeeping as
+// coop_triangles2; the worker returns (d2, closest point); owners fold with the strict
+// `d2 < best[0]` rule in ascending primitive order.  The owner's best point lives in shared memory
+// (`best_pt`, one float4 per thread: x, y, z, primitive index) — only the fold and the retire path
+// touch it.
+struct CoopScratchCp2 {
+  float d2[32];
+  float c[32][3];
+  uint8_t owner[32];
+};
+template <class L>
+SCION_DEV uint32_t coop_points2(const TreeView& T, bool own, const f32x3& p, uint32_t& prim_i, uint32_t prim_end, float& best_d, float4* __restrict__ best_pt,
+                                CoopScratchCp2& sc) {
+  static_assert(L::kStride_primitives == 36, "Triangle stride");
+  const unsigned lane = threadIdx.x & 31u;
+  uint32_t tested = 0;
+  for (;;) {
+    const uint32_t remaining = own ? prim_end - prim_i : 0u;
+    if (__ballot_sync(kFullMask, remaining != 0u) == 0u) break;
+    const uint32_t c = remaining < 32u ? remaining : 32u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFullMask, incl, d);
+      if (lane >= (unsigned)d) incl += v;
+    }
+    const uint32_t excl = incl - c;
+    const bool starts_run = c != 0u && excl < 32u;
+    const uint32_t take = starts_run ? (c < 32u - excl ? c : 32u - excl) : 0u;
+    if (starts_run) sc.owner[excl] = (uint8_t)lane;
+    const unsigned starts = __reduce_or_sync(kFullMask, starts_run ? (1u << excl) : 0u);
+    const uint32_t total = __shfl_sync(kFullMask, incl, 31);
+    __syncwarp();
+    const bool work = lane < total;
+    const unsigned below = starts & (0xffffffffu >> (31u - lane));
+    const unsigned first = 31u - (unsigned)__clz((int)(below | 1u));
+    const unsigned o = sc.owner[first];
+    const uint32_t kk = lane - first;
+    const f32x3 q{__shfl_sync(kFullMask, p.x, o), __shfl_sync(kFullMask, p.y, o), __shfl_sync(kFullMask, p.z, o)};
+    const uint32_t pi = __shfl_sync(kFullMask, prim_i, o) + kk;
+    if (work) {
+      float tri[9];
+      load_triangle36(T.buf[L::kBuf_primitives], pi, tri);
+      const f32x3 cp = closest_point_triangle(q, tri);
+      const f32x3 x = q - cp;
+      sc.d2[lane] = dot(x, x);
+      sc.c[lane][0] = cp.x; sc.c[lane][1] = cp.y; sc.c[lane][2] = cp.z;
+    }
+    __syncwarp();
+    int won = -1;
+    for (uint32_t k = 0; k < take; k++) {
+      const float d2 = sc.d2[excl + k];
+      if (d2 < best_d) {
+        best_d = d2;
+        won = (int)k;
+      }
+    }
+    if (won >= 0) *best_pt = make_float4(sc.c[excl + won][0], sc.c[excl + won][1], sc.c[excl + won][2], __uint_as_float(prim_i + (uint32_t)won));
+    prim_i += take;
+    tested += take;
+    __syncwarp();
+  }
+  return tested;
+}
+
+#ifndef SCION_MINBC
+#define SCION_MINBC 6
+#endif
+#ifndef SCION_PRIM_MINC
+#define SCION_PRIM_MINC 6
+#endif
+#ifndef SCION_INNERC
+#define SCION_INNERC 4
+#endif
+// closest_point kernel v7.  The reference decodes a node three times on the way down: as the
+// child peek of its parent (cpq.scion:9-16), again when it is visited, and its own two children.
+// The value of every decode and of square_distance(p, box) is a pure function, and `best` does not
+// change between the peek of the NEAR child and its visit, so the kernel carries the near child's
+// decoded record and distance into the next step instead of fetching it again.  A step therefore
+// has two decode slots: X = left child (descending lane) or the popped node (popping lane), and
+// Y = right child (descending lanes only).  The instrumented build still counts every decode the
+// reference performs (identical counters), it just does not repeat the work.
 template <class L, bool COUNT>
-__global__ void __launch_bounds__(kBlockThreads) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
+__global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
                                                              scion_cp* __restrict__ out, uint32_t* __restrict__ status,
                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
+  using Node = typename L::Node;
+  using LS = LaneStack<Ref>;
+  enum : int { kPop = 3 };  // stepping lanes: kNode (record + distance of `node` are valid) or kPop (take the next pending reference first)
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  HybridStack<Ref> stack;
-  stack.init(smem_raw);
+  __shared__ CoopScratchCp2 coop[kBlockThreads / 32];
+  __shared__ float4 best_pt[kBlockThreads];
+  __shared__ unsigned long long stash_q[kBlockThreads];
+  Ref deep[LS::kDeep];
+  uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  asm volatile("" : "+r"(window));
+  uint32_t top = window + threadIdx.x * 4u;
   WorkFetcher work;
   (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
-  int sp = 0;
-  uint64_t q = 0;
-  __shared__ CoopScratchCp coop[kBlockThreads / 32];
-  f32x3 p{0.0f, 0.0f, 0.0f}, best_p{0.0f, 0.0f, 0.0f};
-  float best_d = 0;
-  uint32_t best_prim = 0, st = 0, prim_i = 0, prim_end = 0;
-  Ref cur = L::root(T);
+  f32x3 p{0.0f, 0.0f, 0.0f};
+  float best_d = 0, d = 0;
+  uint32_t prim_i = 0, prim_end = 0;
+  bool carried = false;  // (instrumented build) `node` came from its parent's peek: its visit is a decode the reference repeats
+  Node node;
+  Ref root = L::root(T);
+  Ref cur = root;  // reference of `node` (decode_cold of tree-carried layouts needs it)
 
-  auto pop_or_finish = [&]() {
-    if (sp == 0 || st != SCION_Q_OK) {
-      const uint64_t qq = opaque(q);
-      out[qq] = scion_cp{best_d, best_p.x, best_p.y, best_p.z, best_prim};
-      if (status) status[qq] = st;
-      tally.store(counters, qq);
-      mode = kFetch;
-    } else {
-      cur = stack.pop(sp);
-      mode = kNode;
-    }
+  auto retire = [&](uint32_t st) {
+    const uint64_t qq = opaque(stash_q[threadIdx.x]);
+    const float4 b = best_pt[threadIdx.x];
+    out[qq] = scion_cp{best_d, b.x, b.y, b.z, __float_as_uint(b.w)};
+    if (status) status[qq] = st;
+    tally.store(counters, qq);
+    mode = kFetch;
   };
 
-  for (uint32_t it = 0;; it++) {
-    const unsigned idle = (it % kFetchEvery) == 0u ? __ballot_sync(kFullMask, mode == kFetch) : 0u;
-    if (idle) {
-      if (__popc(idle) >= kRefillMin || idle == kFullMask || work.exhausted) {
-        uint64_t nq;
-        if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
-          q = nq;
-          p = f32x3{__ldcs(points + 3 * q), __ldcs(points + 3 * q + 1), __ldcs(points + 3 * q + 2)};
-          best_d = scion::inf();
-          best_p = f32x3{0.0f, 0.0f, 0.0f};
-          best_prim = SCION_MISS_PRIM;
-          st = SCION_Q_OK;
-          tally.reset();
-          sp = 0;
-          cur = L::root(T);
-          mode = kNode;
-        }
-        if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
-      }
-    }
+  auto step = [&]() {
+    bool go = false;  // interior: decode both children
+    Ref rx = cur, ry = cur;
     if (mode == kNode) {
-      typename L::Node node;
-      const float d = cpq_node_distmin<L>(T, p, cur, node, tally);
-      if (!(d < best_d)) {
-        pop_or_finish();
-      } else if (node.variant == L::kLeaf) {
-        prim_i = (uint32_t)node.data.begin;
-        prim_end = (uint32_t)node.data.end;
-        if (prim_i < prim_end) mode = kPrim;
-        else pop_or_finish();
-      } else {
-        float ub;
-        if constexpr (L::kFamily == SCION_FAMILY_DOP14) ub = distmax_point_aabb(p, node.lo1, node.hi1);
-        else ub = distmax_point_aabb(p, node.low, node.high);
-        if (ub < best_d) best_d = ub;  // best = (upper_bound, best[1])
-        typename L::Node ln, rn;
-        const Ref left = node.left, right = node.right;
-        const float dl = cpq_node_distmin<L>(T, p, left, ln, tally);
-        const float dr = cpq_node_distmin<L>(T, p, right, rn, tally);
-        tally.stack((uint32_t)sp + 2u);
-        if (sp + 2 > SCION_STACK_DEPTH) {
-          st = SCION_Q_STACK_OVERFLOW;
-          pop_or_finish();
-        } else if (dl < dr) {
-          stack.push(sp, right);
-          cur = left;
+      if (COUNT && carried) {
+        tally.visit();
+        if (L::kHasCold) tally.cold();
+      }
+      mode = kPop;
+      if (d < best_d) {
+        if (node.variant == L::kLeaf) {
+          prim_i = (uint32_t)node.data.begin;
+          prim_end = (uint32_t)node.data.end;
+          if (prim_i < prim_end) {
+            mode = kPrim;
+            return;
+          }
         } else {
-          stack.push(sp, left);
-          cur = right;
+          float ub;
+          if constexpr (L::kFamily == SCION_FAMILY_DOP14) ub = distmax_point_aabb(p, node.lo1, node.hi1);
+          else ub = distmax_point_aabb(p, node.low, node.high);
+          if (ub < best_d) best_d = ub;  // best = (upper_bound, best[1])
+          go = true;
+          rx = node.left;
+          ry = node.right;
         }
       }
     }
-    const unsigned pmask = (it % kPrimEvery) == kPrimEvery - 1u ? __ballot_sync(kFullMask, mode == kPrim) : 0u;
-    if (pmask) {
-      const bool run = __popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u;
-      if (run) {  // warp-uniform
-        const bool own = mode == kPrim;
-        const uint32_t done = coop_points<L>(T, own, p, prim_i, prim_end, best_d, best_p, best_prim, coop[threadIdx.x >> 5]);
-        if (COUNT) tally.prim_tests += done;
-        if (own) pop_or_finish();
+    const uint32_t rel = top - window;
+    if (!go) {  // pop the next pending reference, or retire
+      if (rel - LS::kSlot < LS::kSmemBytes) {
+        top -= LS::kSlot;
+        LS::load(top, rx);
+      } else if (rel < LS::kSlot) {
+        retire(SCION_Q_OK);
+        return;
+      } else {
+        top -= LS::kSlot;
+        rx = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
       }
+    } else {
+      const uint32_t depth = rel / LS::kSlot;
+      if (COUNT) tally.stack(depth + 2u);  // reference discipline: pop self, push far, push near
+      if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
+        retire(SCION_Q_STACK_OVERFLOW);
+        return;
+      }
+    }
+    Node nx;
+    const float dx = cpq_node_distmin<L>(T, p, rx, nx, tally);
+    if (go) {
+      Node ny;
+      const float dy = cpq_node_distmin<L>(T, p, ry, ny, tally);
+      const bool left_first = dx < dy;  // ties: the right child is visited first (cpq.scion:17 `L < R`)
+      const Ref far = left_first ? ry : rx;
+      if (rel < LS::kSmemBytes) LS::store(top, far);
+      else deep[rel / LS::kSlot - (uint32_t)LS::kSmem] = far;
+      top += LS::kSlot;
+      if (left_first) { node = nx; d = dx; cur = rx; }
+      else { node = ny; d = dy; cur = ry; }
+      carried = true;
+    } else {
+      node = nx;
+      d = dx;
+      cur = rx;
+      carried = false;
+    }
+    mode = kNode;
+  };
+
+  for (;;) {
+#pragma unroll 1
+    for (int k = 0; k < SCION_INNERC; k++) {
+      if (mode == kNode || mode == kPop) step();
+    }
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    if (idle && (__popc(idle) >= kRefillMin || work.exhausted)) {
+      uint64_t nq;
+      if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
+        p = f32x3{__ldcs(points + 3 * nq), __ldcs(points + 3 * nq + 1), __ldcs(points + 3 * nq + 2)};
+        stash_q[threadIdx.x] = nq;
+        best_pt[threadIdx.x] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(SCION_MISS_PRIM));
+        best_d = scion::inf();
+        tally.reset();
+        top = window + threadIdx.x * 4u;
+        LS::store(top, root);  // the root is "popped" by the first step
+        top += LS::kSlot;
+        mode = kPop;
+      }
+      if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
+    }
+    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    if (pmask && (__popc(pmask) >= SCION_PRIM_MINC || __ballot_sync(kFullMask, mode == kNode || mode == kPop) == 0u)) {
+      const bool own = mode == kPrim;
+      const uint32_t done = coop_points2<L>(T, own, p, prim_i, prim_end, best_d, &best_pt[threadIdx.x], coop[threadIdx.x >> 5]);
+      if (COUNT) tally.prim_tests += done;
+      if (own) mode = kPop;
     }
   }
 }
