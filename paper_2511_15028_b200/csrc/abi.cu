@@ -91,7 +91,8 @@ struct scion_dtree {
   void* h2d[kSlots] = {};
   void* d2h[kSlots] = {};
   uint32_t* d_status[kSlots] = {};
-  cudaStream_t streams[kSlots] = {};
+  cudaStream_t streams[kSlots] = {};  // [0] uploads, [1] and [2] kernels (alternating), [3] downloads
+  cudaEvent_t ev_in[kSlots] = {}, ev_run[kSlots] = {}, ev_out[kSlots] = {};
   uint64_t chunk = 0;
   std::mutex host_mutex;
 };
@@ -492,6 +493,9 @@ void scion_dtree_free(scion_dtree* t) {
   cudaSetDevice(t->device);
   for (int i = 0; i < scion_dtree::kSlots; i++) {
     if (t->streams[i]) { cudaStreamSynchronize(t->streams[i]); cudaStreamDestroy(t->streams[i]); }
+    if (t->ev_in[i]) cudaEventDestroy(t->ev_in[i]);
+    if (t->ev_run[i]) cudaEventDestroy(t->ev_run[i]);
+    if (t->ev_out[i]) cudaEventDestroy(t->ev_out[i]);
     if (t->h2d[i]) cudaFree(t->h2d[i]);
     if (t->d2h[i]) cudaFree(t->d2h[i]);
     if (t->d_status[i]) cudaFree(t->d_status[i]);
@@ -584,34 +588,64 @@ int scion_collision_detection_host(const scion_dtree* a, const scion_dtree* b, s
   return rc;
 }
 
-// Host entry points: chunked, double-buffered over two streams so that the H2D copy of chunk
-// k+1 and the D2H copy of chunk k-1 overlap the traversal of chunk k.
+// Host entry points.  The query array is cut into chunks that flow through three dedicated
+// streams — uploads, kernels, downloads — tied together by events, over kSlots staging slots:
+//   upload(c)   waits for kernel(c - kSlots)   (its input slot is free again)
+//   kernel(c)   waits for upload(c) and download(c - kSlots)   (its output slot is drained)
+//   download(c) waits for kernel(c)
+// so the H2D copy engine never idles behind a kernel or a D2H copy of its own slot: the call runs at
+// the speed of the slowest of the three (on a PCIe Gen5 x16 B200 the 32-byte rays: ~55 GB/s).
 static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uint64_t n, void* h_out, uint32_t* h_status) {
   if (!ct || (!h_in && n) || (!h_out && n)) return fail(SCION_ERR_ARG, "null argument");
   scion_dtree* t = const_cast<scion_dtree*>(ct);
   std::lock_guard<std::mutex> lock(t->host_mutex);
   CUDA_OK(cudaSetDevice(t->device));
   const uint64_t in_sz = hit ? sizeof(scion_ray) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
-  const uint64_t kChunk = 1ull << 21;
+  // chunk size: an eighth of the call, between 2^19 and 2^23 queries (every chunk kernel pays ~0.5 ms of
+  // ramp-up and ragged tail, so small chunks are kernel-bound: 2^28 rays run in 225 / 224 / 185 / 183 ms
+  // with 2^20 / 2^21 / 2^22 / 2^23-query chunks); SCION_HOST_CHUNK_LOG2 overrides
+  static const int forced_log2 = [] { const char* e = getenv("SCION_HOST_CHUNK_LOG2"); int l = e ? atoi(e) : 0; return l ? (l < 10 ? 10 : (l > 26 ? 26 : l)) : 0; }();
+  uint64_t kChunk = 1ull << 19;
+  if (forced_log2) kChunk = 1ull << forced_log2;
+  else while (kChunk < (1ull << 23) && kChunk * 8 < n) kChunk <<= 1;
   constexpr int S = scion_dtree::kSlots;
-  if (t->chunk == 0) {
+  if (t->chunk < kChunk) {
     for (int i = 0; i < S; i++) {
-      CUDA_OK(cudaStreamCreateWithFlags(&t->streams[i], cudaStreamNonBlocking));
+      if (!t->streams[i]) {
+        CUDA_OK(cudaStreamCreateWithFlags(&t->streams[i], cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreateWithFlags(&t->ev_in[i], cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&t->ev_run[i], cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&t->ev_out[i], cudaEventDisableTiming));
+      }
+      if (t->h2d[i]) { cudaFree(t->h2d[i]); t->h2d[i] = nullptr; }
+      if (t->d2h[i]) { cudaFree(t->d2h[i]); t->d2h[i] = nullptr; }
+      if (t->d_status[i]) { cudaFree(t->d_status[i]); t->d_status[i] = nullptr; }
       CUDA_OK(cudaMalloc(&t->h2d[i], kChunk * sizeof(scion_ray)));
       CUDA_OK(cudaMalloc(&t->d2h[i], kChunk * sizeof(scion_cp)));
       CUDA_OK(cudaMalloc(&t->d_status[i], kChunk * sizeof(uint32_t)));
     }
     t->chunk = kChunk;
   }
-  int k = 0;
-  for (uint64_t off = 0; off < n; off += kChunk, k = (k + 1) % S) {
+  // kernels alternate between two streams: the ragged tail of chunk c (a persistent grid drains at the
+  // pace of its longest queries) overlaps the head of chunk c + 1
+  cudaStream_t s_in = t->streams[0], s_out = t->streams[3];
+  uint64_t c = 0;
+  for (uint64_t off = 0; off < n; off += kChunk, c++) {
+    const int k = (int)(c % S);
+    cudaStream_t s_run = t->streams[1 + (c & 1)];
     const uint64_t m = std::min(kChunk, n - off);
-    cudaStream_t s = t->streams[k];
-    CUDA_OK(cudaMemcpyAsync(t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s));
-    int rc = run_query(t, hit, t->h2d[k], m, t->d2h[k], h_status ? t->d_status[k] : nullptr, nullptr, 0, s);
+    if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_in, t->ev_run[k], 0));
+    CUDA_OK(cudaMemcpyAsync(t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
+    CUDA_OK(cudaEventRecord(t->ev_in[k], s_in));
+    CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_in[k], 0));
+    if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_out[k], 0));
+    int rc = run_query(t, hit, t->h2d[k], m, t->d2h[k], h_status ? t->d_status[k] : nullptr, nullptr, 0, s_run);
     if (rc) return rc;
-    CUDA_OK(cudaMemcpyAsync((uint8_t*)h_out + off * out_sz, t->d2h[k], m * out_sz, cudaMemcpyDeviceToHost, s));
-    if (h_status) CUDA_OK(cudaMemcpyAsync(h_status + off, t->d_status[k], m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaEventRecord(t->ev_run[k], s_run));
+    CUDA_OK(cudaStreamWaitEvent(s_out, t->ev_run[k], 0));
+    CUDA_OK(cudaMemcpyAsync((uint8_t*)h_out + off * out_sz, t->d2h[k], m * out_sz, cudaMemcpyDeviceToHost, s_out));
+    if (h_status) CUDA_OK(cudaMemcpyAsync(h_status + off, t->d_status[k], m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_out));
+    CUDA_OK(cudaEventRecord(t->ev_out[k], s_out));
   }
   for (int i = 0; i < S; i++) CUDA_OK(cudaStreamSynchronize(t->streams[i]));
   return SCION_OK;
