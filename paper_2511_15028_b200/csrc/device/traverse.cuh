@@ -524,17 +524,20 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
   __shared__ CoopScratch2 coop[kBlockThreads / 32];
   __shared__ RayStash stash[kBlockThreads];          // ray direction: only the leaf phase needs it
   __shared__ unsigned long long stash_q[kBlockThreads];  // query index: only the retire path needs it
+  __shared__ uint2 stash_leaf[kBlockThreads];        // parked primitive range [begin, end)
   Ref deep[LS::kDeep];
   uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
   asm volatile("" : "+r"(window));  // opaque: kept in a register instead of being re-derived (S2R CgaCtaId + 3) at every push and pop
   uint32_t top = window + threadIdx.x * 4u;
+  uint32_t my_leaf = (uint32_t)__cvta_generic_to_shared(&stash_leaf[threadIdx.x]);
+  asm volatile("" : "+r"(my_leaf));  // one register; re-deriving the address costs 7 instructions in a divergent branch
   WorkFetcher work;
   (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
   RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
   float best_t = 0;
-  uint32_t best_prim = 0, prim_i = 0, prim_end = 0;
+  uint32_t best_prim = 0;
   Ref cur = L::root(T);
 
   auto retire = [&](uint32_t st) {
@@ -572,8 +575,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     float t_near;
     const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
     const bool leaf = node.variant == L::kLeaf;
-    const uint32_t pb = leaf ? (uint32_t)node.data.begin : 0u, pe = leaf ? (uint32_t)node.data.end : 0u;
-    const bool p_prim = hit && leaf && pb < pe;
+    const bool p_prim = hit && leaf && (uint32_t)node.data.begin < (uint32_t)node.data.end;
     const bool p_push = hit && !leaf && t_near < best_t;
     const uint32_t rel = top - window;
     // the common push (depth < kSmem) and pop (1 <= depth <= kSmem) are straight-line predicated
@@ -596,9 +598,8 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
       }
       return;
     }
-    if (p_prim) {
-      prim_i = pb;
-      prim_end = pe;
+    if (p_prim) {  // park the primitive range (shared memory: the leaf phase reads it, the step keeps no register for it)
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(my_leaf), "r"((uint32_t)node.data.begin), "r"((uint32_t)node.data.end));
       mode = kPrim;
     } else if (p_push) {
       LS::store(top, node.right);
@@ -638,7 +639,10 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
     if (pmask && (__popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u)) {
       const bool own = mode == kPrim;
-      const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, prim_end, best_t,
+      uint2 range = make_uint2(0u, 0u);
+      if (own) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(range.x), "=r"(range.y) : "r"(my_leaf));
+      uint32_t prim_i = range.x;
+      const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, range.y, best_t,
                                                best_prim, coop[threadIdx.x >> 5]);
       if (COUNT) tally.prim_tests += done;
       if (own) pop_or_retire();
