@@ -568,8 +568,10 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
   auto step = [&]() {
     typename L::Node node;
     L::template decode<(STAGE > 0)>(T, cur, node, stage);
-#if SCION_PF_NEXT
+#if SCION_PF_NEXT == 1
     if constexpr (std::is_integral<Ref>::value) L::template prefetch<1>(T, (Ref)(cur + 1));
+#elif SCION_PF_NEXT > 1  // L2 prefetch SCION_PF_NEXT records ahead in the (preorder) array
+    if constexpr (std::is_integral<Ref>::value) L::template prefetch<2>(T, (Ref)(cur + SCION_PF_NEXT));
 #endif
     tally.visit();
     float t_near;

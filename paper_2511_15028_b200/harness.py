@@ -5,6 +5,7 @@ compile --emit-c | bench`) that belongs to the traversal path.
   python -m paper_2511_15028_b200.harness footprint --layout L --scene terrain:224
   python -m paper_2511_15028_b200.harness emit-cuda --layout L [-o file]
   python -m paper_2511_15028_b200.harness bench --layout L[,L2..] --alg chrt|cpq --scene terrain:708 --queries 4194304 --rays secondary
+  python -m paper_2511_15028_b200.harness bench --layout L[,L2..] --alg cd --scene terrain:224 [--builder median|sah]   # --queries = output capacity
 
 `bench` follows the paper's protocol: 1 warm-up + 9 runs, drop the 2 lowest
 and 2 highest, report the mean of the remaining 5, one CSV row per (layout, algorithm, scene, nGPU).
@@ -67,11 +68,55 @@ def cmd_emit(a):
     return 0
 
 
+def cmd_bench_cd(a):
+    """Collision detection (cd.scion): the scene against a lifted copy of a second scene of the same kind
+    (SPEC.md:599 'second scene + rigid transform'), median split with one primitive per leaf as in the
+    paper's CD experiment (§8.3.3) unless --builder sah."""
+    import torch
+    sa = parse_scene(a.scene)
+    kind, _, arg = a.scene.partition(":")
+    other = {"terrain": sb.Scene.terrain, "sphere": sb.Scene.sphere}.get(kind)
+    if other is None:
+        print("cd needs a triangle scene (terrain:N or sphere:N)", file=sys.stderr)
+        return 2
+    tb = other(int(arg or 64), sb.seed_from_env(1) + 8).triangles().copy()
+    tb[:, 1::3] += np.float32(0.02)
+    sb_scene = sb.Scene.from_triangles(tb)
+    build = (lambda s: s.build_median(1)) if a.builder == "median" else (lambda s: s.build_sah(32, a.max_leaf))
+    la, lb = build(sa), build(sb_scene)
+    cap = a.queries
+    d_out = torch.empty(cap * 8, dtype=torch.uint8, device="cuda:0")
+    print("layout,algorithm,scene,n_gpus,primitives,builder,mean_ms,pairs,mpairs_tested_per_s,node_pairs,tri_tests,levels,max_frontier,bytes_per_launch,achieved_gbs")
+    for layout in a.layout.split(","):
+        da, db = la.encode(layout).upload(0), lb.encode(layout).upload(0)
+        times, n, st = [], 0, {}
+        for i in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            n, st = da.collide(db, d_out.data_ptr(), cap)
+            e1.record()
+            torch.cuda.synchronize()
+            if i:
+                times.append(e0.elapsed_time(e1))
+        ms = float(np.mean(sorted(times)[2:-2]))
+        plan = sb.layout_plan(layout)
+        stride = sum(s["stride_bytes"] for b in plan["buffers"] if b["name"] == plan["node_group"] for s in b["segments"])
+        nbytes = st["node_pairs"] * (2 * stride + 2 * 4) + st["tri_tests"] * 72 + n * 8  # both records + the pair entry; both triangles; output
+        print(f"{layout},cd,{a.scene},1,{la.nprims}+{lb.nprims},{a.builder},{ms:.4f},{n},{(st['node_pairs'] + st['tri_tests']) / ms / 1e3:.2f},{st['node_pairs']},{st['tri_tests']},{st['levels']},{st['max_frontier']},{nbytes},{nbytes / ms / 1e6:.1f}")
+        if n > cap:
+            print(f"{layout}: output capacity {cap} < {n} colliding pairs (count is exact, list truncated)", file=sys.stderr)
+        da.free()
+        db.free()
+    return 0
+
+
 def cmd_bench(a):
     import torch
     if not torch.cuda.is_available():
         print("bench needs a CUDA device (no CPU fallback)", file=sys.stderr)
         return 1
+    if a.alg == "cd":
+        return cmd_bench_cd(a)
     scene = parse_scene(a.scene)
     lt = scene.build_sah(32, a.max_leaf).collapse8()
     lo, hi = scene.bounds()
@@ -140,7 +185,8 @@ def main(argv=None):
     p.add_argument("-o", "--output")
     p = sub.add_parser("bench")
     p.add_argument("--layout", required=True)
-    p.add_argument("--alg", default="chrt", choices=["chrt", "cpq"])
+    p.add_argument("--alg", default="chrt", choices=["chrt", "cpq", "cd"])
+    p.add_argument("--builder", default="median", choices=["median", "sah"], help="cd only: median split, 1 primitive per leaf (paper) or binned SAH")
     p.add_argument("--scene", default="terrain:224")
     p.add_argument("--queries", type=int, default=1 << 20)
     p.add_argument("--rays", default="primary", choices=["primary", "secondary"])
