@@ -94,6 +94,7 @@ struct scion_dtree {
   cudaStream_t streams[kSlots] = {};  // [0] uploads, [1] and [2] kernels (alternating), [3] downloads
   cudaEvent_t ev_in[kSlots] = {}, ev_run[kSlots] = {}, ev_out[kSlots] = {};
   uint64_t chunk = 0;
+  scion::CdScratch cd_scratch;  // collision detection frontiers (guarded by host_mutex)
   std::mutex host_mutex;
 };
 
@@ -501,6 +502,7 @@ void scion_dtree_free(scion_dtree* t) {
     if (t->d_status[i]) cudaFree(t->d_status[i]);
   }
   if (t->counters) cudaFree(t->counters);
+  if (t->cd_scratch.ptr) cudaFree(t->cd_scratch.ptr);
   if (t->image && t->owns_image) cudaFree(t->image);
   delete t;
 }
@@ -565,7 +567,9 @@ int scion_collision_detection(const scion_dtree* a, const scion_dtree* b, scion_
   if (a->device != b->device) return fail(SCION_ERR_ARG, "collision_detection needs both trees on the same device");
   if (!a->kernels->collide) return fail(SCION_ERR_ARG, "cd requires a binary layout (corpus.cpp:86)");
   CUDA_OK(cudaSetDevice(a->device));
-  scion::CdArgs args{a->view, b->view, d_out, capacity, frontier_capacity, out_count, stats, (cudaStream_t)stream};
+  scion_dtree* owner = const_cast<scion_dtree*>(a);
+  std::lock_guard<std::mutex> lock(owner->host_mutex);
+  scion::CdArgs args{a->view, b->view, d_out, capacity, frontier_capacity, out_count, stats, (cudaStream_t)stream, &owner->cd_scratch};
   int overflow = 0;
   CUDA_OK(a->kernels->collide(args, &overflow));
   g_launches.fetch_add(1);

@@ -23,6 +23,10 @@ struct LaunchArgs {
 
 typedef cudaError_t (*launch_fn)(const LaunchArgs&);
 
+struct CdScratch {  // device scratch of collision detection, cached by the owning tree between calls
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
 struct CdArgs {  // collision detection: two trees of the same layout on the same device
   TreeView a, b;
   scion_pair* out;
@@ -31,6 +35,7 @@ struct CdArgs {  // collision detection: two trees of the same layout on the sam
   uint64_t* out_count;      // host
   scion_cd_stats* stats;    // host, nullable
   cudaStream_t stream;
+  CdScratch* scratch;
 };
 typedef cudaError_t (*cd_fn)(const CdArgs&, int* overflow_bits);
 typedef cudaError_t (*occupancy_fn)(int* blocks_per_sm, int* regs, size_t* smem);
