@@ -236,6 +236,13 @@ int scion_dtree_upload_into(const scion_ptree* p, int device, void* d_image, uin
 /* Packed wire image used for replication: [header | globals | buffers...] in ONE
  * contiguous device allocation so that a single ncclBroadcast replicates the tree. */
 int scion_dtree_image(const scion_dtree* t, void** d_ptr, uint64_t* bytes);
+/* Copy the whole device image (header + buffers, scion_dtree_image bytes) to host memory. */
+int scion_dtree_download_image(const scion_dtree* t, void* h_dst, uint64_t bytes);
+/* Device-side build_physical (SPEC.md:276-284 constructor specialisation): the
+ * LogicalTree arrays are uploaded once and every node record is encoded by one CUDA thread; the
+ * resulting image is byte-identical to scion_encode + scion_dtree_upload.  Same builder faults
+ * (SCION_ERR_BUILD) as scion_encode; SCION_ERR_NO_DEVICE without a GPU. */
+int scion_encode_device(const scion_ltree* t, const char* layout, int device, scion_dtree** out);
 /* rebuild a device tree around a received image (no copy; image owned by caller unless adopt=1) */
 int scion_dtree_from_image(const char* layout, void* d_image, uint64_t bytes, int device, int adopt,
                            scion_dtree** out);

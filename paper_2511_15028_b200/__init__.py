@@ -128,6 +128,8 @@ def lib() -> C.CDLL:
         "scion_ptree_image_bytes": (u64, [vp]),
         "scion_dtree_upload_into": (i32, [vp, i32, vp, u64, P(vp)]),
         "scion_dtree_image": (i32, [vp, P(vp), P(u64)]),
+        "scion_dtree_download_image": (i32, [vp, vp, u64]),
+        "scion_encode_device": (i32, [vp, cp, i32, P(vp)]),
         "scion_dtree_from_image": (i32, [cp, vp, u64, i32, i32, P(vp)]),
         "scion_dtree_free": (None, [vp]),
         "scion_closest_hit": (i32, [vp, vp, u64, vp, vp, vp, i32, vp]),
@@ -344,6 +346,12 @@ class LogicalTree:
         _check(lib().scion_encode(self._h, layout.encode(), C.byref(h)))
         return PhysicalTree(h)
 
+    def encode_device(self, layout: str, device: int = 0) -> "DeviceTree":
+        """build_physical on the GPU: byte-identical to encode(layout).upload(device)."""
+        h = C.c_void_p()
+        _check(lib().scion_encode_device(self._h, layout.encode(), device, C.byref(h)))
+        return DeviceTree(h, device)
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.scion_ltree_free(self._h)
@@ -448,6 +456,13 @@ class DeviceTree:
         p, n = C.c_void_p(), C.c_uint64()
         _check(lib().scion_dtree_image(self._h, C.byref(p), C.byref(n)))
         return p.value, n.value
+
+    def download_image(self) -> np.ndarray:
+        """The whole device image (1 KB header + every plan buffer) as host bytes."""
+        _, n = self.image()
+        out = np.empty(n, np.uint8)
+        _check(lib().scion_dtree_download_image(self._h, out.ctypes.data, n))
+        return out
 
     @staticmethod
     def from_image(d_ptr: int, nbytes: int, device: int, layout: Optional[str] = None, adopt: bool = False) -> "DeviceTree":

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "device/launch.cuh"
+#include "host/encode_node.hpp"
 #include "host/physical.hpp"
 #include "host/rng.hpp"
 #include "host/scene.hpp"
@@ -123,11 +124,12 @@ int header_from_ptree(const scion_ptree& p, ImageHeader& h) {
   uint64_t off = kHeaderBytes;
   for (size_t b = 0; b < p.buffers.size(); b++) {
     if (p.seg_bases[b].size() > SCION_MAX_SEGMENTS) return fail(SCION_ERR_LAYOUT, "too many segments");
+    const uint64_t sz = p.sizes.size() == p.buffers.size() ? p.sizes[b] : p.buffers[b].size();
     h.offset[b] = off;
-    h.bytes[b] = p.buffers[b].size();
+    h.bytes[b] = sz;
     h.count[b] = p.counts[b];
     for (size_t s = 0; s < p.seg_bases[b].size(); s++) h.seg_base[b][s] = p.seg_bases[b][s];
-    off += (p.buffers[b].size() + 16 + 255) / 256 * 256;
+    off += (sz + 16 + 255) / 256 * 256;
   }
   for (size_t g = 0; g < p.globals.size(); g++) memcpy(h.glob[g], p.globals[g].data(), 16);
   h.root0 = p.root0;
@@ -170,6 +172,11 @@ struct FileR {
 }  // namespace
 
 namespace scion {
+// device-side encode: one thread per node (host/encode_node.hpp)
+__global__ void encode_nodes_kernel(const enc::EncodeJob job) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < job.count) enc::encode_one(job, i);
+}
 int device_sm_count() {
   static int sms[64] = {0};
   int dev = 0;
@@ -396,6 +403,8 @@ int scion_ptree_load(const char* path, scion_ptree** out) {
     }
     for (uint32_t b = 0; b < nb; b++) {
       p->buffers[b].resize(sizes[b]);
+      p->sizes.resize(nb);
+      p->sizes[b] = sizes[b];
       r.raw(p->buffers[b].data(), sizes[b]);
       char pad[16];
       r.raw(pad, (16 - sizes[b] % 16) % 16);
@@ -463,6 +472,82 @@ uint64_t scion_ptree_image_bytes(const scion_ptree* p) {
   return h.total_bytes;
 }
 int scion_dtree_alloc_like(const scion_ptree* p, int device, scion_dtree** out) { return dtree_create(p, device, false, out); }
+
+// Device-side encode: the per-node encoders of host/encode_node.hpp run as one
+// CUDA thread per node on the uploaded LogicalTree arrays and write the records straight into the
+// device image; sizes, globals and the root reference come from the same prepare() as the host path,
+// so the image is byte-identical to scion_encode + scion_dtree_upload (tests/test_device_encode.py).
+int scion_encode_device(const scion_ltree* t, const char* layout, int device, scion_dtree** out) {
+  if (!t || !layout || !out) return fail(SCION_ERR_ARG, "null argument");
+  const scion::LayoutEntry* e = nullptr;
+  scion_ptree shell;
+  scion::enc::EncodeJob job;
+  std::vector<uint32_t> post;
+  SCION_TRY(e = scion::find_layout(layout); if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + layout + "'");
+            if (e->plan->family == scion::lc::Family::Bvh8 && !t->has_wide) return fail(SCION_ERR_BUILD, "8-wide layouts need scion_ltree_collapse8 first");
+            scion::encode_shell(*t, *e, shell, job, post);)
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) { cudaGetLastError(); return fail(SCION_ERR_NO_DEVICE, "no CUDA device: this backend has no CPU fallback"); }
+  if (device < 0 || device >= ndev) return fail(SCION_ERR_ARG, "device index out of range");
+  CUDA_OK(cudaSetDevice(device));
+  auto* d = new scion_dtree();
+  d->device = device;
+  d->layout = e;
+  int rc = header_from_ptree(shell, d->header);
+  if (rc) { delete d; return rc; }
+  std::vector<void*> temps;
+  auto bail = [&](int code) { for (void* p : temps) cudaFree(p); scion_dtree_free(d); return code; };
+  auto up = [&](const void* src, size_t bytes, const void** dst) -> cudaError_t {
+    void* p = nullptr;
+    cudaError_t ce = cudaMalloc(&p, bytes ? bytes : 16);
+    if (ce != cudaSuccess) return ce;
+    temps.push_back(p);
+    *dst = p;
+    return bytes ? cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+  };
+#define ENC_OK(x) do { cudaError_t ce__ = (x); if (ce__ != cudaSuccess) return bail(fail(SCION_ERR_CUDA, cudaGetErrorString(ce__))); } while (0)
+  ENC_OK(cudaMalloc(&d->image, d->header.total_bytes));
+  ENC_OK(cudaMemset(d->image, 0, d->header.total_bytes));
+  ENC_OK(cudaMemcpy(d->image, &d->header, sizeof(ImageHeader), cudaMemcpyHostToDevice));
+  const scion::lc::Buffer* prim = e->plan->buffer_named("primitives");
+  if (!prim) return bail(fail(SCION_ERR_LAYOUT, "layout has no primitives array"));
+  if (!t->tris.empty()) ENC_OK(cudaMemcpy(d->image + d->header.offset[prim->id], t->tris.data(), t->tris.size() * 4, cudaMemcpyHostToDevice));
+  const void* p = nullptr;
+  if (job.kind == scion::enc::kBvh8) {
+    ENC_OK(up(t->wnodes.data(), t->wnodes.size() * sizeof(scion_wnode), &p)); job.wnodes = (const scion_wnode*)p;
+    ENC_OK(up(t->wleaves.data(), t->wleaves.size() * sizeof(scion_wleaf), &p)); job.wleaves = (const scion_wleaf*)p;
+    job.nodes = nullptr;
+  } else {
+    ENC_OK(up(t->nodes.data(), t->nodes.size() * sizeof(scion_lnode), &p)); job.nodes = (const scion_lnode*)p;
+    if (job.kind == scion::enc::kDop14) {
+      ENC_OK(up(t->dop_lo2.data(), t->dop_lo2.size() * 4, &p)); job.dop_lo2 = (const float*)p;
+      ENC_OK(up(t->dop_hi2.data(), t->dop_hi2.size() * 4, &p)); job.dop_hi2 = (const float*)p;
+    }
+    if (job.kind == scion::enc::kPbrtPost) { ENC_OK(up(post.data(), post.size() * 4, &p)); job.post = (const uint32_t*)p; }
+  }
+  for (auto& f : job.f)
+    if (f.buffer >= 0) f.base = d->image + d->header.offset[f.buffer];
+  if (job.count) {
+    scion::encode_nodes_kernel<<<(unsigned)((job.count + 127) / 128), 128>>>(job);
+    ENC_OK(cudaGetLastError());
+    g_launches.fetch_add(1);
+  }
+  ENC_OK(cudaDeviceSynchronize());
+#undef ENC_OK
+  for (void* q : temps) cudaFree(q);
+  temps.clear();
+  rc = finish_dtree(d);
+  if (rc) { scion_dtree_free(d); return rc; }
+  *out = d;
+  return SCION_OK;
+}
+int scion_dtree_download_image(const scion_dtree* t, void* h_dst, uint64_t bytes) {
+  if (!t || !h_dst) return fail(SCION_ERR_ARG, "null argument");
+  if (bytes < t->header.total_bytes) return fail(SCION_ERR_ARG, "destination smaller than the image");
+  CUDA_OK(cudaSetDevice(t->device));
+  CUDA_OK(cudaMemcpy(h_dst, t->image, t->header.total_bytes, cudaMemcpyDeviceToHost));
+  return SCION_OK;
+}
 
 int scion_dtree_image(const scion_dtree* t, void** d_ptr, uint64_t* bytes) {
   if (!t) return fail(SCION_ERR_ARG, "null tree");

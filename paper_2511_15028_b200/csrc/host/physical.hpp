@@ -14,6 +14,7 @@ struct scion_ptree {
   std::string layout;                    // registry name
   const scion::lc::Plan* plan = nullptr; // owned by the registry (process lifetime)
   std::vector<std::vector<uint8_t>> buffers;      // indexed by plan buffer id
+  std::vector<uint64_t> sizes;                    // byte size per buffer (== buffers[b].size() unless this is a shell, see encode_shell)
   std::vector<uint64_t> counts;                   // element count per buffer (arena: bytes)
   std::vector<std::vector<uint64_t>> seg_bases;   // byte offsets per buffer
   std::vector<std::array<uint8_t, 16>> globals;   // raw little-endian cells, plan.globals order
@@ -38,5 +39,8 @@ const LayoutEntry* find_layout(const std::string& name);
 
 // build_physical: throws std::runtime_error (builder hard fault) on capacity violations
 void encode_tree(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& out);
+// device-side encode: sizes, globals, root reference and the per-node job, but no buffer contents
+namespace enc { struct EncodeJob; }
+void encode_shell(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& out, enc::EncodeJob& job, std::vector<uint32_t>& post);
 
 }  // namespace scion
