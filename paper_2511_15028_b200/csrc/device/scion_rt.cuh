@@ -24,6 +24,10 @@
 #define SCION_HOSTDEV inline
 #endif
 
+#ifndef SCION_LDG256
+#define SCION_LDG256 1
+#endif
+
 namespace scion {
 
 // --------------------------------------------------------------------------- device tree view
@@ -308,6 +312,17 @@ SCION_HOSTDEV void ld128(const uint8_t* p, uint32_t* o) {
   memcpy(o, p, 16);
 #endif
 }
+// 256-bit read-only load (sm_100: LDG.E.256): one L1 wavefront per lane where two LDG.128 take two —
+// the f32 layouts are L1-tag-bound (profiles/r1_ncu_v8_c5_pbrt.txt: l1tex throughput 98 %)
+SCION_HOSTDEV void ld256(const uint8_t* p, uint32_t* o) {
+#if defined(__CUDA_ARCH__)
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7])
+               : "l"(p));
+#else
+  memcpy(o, p, 32);
+#endif
+}
 SCION_HOSTDEV uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t shift_bits) {
 #if defined(__CUDA_ARCH__)
   return __funnelshift_r(lo, hi, shift_bits);
@@ -335,7 +350,10 @@ SCION_HOSTDEV void prefetch_to(const void* p) {
 template <int BYTES, int ALIGN>
 SCION_HOSTDEV void load_record(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
   constexpr int NW = (BYTES + 3) / 4;
-  if constexpr (ALIGN % 16 == 0 && BYTES % 16 == 0) {
+  if constexpr (SCION_LDG256 && ALIGN % 32 == 0 && BYTES % 32 == 0) {
+#pragma unroll
+    for (int i = 0; i < NW; i += 8) ld256(p + 4 * i, r.w + i);
+  } else if constexpr (ALIGN % 16 == 0 && BYTES % 16 == 0) {
 #pragma unroll
     for (int i = 0; i < NW; i += 4) ld128(p + 4 * i, r.w + i);
   } else if constexpr (ALIGN % 8 == 0 && BYTES % 8 == 0) {
