@@ -345,6 +345,9 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
 #ifndef SCION_PF_NEXT
 #define SCION_PF_NEXT 0
 #endif
+#ifndef SCION_PF_MIN
+#define SCION_PF_MIN 0
+#endif
 #ifndef SCION_INNER
 #define SCION_INNER 4
 #endif
@@ -605,7 +608,15 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
       mode = kPrim;
     } else if (p_push) {
       LS::store(top, node.right);
-      if (kPrefetch) L::prefetch(T, node.right);
+      if constexpr (kPrefetch) {
+        // L2-prefetch the pushed child, but only when it is far: a right sibling a few records away shares
+        // its lines with what this lane just fetched, and every prefetch costs an L1 tag lookup per lane
+        if constexpr (std::is_integral<Ref>::value && SCION_PF_MIN > 0) {
+          if ((uint64_t)(node.right - cur) > (uint64_t)SCION_PF_MIN) L::prefetch(T, node.right);
+        } else {
+          L::prefetch(T, node.right);
+        }
+      }
       top += LS::kSlot;
       cur = node.left;
     } else {
