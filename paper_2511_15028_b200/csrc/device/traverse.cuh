@@ -9,17 +9,20 @@
 // right child), because hit ids are only bit-exact when pruning sees the same `best` at the same
 // moment.
 //
-// Execution model (justified by profiles/r1_ncu_v1_c5_q16_*: the first, one-warp-32-rays kernel
-// ran at 6.2 of 32 active threads per instruction, its triangle loop at 1 of 32):
-//   * persistent warps; every LANE is refilled with a new query as soon as its previous one
-//     retires (ballot + prefix popcount over a warp-private chunk of the global work counter);
-//   * the per-lane loop body is a small state machine — FETCH, NODE, PRIM — so that lanes in the
-//     same state execute the same instructions in the same iteration: all NODE lanes decode and
-//     test one node, then all PRIM lanes test one primitive;
-//   * the PRIM phase only runs when enough lanes wait in it (or nothing else can progress), which
-//     batches the expensive, rare Moeller-Trumbore evaluations.
-// Stack: first entries in shared memory laid out [entry][thread] (lane l always hits bank l, so
-// any mix of per-lane depths is conflict free), deeper entries in local memory.
+// Execution model (justified by profiles/r1_ncu_v1_c5_q16.txt: the first, one-warp-32-rays kernel
+// ran at 6.2 of 32 active threads per instruction, its triangle loop at 1 of 32; evolution v1..v9 in
+// DESIGN.md §5):
+//   * persistent warps; every LANE is refilled with a new query once enough lanes have retired
+//     (ballot + prefix popcount over a warp-private chunk of the global work counter);
+//   * per-lane state machine — FETCH, NODE, PRIM — so that lanes in the same state execute the same
+//     instructions: a NODE step decodes and tests one node and pushes / pops on one predicated
+//     straight-line path; leaf ranges are parked and resolved by all 32 lanes together once enough
+//     lanes wait (cooperative PRIM phase), which batches the rare Moeller-Trumbore evaluations;
+//   * state that only the PRIM / retire paths need (ray direction, query index, leaf range) lives in
+//     shared memory, so the NODE step runs in 56 registers (9 CTAs/SM).
+// Stack: LaneStack below — first entries in shared memory laid out [entry][word][thread] (lane l
+// always hits bank l, so any mix of per-lane depths is conflict free) and addressed by one register,
+// deeper entries in local memory.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -54,67 +57,7 @@ constexpr int kChunk = SCION_CHUNK;     // queries a warp takes from the global 
 constexpr int kRefillMin = SCION_REFILL_MIN;   // refill when at least this many lanes are idle (or all of them)
 constexpr int kPrimMin = SCION_PRIM_MIN;       // run the PRIM phase when at least this many lanes wait in it
 
-// Hybrid traversal stack (see header comment).  kSmem is sized so that one CTA uses 16 KB of
-// shared memory whatever the entry size.
-constexpr int kStackSmemBytesPerBlock = SCION_STACK_SMEM;
-template <class Entry>
-struct HybridStack {
-  static_assert(sizeof(Entry) % 4 == 0, "stack entries are stored as 32-bit words");
-  static constexpr int kWords = (int)sizeof(Entry) / 4;
-  static constexpr int kSmem = (kStackSmemBytesPerBlock / kBlockThreads / (int)sizeof(Entry)) < SCION_STACK_DEPTH
-                                   ? (kStackSmemBytesPerBlock / kBlockThreads / (int)sizeof(Entry))
-                                   : SCION_STACK_DEPTH;
-  static constexpr int kDeep = SCION_STACK_DEPTH - kSmem > 0 ? SCION_STACK_DEPTH - kSmem : 1;
-  static constexpr uint32_t kEntryStride = kBlockThreads * (uint32_t)sizeof(Entry);  // bytes between entry e and e+1 of one thread
-  // `sp` is deliberately NOT a member: the struct holds a dynamically indexed array and therefore
-  // lives in local memory; a member counter would be re-loaded / re-stored around every access
-  // (seen as STL/LDL pairs in profiles/r1_ncu_v2_c5_q16.txt).  The shared-memory part is addressed
-  // through a precomputed 32-bit shared-space address + st.shared/ld.shared: the generic-pointer
-  // form re-derived the window base (S2R/LEA chain, 18 SASS instructions per push) every time.
-  Entry deep[kDeep];
-  uint32_t base;  // shared-space byte address of this thread's entry 0
-  SCION_DEV void init(void* smem_generic) {
-    base = (uint32_t)__cvta_generic_to_shared(smem_generic) + threadIdx.x * (uint32_t)sizeof(Entry);
-  }
-  SCION_DEV void push(int& sp, const Entry& r) {
-    if (sp < kSmem) {
-      uint32_t w[kWords];
-      memcpy(w, &r, sizeof(Entry));
-      const uint32_t a = base + (uint32_t)sp * kEntryStride;
-#pragma unroll
-      for (int i = 0; i < kWords; i++) asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + 4u * i), "r"(w[i]) : "memory");
-    } else {
-      deep[sp - kSmem] = r;
-    }
-    sp++;
-  }
-  // store entry r at absolute position `pos` iff `on` — no branch on the common (shared-memory) path, so
-  // eight conditional pushes of an 8-wide node issue as straight-line predicated code
-  SCION_DEV void store_if(bool on, int pos, const Entry& r) {
-    uint32_t w[kWords];
-    memcpy(w, &r, sizeof(Entry));
-    const uint32_t a = base + (uint32_t)pos * kEntryStride;
-    const uint32_t p = (on && pos < kSmem) ? 1u : 0u;
-#pragma unroll
-    for (int i = 0; i < kWords; i++)
-      asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.b32 [%0], %1; }" ::"r"(a + 4u * i), "r"(w[i]), "r"(p) : "memory");
-    if (on && pos >= kSmem) deep[pos - kSmem] = r;
-  }
-  SCION_DEV Entry pop(int& sp) {
-    sp--;
-    Entry r;
-    if (sp < kSmem) {
-      uint32_t w[kWords];
-      const uint32_t a = base + (uint32_t)sp * kEntryStride;
-#pragma unroll
-      for (int i = 0; i < kWords; i++) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(a + 4u * i) : "memory");
-      memcpy(&r, w, sizeof(Entry));
-    } else {
-      r = deep[sp - kSmem];
-    }
-    return r;
-  }
-};
+constexpr int kStackSmemBytesPerBlock = SCION_STACK_SMEM;  // shared-memory share of the per-lane stacks of one CTA (LaneStack below)
 
 template <bool COUNT>
 struct Tally {
@@ -168,150 +111,6 @@ SCION_DEV RayCtx load_ray(const scion_ray* rays, uint64_t q) {
   return make_ray(a.x, a.y, a.z, a.w, b.x, b.y, b.z);
 }
 
-// one primitive: `if intersects(ray, t) && distmin(ray, t) < best[0] { best = (distmin(ray, t), t) }`
-template <class L>
-SCION_DEV void test_triangle(const TreeView& T, const RayCtx& ray, uint32_t i, float& best_t, uint32_t& best_prim) {
-  static_assert(L::kStride_primitives == 36, "Triangle stride");
-  float tri[9];
-  load_triangle36(T.buf[L::kBuf_primitives], i, tri);
-  float t;
-  if (ray_tri_mt(ray, tri, t) && t < best_t) {
-    best_t = t;
-    best_prim = i;
-  }
-}
-
-// Warp-cooperative leaf processing.  Every lane with has=true owns a pending primitive range
-// [prim_i, prim_end) of its own ray; the (owner, primitive) pairs of ALL owners are spread over
-// the 32 lanes so that each lane runs one Moeller-Trumbore test per round for some owner's ray
-// (ray fetched by shuffle).  Owners then fold their results in ascending primitive order with the
-// reference's strict `t < best` rule, which is exactly the sequential foreach of chrt.scion:10-15
-// (each test is a pure function of (ray, triangle); only the fold depends on order).
-struct CoopScratch {
-  uint8_t owner[32];
-  uint8_t k[32];
-  float t[32];
-};
-template <class L>
-SCION_DEV uint32_t coop_triangles(const TreeView& T, bool has, const RayCtx& ray, uint32_t& prim_i, uint32_t prim_end, float& best_t,
-                                  uint32_t& best_prim, CoopScratch& sc) {
-  static_assert(L::kStride_primitives == 36, "Triangle stride");
-  const unsigned lane = threadIdx.x & 31u;
-  uint32_t tested = 0;
-  for (;;) {
-    const uint32_t remaining = has ? prim_end - prim_i : 0u;
-    if (__ballot_sync(kFullMask, remaining != 0u) == 0u) break;
-    const uint32_t c = remaining < 32u ? remaining : 32u;
-    uint32_t incl = c;  // inclusive prefix sum over lanes
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(kFullMask, incl, d);
-      if (lane >= (unsigned)d) incl += v;
-    }
-    const uint32_t excl = incl - c;
-    const uint32_t total = __shfl_sync(kFullMask, incl, 31);
-    const uint32_t take = excl >= 32u ? 0u : (c < 32u - excl ? c : 32u - excl);
-    for (uint32_t k = 0; k < take; k++) {
-      sc.owner[excl + k] = (uint8_t)lane;
-      sc.k[excl + k] = (uint8_t)k;
-    }
-    __syncwarp();
-    const bool work = lane < (total < 32u ? total : 32u);
-    const unsigned o = work ? sc.owner[lane] : 0u;
-    const uint32_t kk = work ? sc.k[lane] : 0u;
-    RayCtx r;
-    r.ox = __shfl_sync(kFullMask, ray.ox, o);
-    r.oy = __shfl_sync(kFullMask, ray.oy, o);
-    r.oz = __shfl_sync(kFullMask, ray.oz, o);
-    r.tmax = __shfl_sync(kFullMask, ray.tmax, o);
-    r.dx = __shfl_sync(kFullMask, ray.dx, o);
-    r.dy = __shfl_sync(kFullMask, ray.dy, o);
-    r.dz = __shfl_sync(kFullMask, ray.dz, o);
-    const uint32_t pi = __shfl_sync(kFullMask, prim_i, o) + kk;
-    float t = scion::inf();
-    if (work) {
-      float tri[9];
-      load_triangle36(T.buf[L::kBuf_primitives], pi, tri);
-      float th;
-      if (ray_tri_mt(r, tri, th)) t = th;
-      sc.t[lane] = t;
-    }
-    __syncwarp();
-    for (uint32_t k = 0; k < take; k++) {
-      const float th = sc.t[excl + k];
-      if (th < best_t) {  // a miss is +inf and never passes
-        best_t = th;
-        best_prim = prim_i + k;
-      }
-    }
-    prim_i += take;
-    tested += take;
-    __syncwarp();
-  }
-  return tested;
-}
-
-// Cooperative leaf phase of closest_point (cpq.scion:25-31): same scheme as coop_triangles, the
-// worker returns (d2, closest point); owners fold with the strict `d2 < best[0]` rule in order.
-struct CoopScratchCp {
-  uint8_t owner[32];
-  uint8_t k[32];
-  float d2[32];
-  float c[32][3];
-};
-template <class L>
-SCION_DEV uint32_t coop_points(const TreeView& T, bool has, const f32x3& p, uint32_t& prim_i, uint32_t prim_end, float& best_d, f32x3& best_p,
-                               uint32_t& best_prim, CoopScratchCp& sc) {
-  static_assert(L::kStride_primitives == 36, "Triangle stride");
-  const unsigned lane = threadIdx.x & 31u;
-  uint32_t tested = 0;
-  for (;;) {
-    const uint32_t remaining = has ? prim_end - prim_i : 0u;
-    if (__ballot_sync(kFullMask, remaining != 0u) == 0u) break;
-    const uint32_t c = remaining < 32u ? remaining : 32u;
-    uint32_t incl = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(kFullMask, incl, d);
-      if (lane >= (unsigned)d) incl += v;
-    }
-    const uint32_t excl = incl - c;
-    const uint32_t total = __shfl_sync(kFullMask, incl, 31);
-    const uint32_t take = excl >= 32u ? 0u : (c < 32u - excl ? c : 32u - excl);
-    for (uint32_t k = 0; k < take; k++) {
-      sc.owner[excl + k] = (uint8_t)lane;
-      sc.k[excl + k] = (uint8_t)k;
-    }
-    __syncwarp();
-    const bool work = lane < (total < 32u ? total : 32u);
-    const unsigned o = work ? sc.owner[lane] : 0u;
-    const uint32_t kk = work ? sc.k[lane] : 0u;
-    const f32x3 q{__shfl_sync(kFullMask, p.x, o), __shfl_sync(kFullMask, p.y, o), __shfl_sync(kFullMask, p.z, o)};
-    const uint32_t pi = __shfl_sync(kFullMask, prim_i, o) + kk;
-    if (work) {
-      float tri[9];
-      load_triangle36(T.buf[L::kBuf_primitives], pi, tri);
-      const f32x3 cp = closest_point_triangle(q, tri);
-      const f32x3 x = q - cp;
-      sc.d2[lane] = dot(x, x);
-      sc.c[lane][0] = cp.x; sc.c[lane][1] = cp.y; sc.c[lane][2] = cp.z;
-    }
-    __syncwarp();
-    for (uint32_t k = 0; k < take; k++) {
-      const float d2 = sc.d2[excl + k];
-      if (d2 < best_d) {
-        best_d = d2;
-        best_p = f32x3{sc.c[excl + k][0], sc.c[excl + k][1], sc.c[excl + k][2]};
-        best_prim = prim_i + k;
-      }
-    }
-    prim_i += take;
-    tested += take;
-    __syncwarp();
-  }
-  return tested;
-}
-
 // bounds test of one binary / DOP node against the ray.  Loads the cold segment only when the
 // reference semantics would evaluate it (dop.scion:20-21 `if I {...}`).
 template <class L, class TallyT>
@@ -352,10 +151,7 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
 #define SCION_INNER 4
 #endif
 constexpr bool kPrefetch = SCION_PREFETCH != 0;  // L2-prefetch a node record when its reference is pushed (+3-4 % on C5, binary)
-constexpr bool kPrefetchWide = false;             // 8-wide: up to 8 prefetches per node, most culled later: -4 % on C5
 constexpr int kInner = SCION_INNER;  // node steps between two looks at the warp (idle lanes to refill, lanes waiting with a leaf)
-constexpr uint32_t kFetchEvery = 2;  // (8-wide / CPQ kernels) look for idle lanes every kFetchEvery-th iteration
-constexpr uint32_t kPrimEvery = 4;   // (8-wide / CPQ kernels) look for waiting PRIM lanes every kPrimEvery-th iteration
 
 // keeps the result-store address arithmetic inside the (rare) retire branch instead of letting the
 // compiler hoist it into every loop iteration (9 SASS instructions per iteration in v3)
