@@ -750,6 +750,9 @@ SCION_DEV uint32_t coop_points2(const TreeView& T, bool own, const f32x3& p, uin
 // has two decode slots: X = left child (descending lane) or the popped node (popping lane), and
 // Y = right child (descending lanes only).  The instrumented build still counts every decode the
 // reference performs (identical counters), it just does not repeat the work.
+// Rejected: ONE decode per step (modes pop / peek-left / peek-right, every decode at ~25/32 lanes instead
+// of the Y slot at ~12/32): 886 instead of 1247 Mq/s — the two child loads of a step overlap in the
+// memory system, and the kernel is bound by that latency, not by issue slots.
 template <class L, bool COUNT>
 __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const TreeView T, const float* __restrict__ points, uint64_t n,
                                                              scion_cp* __restrict__ out, uint32_t* __restrict__ status,
