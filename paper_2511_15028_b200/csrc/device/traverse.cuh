@@ -168,12 +168,12 @@ SCION_DEV uint64_t opaque(uint64_t q) {
 // nor the thread's base address occupies a register.  Entries beyond the shared-memory share go
 // to a local array (rare: the window holds the first 32 references of a 4-byte-reference layout).
 // ------------------------------------------------------------------------------------------
-template <class Entry>
+template <class Entry, int kWindowBytes = kStackSmemBytesPerBlock>
 struct LaneStack {
   static_assert(sizeof(Entry) % 4 == 0, "stack entries are stored as 32-bit words");
   static constexpr int kWords = (int)sizeof(Entry) / 4;
   static constexpr uint32_t kSlot = (uint32_t)kBlockThreads * 4u * (uint32_t)kWords;
-  static constexpr int kFit = (int)((uint32_t)kStackSmemBytesPerBlock / kSlot);
+  static constexpr int kFit = (int)((uint32_t)kWindowBytes / kSlot);
   static constexpr int kSmem = kFit < SCION_STACK_DEPTH ? kFit : SCION_STACK_DEPTH;
   static_assert(kSmem >= 1, "the shared-memory window must hold at least one entry per thread");
   static constexpr int kDeep = SCION_STACK_DEPTH - kSmem > 0 ? SCION_STACK_DEPTH - kSmem : 1;
@@ -699,6 +699,13 @@ struct WideEntry {
 #ifndef SCION_MINB8
 #define SCION_MINB8 4
 #endif
+#ifndef SCION_STACK_SMEM8
+// 4 CTAs/SM (124 registers) leave shared memory to spare, and the entries are 8 bytes (16 with 64-bit
+// references).  C5 probe, bvh8 / bvh8-q16 (64-bit references): 12 KB 1433 / 1391, 16 KB 1494 / 1451,
+// 24 KB 1531 / 1493, 32 KB 1529 / 1491 Mrays/s; the -ci layouts (32-bit references) do not care.
+#define SCION_STACK_SMEM8 (24 * 1024)
+#endif
+constexpr int kStackSmemBytesPerBlock8 = SCION_STACK_SMEM8;
 #ifndef SCION_INNER8
 #define SCION_INNER8 1
 #endif
@@ -723,7 +730,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   using Entry = WideEntry<Ref>;
-  using LS = LaneStack<Entry>;
+  using LS = LaneStack<Entry, kStackSmemBytesPerBlock8>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CoopScratch2 coop[kBlockThreads / 32];
   __shared__ RayStash stash[kBlockThreads];
