@@ -1,0 +1,170 @@
+// scion_run — native C++ harness over the C ABI (include/scion_b200.h): the slice of the reference CLI
+// (`layoutc footprint | bench`) that belongs to the traversal path, written the way a
+// maintainer of the C++ reference would call the B200 backend — nothing here but the C ABI and the
+// CUDA runtime (device buffers, events).
+//   scion_run layouts
+//   scion_run footprint <layout> <terrain|sphere|cloud>:<N>
+//   scion_run bench     <layout> <scene>:<N> <queries> [primary|secondary|points] [--host-encode]
+// `bench` follows the paper's protocol: 1 warm-up + 9 runs, drop the 2
+// lowest and 2 highest, mean of the remaining 5; prints one CSV row; the un-timed instrumented pass gives
+// the reference's counters (node visits, primitive tests) and the algorithmic bytes per query.
+// Exit codes as the reference CLI: 0 pass, 1 diagnostics / query errors, 2 usage.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "scion_b200.h"
+
+static int die(int code, const char* what) {
+  std::fprintf(stderr, "scion_run: %s: %s\n", what, scion_last_error());
+  return code;
+}
+#define CK(x) do { if ((x) != SCION_OK) return die(1, #x); } while (0)
+#define CU(x) do { cudaError_t e__ = (x); if (e__ != cudaSuccess) { std::fprintf(stderr, "scion_run: %s: %s\n", #x, cudaGetErrorString(e__)); return 1; } } while (0)
+
+static int make_scene(const std::string& spec, scion_scene** out, bool* terrain) {
+  const size_t c = spec.find(':');
+  const std::string kind = spec.substr(0, c);
+  const uint64_t n = c == std::string::npos ? 64 : std::strtoull(spec.c_str() + c + 1, nullptr, 10);
+  *terrain = kind == "terrain";
+  if (kind == "terrain") return scion_scene_terrain((uint32_t)n, 1, out);
+  if (kind == "sphere") return scion_scene_sphere((uint32_t)n, 1, out);
+  if (kind == "cloud") return scion_scene_cloud(n, 1, out);
+  return SCION_ERR_ARG;
+}
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: scion_run layouts | footprint <layout> <scene>:<N> | bench <layout> <scene>:<N> <queries> [primary|secondary|points] [--host-encode]\n");
+    return 2;
+  }
+  const std::string cmd = argv[1];
+  if (cmd == "layouts") {
+    for (int i = 0; i < scion_layout_count(); i++) {
+      scion_layout_info li;
+      CK(scion_layout_info_at(i, &li));
+      std::printf("%-14s family=%d arity=%d node_stride=%u segments=%u ref_bits=%u max_leaf=%u cpq=%d\n", li.name, li.family, li.arity, li.node_stride, li.n_segments, li.ref_bits,
+                  li.max_leaf, li.has_cpq);
+    }
+    return 0;
+  }
+  if ((cmd != "footprint" && cmd != "bench") || argc < 4) return 2;
+  const char* layout = argv[2];
+  scion_layout_info li;
+  if (scion_layout_find(layout, &li) != SCION_OK) return die(2, "unknown layout");
+  scion_scene* scene = nullptr;
+  bool terrain = false;
+  if (make_scene(argv[3], &scene, &terrain) != SCION_OK) return die(2, "bad scene");
+  scion_ltree* lt = nullptr;
+  CK(scion_build_sah(scene, 32, 4, 64, &lt));
+  if (li.arity == 8) CK(scion_ltree_collapse8(lt));
+  const uint64_t nprims = scion_ltree_nprims(lt);
+
+  if (cmd == "footprint") {
+    scion_ptree* pt = nullptr;
+    CK(scion_encode(lt, layout, &pt));
+    std::printf("{\"layout\": \"%s\", \"scene\": \"%s\", \"primitives\": %llu, \"total_bytes\": %llu, \"node_bytes\": %llu, \"bvh_bytes_per_prim\": %.6f, \"node_stride\": %u}\n", layout,
+                argv[3], (unsigned long long)nprims, (unsigned long long)scion_ptree_total_bytes(pt), (unsigned long long)scion_ptree_node_bytes(pt),
+                (double)scion_ptree_node_bytes(pt) / (double)nprims, li.node_stride);
+    scion_ptree_free(pt);
+    scion_ltree_free(lt);
+    scion_scene_free(scene);
+    return 0;
+  }
+
+  if (argc < 5) return 2;
+  const uint64_t n = std::strtoull(argv[4], nullptr, 10);
+  std::string kind = argc > 5 && argv[5][0] != '-' ? argv[5] : "primary";
+  bool host_encode = false;
+  for (int i = 5; i < argc; i++) host_encode |= std::strcmp(argv[i], "--host-encode") == 0;
+  const bool cpq = kind == "points";
+  if (cpq && !li.has_cpq) { std::fprintf(stderr, "scion_run: cpq requires a binary layout\n"); return 2; }
+
+  scion_dtree* dt = nullptr;
+  uint64_t node_bytes = 0;
+  double hot = (double)li.node_stride;  // bytes of the segment every visit reads (segment 0 of the node group)
+  {
+    scion_ptree* pt = nullptr;  // footprint numbers come from the host plan either way
+    CK(scion_encode(lt, layout, &pt));
+    node_bytes = scion_ptree_node_bytes(pt);
+    for (int b = 0; b < scion_ptree_nbuffers(pt) && li.n_segments > 1; b++) {
+      uint64_t bases[8], count = 0;
+      const int ns = scion_ptree_segment_bases(pt, b, bases, 8);
+      CK(scion_ptree_buffer(pt, b, nullptr, nullptr, nullptr, &count));
+      if (ns > 1 && count) hot = (double)(bases[1] - bases[0]) / (double)count;  // plan.cpp:333-347: base[s+1] = base[s] + count * stride[s] (aligned)
+    }
+    if (host_encode) CK(scion_dtree_upload(pt, 0, &dt));
+    scion_ptree_free(pt);
+    if (!host_encode) CK(scion_encode_device(lt, layout, 0, &dt));  // build_physical on the GPU
+  }
+  float lo[3], hi[3];
+  scion_scene_bounds(scene, lo, hi);
+  void *d_q = nullptr, *d_r = nullptr;
+  uint32_t* d_st = nullptr;
+  scion_counters* d_ctr = nullptr;
+  CU(cudaMalloc(&d_q, n * (cpq ? 12 : sizeof(scion_ray))));
+  CU(cudaMalloc(&d_r, n * (cpq ? sizeof(scion_cp) : sizeof(scion_hit))));
+  CU(cudaMalloc(&d_st, n * sizeof(uint32_t)));
+  CU(cudaMalloc(&d_ctr, n * sizeof(scion_counters)));
+  if (cpq) {
+    CK(scion_gen_points(lo, hi, 7, 0, n, (float*)d_q, nullptr));
+  } else if (kind == "secondary") {
+    CK(scion_gen_secondary(dt, 7, 0, n, (scion_ray*)d_q, nullptr));
+  } else {
+    uint32_t side = 1;
+    while ((uint64_t)(side + 1) * (side + 1) <= n) side++;
+    scion_camera cam;
+    scion_camera_default(lo, hi, terrain ? 1 : 0, side, side, &cam);
+    CK(scion_gen_primary(&cam, 0, n, (scion_ray*)d_q, nullptr));
+  }
+  auto run = [&](uint32_t* st, scion_counters* ctr) {
+    return cpq ? scion_closest_point(dt, (const float*)d_q, n, (scion_cp*)d_r, st, ctr, 0, nullptr)
+               : scion_closest_hit(dt, (const scion_ray*)d_q, n, (scion_hit*)d_r, st, ctr, 0, nullptr);
+  };
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  std::vector<float> ms;
+  for (int i = 0; i < 10; i++) {
+    CU(cudaEventRecord(e0));
+    CK(run(nullptr, nullptr));
+    CU(cudaEventRecord(e1));
+    CU(cudaEventSynchronize(e1));
+    float t = 0;
+    CU(cudaEventElapsedTime(&t, e0, e1));
+    if (i) ms.push_back(t);
+  }
+  std::sort(ms.begin(), ms.end());
+  const double mean_ms = (ms[2] + ms[3] + ms[4] + ms[5] + ms[6]) / 5.0;
+  // instrumented pass: the reference's cost counters + per-query status
+  CK(run(d_st, d_ctr));
+  CU(cudaDeviceSynchronize());
+  std::vector<scion_counters> ctr(n);
+  std::vector<uint32_t> st(n);
+  CU(cudaMemcpy(ctr.data(), d_ctr, n * sizeof(scion_counters), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(st.data(), d_st, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  double visits = 0, prims = 0, cold = 0;
+  uint64_t errors = 0;
+  for (uint64_t i = 0; i < n; i++) {
+    visits += ctr[i].node_visits;
+    prims += ctr[i].prim_tests;
+    cold += ctr[i].cold_loads;
+    errors += st[i] != SCION_Q_OK;
+  }
+  visits /= (double)n; prims /= (double)n; cold /= (double)n;
+  // algorithmic bytes per query: hot segment per visit, the rest of the node per cold load
+  const double bpq = visits * hot + cold * ((double)li.node_stride - hot) + prims * 36.0 + (cpq ? 32.0 : 40.0);
+  std::printf("layout,algorithm,scene,n_gpus,queries,kind,mean_ms,mqueries_per_s,bvh_bytes_per_prim,node_visits,prim_tests,bytes_per_query,achieved_gbs,query_errors,encode\n");
+  std::printf("%s,%s,%s,1,%llu,%s,%.4f,%.2f,%.3f,%.2f,%.2f,%.1f,%.1f,%llu,%s\n", layout, cpq ? "cpq" : "chrt", argv[3], (unsigned long long)n, kind.c_str(), mean_ms, (double)n / mean_ms / 1e3,
+              (double)node_bytes / (double)nprims, visits, prims, bpq, bpq * (double)n / mean_ms / 1e6, (unsigned long long)errors, host_encode ? "host" : "device");
+  cudaFree(d_q); cudaFree(d_r); cudaFree(d_st); cudaFree(d_ctr);
+  scion_dtree_free(dt);
+  scion_ltree_free(lt);
+  scion_scene_free(scene);
+  return errors ? 1 : 0;
+}

@@ -59,3 +59,38 @@ def test_bench_csv(built):
     lines = out.strip().splitlines()
     assert rc == 0 and lines[0].startswith("layout,algorithm,scene,n_gpus") and len(lines) == 3
     assert float(lines[1].split(",")[7]) > 0
+
+
+def test_native_harness_footprint_equals_python(built):
+    """csrc/tools/scion_run.cpp: a C++ caller that uses nothing but include/scion_b200.h (the drop-in boundary)."""
+    import json, os, subprocess
+    sb = built
+    exe = os.path.join(os.path.dirname(sb.__file__), "bin", "scion_run")
+    assert os.path.exists(exe), "scion_run is built by csrc/Makefile"
+    out = subprocess.run([exe, "layouts"], capture_output=True, text=True)
+    assert out.returncode == 0 and len(out.stdout.strip().splitlines()) == len(sb.layouts())
+    for layout in ("pbrt-q16", "bvh8-q8-ci", "dop14"):
+        r = subprocess.run([exe, "footprint", layout, "terrain:24"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        rep = json.loads(r.stdout)
+        lt = sb.Scene.terrain(24, 1).build_sah(32, 4).collapse8()
+        pt = lt.encode(layout)
+        assert rep["total_bytes"] == pt.total_bytes and rep["node_bytes"] == pt.node_bytes and rep["primitives"] == lt.nprims
+    assert subprocess.run([exe, "footprint", "no-such-layout", "terrain:8"], capture_output=True).returncode == 2  # usage class
+    if sb.device_count() == 0:  # the product has no CPU fallback: bench must fail loudly
+        r = subprocess.run([exe, "bench", "pbrt-q16", "terrain:8", "256"], capture_output=True, text=True)
+        assert r.returncode == 1 and "no CUDA device" in r.stderr
+
+
+@pytest.mark.gpu
+def test_native_harness_bench(built):
+    import os, subprocess
+    sb = built
+    exe = os.path.join(os.path.dirname(sb.__file__), "bin", "scion_run")
+    for args in (["pbrt-q16", "terrain:64", "65536", "primary"], ["bvh8-q8-ci", "terrain:64", "65536", "secondary"], ["pbrt-soa", "sphere:32", "4096", "points"],
+                 ["sg-eq", "terrain:64", "65536", "secondary", "--host-encode"]):
+        r = subprocess.run([exe, "bench"] + args, capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        head, row = r.stdout.strip().splitlines()
+        rec = dict(zip(head.split(","), row.split(",")))
+        assert rec["layout"] == args[0] and float(rec["mqueries_per_s"]) > 0 and int(rec["query_errors"]) == 0 and float(rec["node_visits"]) > 0
