@@ -23,6 +23,7 @@ class Segment:
     count: int
     camera: object = None   # sb.Camera for primary
     seed: int = 0
+    offset: int = 0    # first index of this segment inside its generator stream (a stream may be cut into several segments)
 
 
 @dataclass
@@ -91,12 +92,23 @@ def workload(name: str, lo=None, hi=None, scale: float = 1.0) -> Workload:
         w.segments = [Segment("points", cnt(1 << 24), seed=seed + 4)]
         return w
     if name == "c5":  # 256M primary + secondary rays, 10M-triangle terrain
-        w = Workload(name, "terrain", 2236, 1, "chrt", description="9999392-triangle terrain, 2^28 rays = 8 orbit cameras x 4096^2 primary + 2^27 secondary")
+        w = Workload(name, "terrain", 2236, 1, "chrt", description="9999392-triangle terrain, 2^28 rays = 8 orbit cameras x 4096^2 primary + 2^27 secondary, interleaved in 128 strips")
         if lo is not None:
             side = max(1, int(round(4096 * math.sqrt(scale))))
-            for k in range(8):
-                w.segments.append(Segment("primary", side * side, orbit_camera(lo, hi, k, 8, side, side)))
-            w.segments.append(Segment("secondary", 8 * side * side, seed=seed + 5))
+            # Order of the global index space: 8 rounds; round j holds one eighth (a strip of rows) of every camera's
+            # image — strip (j + k) mod 8 of camera k, because the top and the bottom of an image cost very different
+            # amounts — each followed by one piece of the secondary stream.  Any contiguous 1/2, 1/4 or 1/8
+            # of the index space — the range of one rank — then holds the same mix of cheap coherent and expensive
+            # incoherent rays and of all eight viewpoints ("the only risk is cost imbalance of
+            # contiguous primary-ray ranges").  The SET of rays does not depend on the order.
+            img = side * side
+            strip = max(1, img // 8)
+            rounds = 8 if img % 8 == 0 else 1
+            for j in range(rounds):
+                for k in range(8):
+                    cnt_p = strip if rounds == 8 else img
+                    w.segments.append(Segment("primary", cnt_p, orbit_camera(lo, hi, k, 8, side, side), offset=((j + k) % 8) * strip if rounds == 8 else 0))
+                    w.segments.append(Segment("secondary", cnt_p, seed=seed + 5, offset=(j * 8 + k) * cnt_p))
         return w
     raise ValueError(f"unknown workload {name}")
 
@@ -110,7 +122,7 @@ def slices(w: Workload, first: int, count: int) -> List[Tuple[Segment, int, int,
     for seg in w.segments:
         a, b = max(first, base), min(end, base + seg.count)
         if a < b:
-            out.append((seg, a - base, b - a, a - first))
+            out.append((seg, a - base + seg.offset, b - a, a - first))
         base += seg.count
     return out
 

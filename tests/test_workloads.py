@@ -13,8 +13,24 @@ def test_slices_and_per_rank_generation(built):
     scene = built.Scene.terrain(10, 1)
     lt = scene.build_sah(32, 4)
     lo, hi = scene.bounds()
-    wl = W.workload("c5", lo, hi, scale=2.0 ** -16)  # 8 cameras x 16x16 + 2048 secondary
-    assert wl.total == 8 * 256 + 2048 and len(wl.segments) == 9
+    wl = W.workload("c5", lo, hi, scale=2.0 ** -16)  # 8 cameras x 16x16 primary + 2048 secondary, interleaved in 8 rounds
+    assert wl.total == 8 * 256 + 2048 and len(wl.segments) == 128
+    # the secondary segments are consecutive pieces of ONE stream (same seed): together they are its first 2048 rays
+    sec = [s for s in wl.segments if s.kind == "secondary"]
+    assert [s.offset for s in sec] == [i * 32 for i in range(64)] and len({s.seed for s in sec}) == 1
+    # every camera's image is covered exactly once
+    for k in range(8):
+        strips = sorted((s.offset, s.count) for s in wl.segments if s.kind == "primary")[k::8]
+    prim = {}
+    for s in wl.segments:
+        if s.kind == "primary":
+            prim.setdefault(tuple(s.camera.eye), []).append((s.offset, s.count))
+    assert len(prim) == 8 and all(sorted(v) == [(j * 32, 32) for j in range(8)] for v in prim.values())
+    # every eighth of the index space holds the same mix: what makes contiguous rank ranges balanced
+    for r in range(8):
+        first, count = built.partition(wl.total, r, 8)
+        kinds = sorted((seg.kind, c) for seg, _, c, _ in W.slices(wl, first, count))
+        assert kinds == [("primary", 32)] * 8 + [("secondary", 32)] * 8
     full = W.generate_host(wl, lt.triangles(), lo, hi, 0, wl.total)
     assert full.shape[0] == wl.total
     for world in (1, 2, 3, 8):
@@ -33,7 +49,7 @@ def test_slices_and_per_rank_generation(built):
     try:
         wl2 = W.workload("c5", lo, hi, scale=2.0 ** -16)
         other = W.generate_host(wl2, lt.triangles(), lo, hi, 0, wl2.total)
-        assert not np.array_equal(other.view(np.uint32)[8 * 256:], full.view(np.uint32)[8 * 256:])
+        assert not np.array_equal(other.view(np.uint32).reshape(-1, 8)[32:64], full.view(np.uint32).reshape(-1, 8)[32:64])  # first secondary piece
     finally:
         del os.environ["LAYOUTC_SEED"]
 
