@@ -13,10 +13,14 @@
 // Queries fan out with OpenMP schedule(dynamic,64), the paper's CPU scheme;
 // each query owns its accumulators.
 //
-// PARITY PINNING: no executable reference exists for this path (src/interp.cpp, src/harness.cpp
-// are placeholders).  Pinned against the reference's KATs (tests/test_oracle_kats.py) and the
-// reference planner's slot tables (tests/golden/ref_plans.json); hit results themselves are
-// "parity unpinned" beyond those vectors — see DESIGN.md.
+// PARITY PINNING: the reference has no executor (src/interp.cpp, src/harness.cpp are placeholders), but
+// its compiler does produce the lowered traversal.  closest_hit is pinned against that: oracle/ref_interp.cpp
+// executes the reference's own IR (reference parser, sema, planner, specialize_destructors, bit reader) on
+// trees built by this repository and tests/test_ref_ir_golden.py requires this oracle (and the CUDA kernels)
+// to reproduce its answers bit for bit for the 15 corpus layouts.  Also pinned: the reference's KATs
+// (tests/test_oracle_kats.py) and the reference planner's slot tables (tests/golden/ref_plans.json).
+// Still "parity unpinned": the arithmetic inside intrinsics (dot/cross/sum association, min/max on NaN),
+// closest_point and collision_detection results (the reference's lowering of both is broken) — see DESIGN.md §4.
 #include <omp.h>
 
 #include <algorithm>

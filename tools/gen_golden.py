@@ -3,6 +3,7 @@ where /root/reference exists):
   ref_plans.json      — the REFERENCE planner's output (oracle/_ref/ref_probe, i.e. the reference's
                         own parse_corpus -> check_layout -> plan_layout) for its 15 corpus layouts
                         and for our authored layout files.
+  ref_ir.npz          — written by tools/gen_ref_ir_golden.py (the reference's own lowered IR, interpreted): see there.
   hits_small.npz      — oracle results (closest_hit / closest_point) on a small seeded scene for
                         every layout: the GPU tests compare against these even where the oracle
                         library is unavailable.

@@ -1,0 +1,106 @@
+"""Regenerates tests/golden/ref_ir.npz — closest-hit answers computed by the REFERENCE's own compiled
+traversal (oracle/_ref/ref_interp: the reference's parser, type checker, planner and destructor specialiser,
+its lowered IR executed by the interpreter in oracle/ref_interp.cpp) on PhysicalTrees produced by THIS
+repository's encoders, for the reference's 15 corpus layouts.  Run in the build container (the only place
+/root/reference exists); the fixture pins both the CPU oracle and the CUDA kernels on the GPU box.
+
+The reference returns `best = (t, Triangle)` — the triangle VALUE; it is mapped back to the primitive index
+through the tree-ordered triangle array (exact 9-float match, first occurrence)."""
+import os, struct, subprocess, sys, tempfile
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import paper_2511_15028_b200 as sb
+
+INTERP = os.path.join(ROOT, "oracle", "_ref", "ref_interp")
+CORPUS = ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14",
+          "bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
+
+
+def wstr(f, s):
+    b = s.encode()
+    f.write(struct.pack("<I", len(b)))
+    f.write(b)
+
+
+def write_input(path, pt, rays):
+    with open(path, "wb") as f:
+        bufs = pt.buffers()
+        f.write(struct.pack("<II", 0x54494353, len(bufs)))
+        for b in bufs:
+            wstr(f, b["name"])
+            f.write(struct.pack("<QI", b["count"], len(b["seg_bases"])))
+            for s in b["seg_bases"]:
+                f.write(struct.pack("<Q", s))
+            f.write(struct.pack("<Q", b["bytes"]))
+            f.write(bytes(b["data"]))
+        gl = pt.globals()
+        f.write(struct.pack("<I", len(gl)))
+        for g in gl:
+            wstr(f, g["name"])
+            f.write(g["raw"])
+        r0, carried = pt.root()
+        f.write(struct.pack("<Q6f", r0, *carried))
+        f.write(struct.pack("<Q", rays.shape[0]))
+        f.write(rays.tobytes())
+
+
+def special_rays(lo, hi):
+    """axis-parallel rays (zero direction components: the 0 * inf = NaN path of the slab test), rays starting
+    inside the bounds, a finite tmax that cuts hits off, and rays that miss the root"""
+    c = 0.5 * (lo + hi)
+    out = []
+    for axis in range(3):
+        for sgn in (1.0, -1.0):
+            d = np.zeros(3, np.float32); d[axis] = sgn
+            o = c.copy(); o[axis] = (lo[axis] - 1.0) if sgn > 0 else (hi[axis] + 1.0)
+            for dx, dz in ((0.0, 0.0), (0.13, -0.21), (-0.4, 0.33)):
+                oo = o.copy(); oo[(axis + 1) % 3] += dx * (hi - lo)[(axis + 1) % 3]; oo[(axis + 2) % 3] += dz * (hi - lo)[(axis + 2) % 3]
+                out.append((oo, np.inf, d))
+                out.append((oo, 0.75, d))
+    out.append((c + np.float32(0.01), np.inf, np.array([0.3, -0.9, 0.1], np.float32)))   # from inside
+    out.append((hi + 5.0, np.inf, np.array([1.0, 1.0, 1.0], np.float32)))                 # misses the root
+    out.append((c, np.inf, np.array([-0.0, -1.0, 0.0], np.float32)))                      # -0.0 is not negative
+    rays = np.zeros(len(out), sb.RAY_DTYPE)
+    for i, (o, tmax, d) in enumerate(out):
+        rays[i] = (o[0], o[1], o[2], tmax, d[0], d[1], d[2], 0.0)
+    return rays
+
+
+def main():
+    assert os.path.exists(INTERP), "build it first: make -C oracle ref"
+    out = {}
+    for tag, scene, builder in (("terrain", sb.Scene.terrain(12, 5), "sah"), ("sphere", sb.Scene.sphere(8, 3), "median")):
+        lt = (scene.build_sah(32, 4) if builder == "sah" else scene.build_median(2)).collapse8()
+        lo, hi = scene.bounds()
+        cam = sb.default_camera(lo, hi, tag == "terrain", 16, 16)
+        rays = np.concatenate([sb.gen_primary_host(cam, 0, 256), sb.gen_secondary_host(lt.triangles(), 9, 0, 192), special_rays(np.asarray(lo), np.asarray(hi))])
+        tris = np.ascontiguousarray(lt.triangles(), np.float32).reshape(-1, 9)
+        index = {}
+        for i, t in enumerate(tris):
+            index.setdefault(t.tobytes(), i)
+        out[f"{tag}:rays"] = rays.view(np.float32).reshape(-1, 8).copy()
+        out[f"{tag}:scene"] = np.array([12, 5] if tag == "terrain" else [8, 3])
+        for layout in CORPUS:
+            pt = lt.encode(layout)
+            with tempfile.TemporaryDirectory() as td:
+                fin, fout = os.path.join(td, "in.bin"), os.path.join(td, "out.bin")
+                write_input(fin, pt, rays)
+                r = subprocess.run([INTERP, layout, "chrt", fin, fout], capture_output=True, text=True)
+                if r.returncode != 0:
+                    raise SystemExit(f"{layout}: {r.stderr}")
+                rec = np.fromfile(fout, np.float32).reshape(-1, 10)
+            t = rec[:, 0].copy()
+            prim = np.full(len(t), sb.MISS_PRIM, np.uint32)
+            for q in range(len(t)):
+                if np.isfinite(t[q]):
+                    prim[q] = index[rec[q, 1:].tobytes()]
+            out[f"{tag}:t:{layout}"] = t
+            out[f"{tag}:prim:{layout}"] = prim
+            print(f"{tag:8s} {layout:14s} hits {int(np.isfinite(t).sum()):4d}/{len(t)}  {r.stderr.strip()}")
+    np.savez_compressed(os.path.join(ROOT, "tests", "golden", "ref_ir.npz"), **out)
+    print("tests/golden/ref_ir.npz written")
+
+
+if __name__ == "__main__":
+    main()
