@@ -279,6 +279,16 @@ int scion_collision_detection(const scion_dtree* a, const scion_dtree* b, scion_
 /* host-buffer form: pairs copied back (D2H) */
 int scion_collision_detection_host(const scion_dtree* a, const scion_dtree* b, scion_pair* h_out, uint64_t capacity, uint64_t* out_count,
                                    scion_cd_stats* stats);
+/* Batch ray/triangle primitive test: pair i = (d_rays[i], d_tris9[9*i .. 9*i+8]).  method 0 = Moeller-Trumbore
+ * (geometry.scion:25-38, the test every traversal uses), 1 = Pluecker coordinates (geometry.scion:40-55; never
+ * selected by the corpus dispatcher :57-59 — exposed for the Appendix F fidelity check, SPEC acceptance 9). */
+typedef struct scion_trihit {
+  float b0, b1, b2, t; /* TriangleIntersection (geometry.scion:9); zeros on a miss */
+  uint32_t hit;
+} scion_trihit;
+#define SCION_TRI_MT 0
+#define SCION_TRI_PLUECKER 1
+int scion_ray_triangle(const scion_ray* d_rays, const float* d_tris9, uint64_t n, int method, scion_trihit* d_out, void* stream);
 /* Host-buffer entry points (the reference-facing call: host in, host out). H2D copy,
  * kernel, D2H copy, stream sync; chunked + double-buffered over two streams. */
 int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64_t n, scion_hit* h_hits,

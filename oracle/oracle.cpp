@@ -279,6 +279,21 @@ int oracle_ray_tri(const float o[3], const float d[3], float tmax, const float t
   out[0] = h.b0; out[1] = h.b1; out[2] = h.b2; out[3] = h.t;
   return h.some ? 1 : 0;
 }
+// batch form, method 0 = Moeller-Trumbore (geometry.scion:25-38), 1 = Pluecker (geometry.scion:40-55);
+// rays are scion_ray records (8 floats), out = (b0, b1, b2, t, hit as 0/1 bits) per pair
+void oracle_ray_tri_batch(const float* rays8, const float* tris9, uint64_t n, int method, float* out5) {
+  for (uint64_t i = 0; i < n; i++) {
+    const float* r = rays8 + 8 * i;
+    Tri t;
+    std::memcpy(&t, tris9 + 9 * i, 36);
+    const Ray ray{{r[0], r[1], r[2]}, {r[4], r[5], r[6]}, r[3]};
+    const TriHit h = method == 1 ? ray_tri_pc(ray, t) : ray_tri_mt(ray, t);
+    float* o = out5 + 5 * i;
+    o[0] = h.b0; o[1] = h.b1; o[2] = h.b2; o[3] = h.t;
+    const uint32_t hit = h.some ? 1u : 0u;
+    std::memcpy(o + 4, &hit, 4);
+  }
+}
 void oracle_point_tri(const float p[3], const float tri9[9], float out_pt[3], float out_bary[3]) {
   Tri t;
   std::memcpy(&t, tri9, 36);

@@ -130,6 +130,31 @@ inline TriHit ray_tri_mt(const Ray& ray, const Tri& tri) {
   return {true, b0, u, v, t};
 }
 
+// ------------------------------------------------------------------ geometry.scion:40-55 (Pluecker-coordinate test)
+// 2^-23 edge tolerance band; `min({..})` / `max({..})` fold left to right; the dispatcher
+// (geometry.scion:57-59) always selects MT, so no traversal of the corpus calls this one — it exists for the
+// Appendix F fidelity check (SPEC acceptance criterion 9: MT vs Pluecker cross-agreement).
+inline TriHit ray_tri_pc(const Ray& ray, const Tri& tri) {
+  V3 v0 = sub(tri.p0, ray.o), v1 = sub(tri.p1, ray.o), v2 = sub(tri.p2, ray.o);
+  V3 e0 = sub(v2, v0), e1 = sub(v0, v1), e2 = sub(v1, v2);
+  float u_raw = dot(cross(e0, add(v2, v0)), ray.d);
+  float v_raw = dot(cross(e1, add(v0, v1)), ray.d);
+  float w_raw = dot(cross(e2, add(v1, v2)), ray.d);
+  float uvw = (u_raw + v_raw) + w_raw;
+  float e = 0.00000011920928955078125f * fabs_bits(uvw);
+  float min_uvw = fminf(fminf(u_raw, v_raw), w_raw), max_uvw = fmaxf(fmaxf(u_raw, v_raw), w_raw);
+  if (!(min_uvw >= -e || max_uvw <= e)) return {false, 0, 0, 0, 0};
+  V3 ng = cross(e0, e1);
+  float den = 2.0f * dot(ng, ray.d), t_raw = 2.0f * dot(v0, ng);
+  float t = t_raw / den;
+  if (!(t >= 0.0f && t <= ray.tmax)) return {false, 0, 0, 0, 0};
+  if (den == 0.0f) return {false, 0, 0, 0, 0};
+  float inv_uvw = 1.0f / uvw;
+  float b0 = w_raw * inv_uvw, b1 = u_raw * inv_uvw, b2 = v_raw * inv_uvw;
+  if (b0 < 0.0f || b1 < 0.0f || b2 < 0.0f) return {false, 0, 0, 0, 0};
+  return {true, b0, b1, b2, t};
+}
+
 // ------------------------------------------------------------------ geometry.scion:76-100
 struct ClosestPt { V3 p; V3 bary; };
 inline ClosestPt point_triangle(V3 p, const Tri& tri) {

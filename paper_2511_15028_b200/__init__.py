@@ -129,6 +129,7 @@ def lib() -> C.CDLL:
         "scion_dtree_upload_into": (i32, [vp, i32, vp, u64, P(vp)]),
         "scion_dtree_image": (i32, [vp, P(vp), P(u64)]),
         "scion_dtree_download_image": (i32, [vp, vp, u64]),
+        "scion_ray_triangle": (i32, [vp, vp, u64, i32, vp, vp]),
         "scion_encode_device": (i32, [vp, cp, i32, P(vp)]),
         "scion_dtree_from_image": (i32, [cp, vp, u64, i32, i32, P(vp)]),
         "scion_dtree_free": (None, [vp]),
@@ -518,6 +519,15 @@ class DeviceTree:
 
     def __del__(self):
         self.free()
+
+
+TRIHIT_DTYPE = np.dtype([("b0", np.float32), ("b1", np.float32), ("b2", np.float32), ("t", np.float32), ("hit", np.uint32)])
+TRI_MT, TRI_PLUECKER = 0, 1
+
+
+def ray_triangle(d_rays: int, d_tris9: int, n: int, method: int, d_out: int, stream: int = 0):
+    """Batch ray/triangle test on the device: Moeller-Trumbore (0) or Pluecker coordinates (1), geometry.scion:25-55."""
+    _check(lib().scion_ray_triangle(d_rays, d_tris9, n, method, d_out, stream or None))
 
 
 # --------------------------------------------------------------------------------------- generators

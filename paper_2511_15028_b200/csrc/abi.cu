@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "device/geometry.cuh"
 #include "device/launch.cuh"
 #include "host/encode_node.hpp"
 #include "host/physical.hpp"
@@ -172,6 +173,20 @@ struct FileR {
 }  // namespace
 
 namespace scion {
+__global__ void ray_triangle_kernel(const scion_ray* __restrict__ rays, const float* __restrict__ tris, uint64_t n, int method, scion_trihit* __restrict__ out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const scion_ray r = rays[i];
+  const RayCtx ray = make_ray(r.ox, r.oy, r.oz, r.tmax, r.dx, r.dy, r.dz);
+  float tri[9];
+#pragma unroll
+  for (int k = 0; k < 9; k++) tri[k] = tris[9 * i + k];
+  scion_trihit h{0.0f, 0.0f, 0.0f, 0.0f, 0u};
+  float b0, b1, b2, t;
+  const bool hit = method == SCION_TRI_PLUECKER ? ray_tri_pc_full(ray, tri, b0, b1, b2, t) : ray_tri_mt_full(ray, tri, b0, b1, b2, t);
+  if (hit) h = scion_trihit{b0, b1, b2, t, 1u};
+  out[i] = h;
+}
 // device-side encode: one thread per node (host/encode_node.hpp)
 __global__ void encode_nodes_kernel(const enc::EncodeJob job) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -643,6 +658,16 @@ int scion_closest_hit(const scion_dtree* t, const scion_ray* d_rays, uint64_t n,
 }
 int scion_closest_point(const scion_dtree* t, const float* d_points, uint64_t n, scion_cp* d_out, uint32_t* d_status, scion_counters* d_counters, int variant, void* stream) {
   return run_query(t, false, d_points, n, d_out, d_status, d_counters, variant, stream);
+}
+
+int scion_ray_triangle(const scion_ray* d_rays, const float* d_tris9, uint64_t n, int method, scion_trihit* d_out, void* stream) {
+  if ((!d_rays || !d_tris9 || !d_out) && n) return fail(SCION_ERR_ARG, "null argument");
+  if (method != SCION_TRI_MT && method != SCION_TRI_PLUECKER) return fail(SCION_ERR_ARG, "unknown triangle test");
+  if (n == 0) return SCION_OK;
+  scion::ray_triangle_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_rays, d_tris9, n, method, d_out);
+  CUDA_OK(cudaGetLastError());
+  g_launches.fetch_add(1);
+  return SCION_OK;
 }
 
 int scion_collision_detection(const scion_dtree* a, const scion_dtree* b, scion_pair* d_out, uint64_t capacity, uint64_t* out_count,

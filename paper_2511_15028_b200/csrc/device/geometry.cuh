@@ -68,6 +68,59 @@ SCION_DEV bool ray_tri_mt(const RayCtx& ray, const float* p, float& t_out) {
   return true;
 }
 
+// full results of the two ray/triangle tests of geometry.scion (batch entry point scion_ray_triangle):
+// intersectsp_ray_tri_mt :25-38 with barycentrics, and the Pluecker-coordinate test intersectsp_ray_tri_pc
+// :40-55 (2^-23 tolerance band; `min({..})` folds left to right).  The corpus dispatcher (:57-59) always
+// takes MT — the Pluecker test is here for the Appendix F fidelity check (SPEC acceptance criterion 9).
+SCION_DEV bool ray_tri_mt_full(const RayCtx& ray, const float* p, float& b0, float& b1, float& b2, float& t_out) {
+  const f32x3 p0{p[0], p[1], p[2]}, p1{p[3], p[4], p[5]}, p2{p[6], p[7], p[8]};
+  const f32x3 e1 = p0 - p1, e2 = p2 - p0;
+  const f32x3 ng = cross(e2, e1);
+  const f32x3 c = p0 - f32x3{ray.ox, ray.oy, ray.oz};
+  const f32x3 d{ray.dx, ray.dy, ray.dz};
+  const f32x3 r = cross(c, d);
+  const float D = dot(ng, d);
+  if (D == 0.0f) return false;
+  const float abs_D = scion::abs(D);
+  const uint32_t sgn_D = f2u(D) & 2147483648u;
+  const float u_raw = u2f(f2u(dot(r, e2)) ^ sgn_D);
+  const float v_raw = u2f(f2u(dot(r, e1)) ^ sgn_D);
+  if (!(u_raw >= 0.0f && v_raw >= 0.0f && u_raw + v_raw <= abs_D)) return false;
+  const float t_raw = u2f(f2u(dot(ng, c)) ^ sgn_D);
+  if (!(abs_D * 0.0f < t_raw && t_raw <= abs_D * ray.tmax)) return false;
+  const float inv_abs_D = 1.0f / abs_D;
+  t_out = t_raw * inv_abs_D;
+  const float u = u_raw * inv_abs_D, v = v_raw * inv_abs_D;
+  b0 = 1.0f - u - v;
+  b1 = u;
+  b2 = v;
+  return true;
+}
+SCION_DEV bool ray_tri_pc_full(const RayCtx& ray, const float* p, float& b0, float& b1, float& b2, float& t_out) {
+  const f32x3 o{ray.ox, ray.oy, ray.oz}, d{ray.dx, ray.dy, ray.dz};
+  const f32x3 v0 = f32x3{p[0], p[1], p[2]} - o, v1 = f32x3{p[3], p[4], p[5]} - o, v2 = f32x3{p[6], p[7], p[8]} - o;
+  const f32x3 e0 = v2 - v0, e1 = v0 - v1, e2 = v1 - v2;
+  const float u_raw = dot(cross(e0, v2 + v0), d);
+  const float v_raw = dot(cross(e1, v0 + v1), d);
+  const float w_raw = dot(cross(e2, v1 + v2), d);
+  const float uvw = (u_raw + v_raw) + w_raw;
+  const float e = 0.00000011920928955078125f * scion::abs(uvw);
+  const float min_uvw = fminf(fminf(u_raw, v_raw), w_raw), max_uvw = fmaxf(fmaxf(u_raw, v_raw), w_raw);
+  if (!(min_uvw >= -e || max_uvw <= e)) return false;
+  const f32x3 ng = cross(e0, e1);
+  const float den = 2.0f * dot(ng, d), t_raw = 2.0f * dot(v0, ng);
+  const float t = t_raw / den;
+  if (!(t >= 0.0f && t <= ray.tmax)) return false;
+  if (den == 0.0f) return false;
+  const float inv_uvw = 1.0f / uvw;
+  b0 = w_raw * inv_uvw;
+  b1 = u_raw * inv_uvw;
+  b2 = v_raw * inv_uvw;
+  if (b0 < 0.0f || b1 < 0.0f || b2 < 0.0f) return false;
+  t_out = t;
+  return true;
+}
+
 // slab_hit, dop.scion:5-17
 SCION_DEV bool slab_hit(float o, float d, float lo, float hi, float& tn, float& tf) {
   if (d == 0.0f) return !(o < lo || o > hi);

@@ -42,6 +42,8 @@ class Oracle:
         L.oracle_ray_aabb.argtypes = [vp, vp, f32, vp, vp, vp]
         L.oracle_ray_tri.argtypes = [vp, vp, f32, vp, vp]
         L.oracle_point_tri.argtypes = [vp, vp, vp, vp]
+        L.oracle_ray_tri_batch.argtypes = [vp, vp, u64, i32, vp]
+        L.oracle_ray_tri_batch.restype = None
         L.oracle_sqdist_point_aabb.argtypes = [vp, vp, vp]
         L.oracle_sqdist_point_aabb.restype = f32
         L.oracle_distmax_point_aabb.argtypes = [vp, vp, vp]
@@ -160,6 +162,14 @@ class Oracle:
         n = self.lib.oracle_brute_collisions(a.ctypes.data, a.shape[0], b.ctypes.data, b.shape[0], out.ctypes.data, capacity)
         assert 0 <= n <= capacity
         return out[:n].copy()
+
+    def ray_tri_batch(self, rays, tris9, method):
+        """(b0, b1, b2, t, hit) per (ray, triangle) pair; method 0 = Moeller-Trumbore, 1 = Pluecker"""
+        rays = np.ascontiguousarray(rays)
+        tris = np.ascontiguousarray(tris9, np.float32)
+        out = np.zeros((rays.shape[0], 5), np.float32)
+        self.lib.oracle_ray_tri_batch(rays.ctypes.data, tris.ctypes.data, rays.shape[0], method, out.ctypes.data)
+        return out
 
     def sat(self, a9, b9):
         a, b = np.ascontiguousarray(a9, np.float32), np.ascontiguousarray(b9, np.float32)
