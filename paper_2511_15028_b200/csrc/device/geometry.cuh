@@ -214,7 +214,21 @@ SCION_DEV void load_triangle36(const uint8_t* prims, uint64_t index, float (&v)[
   const uint64_t addr = (uint64_t)prims + index * 36ull;
   const uint4* q = reinterpret_cast<const uint4*>(addr & ~15ull);
   const uint32_t s = (uint32_t)(addr >> 2) & 3u;
+#if SCION_CACHE_HINTS >= 3
+  uint4 a, b, c;
+  const uint64_t pol = l2_policy_stream();
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(q), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(q + 1), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "l"(q + 2), "l"(pol));
+#elif SCION_CACHE_HINTS >= 2
+  uint4 a, b, c;
+  const uint64_t pol = l2_policy_stream();
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(q), "l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(q + 1), "l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "l"(q + 2), "l"(pol));
+#else
   const uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+#endif
   const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
   const bool s1 = (s & 1u) != 0u, s2 = (s & 2u) != 0u;
 #pragma unroll

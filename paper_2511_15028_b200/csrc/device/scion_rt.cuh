@@ -27,6 +27,13 @@
 #ifndef SCION_LDG256
 #define SCION_LDG256 1
 #endif
+#ifndef SCION_CACHE_HINTS
+// 0: plain read-only loads.  4 (default): primitive loads bypass L1 allocation and carry an L2 evict_first
+// policy — 360 MB of randomly accessed triangles otherwise push the 93 MB node array out of L2 (C5 probe:
+// pbrt-q16 +2.0 %, sg-eq +1.1 %, bvh8-q8-ci +0.8 %, closest point +4 %, pbrt -1.5 %, dop14 -0.5 %).
+// 1: node records L2 evict_last (±0);  2: 1 + primitives evict_first (+1.7 %);  3: 2 + L1::no_allocate (-3 %).
+#define SCION_CACHE_HINTS 4
+#endif
 #ifndef SCION_LDG_PARITY
 #define SCION_LDG_PARITY 1
 #endif
@@ -307,8 +314,15 @@ SCION_HOSTDEV void ld64(const uint8_t* p, uint32_t* o) {
   memcpy(o, p, 8);
 #endif
 }
-SCION_HOSTDEV void ld128(const uint8_t* p, uint32_t* o) {
 #if defined(__CUDA_ARCH__)
+// L2 eviction policies (experiment SCION_CACHE_HINTS): node records evict_last, primitives evict_first
+__device__ __forceinline__ uint64_t l2_policy_keep() { uint64_t p; asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p)); return p; }
+__device__ __forceinline__ uint64_t l2_policy_stream() { uint64_t p; asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p; }
+#endif
+SCION_HOSTDEV void ld128(const uint8_t* p, uint32_t* o) {
+#if defined(__CUDA_ARCH__) && (SCION_CACHE_HINTS == 1 || SCION_CACHE_HINTS == 2 || SCION_CACHE_HINTS == 3)
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p), "l"(l2_policy_keep()));
+#elif defined(__CUDA_ARCH__)
   uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
   o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
 #else

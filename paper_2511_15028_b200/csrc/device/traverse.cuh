@@ -51,6 +51,10 @@ constexpr int kChunk = SCION_CHUNK;     // queries a warp takes from the global 
 #ifndef SCION_GUIDED_CHUNKS
 #define SCION_GUIDED_CHUNKS 1
 #endif
+#ifndef SCION_GUIDED_NUM  /* switch to 32-query chunks when fewer than NUM/DEN full chunks per warp remain */
+#define SCION_GUIDED_NUM 2ull
+#define SCION_GUIDED_DEN 1ull
+#endif
 #ifndef SCION_REFILL_MIN
 #define SCION_REFILL_MIN 4
 #endif
@@ -77,7 +81,8 @@ struct Tally {
 
 // Warp-private window on the global work counter.  All 32 lanes call refill(); lanes that pass
 // want=true and for which work is left get a query index.  All members are warp-uniform.
-struct WorkFetcher {
+template <bool GUIDED>
+struct WorkFetcherT {
   unsigned long long chunk_base = 0;
   unsigned chunk_left = 0;
   bool exhausted = false;
@@ -96,9 +101,15 @@ struct WorkFetcher {
         unsigned take = (unsigned)kChunk;
         if (lane == 0) {
 #if SCION_GUIDED_CHUNKS
+          if (GUIDED) {
+#if SCION_GUIDED_CHUNKS == 2
           const unsigned long long seen = *reinterpret_cast<volatile unsigned long long*>(next);
+#else
+          const unsigned long long seen = chunk_base;  // end of this warp's previous chunk: a lower bound of the global progress, no extra load
+#endif
           const unsigned long long rem = seen < n ? n - seen : 0ull;
-          if (rem < (unsigned long long)gridDim.x * (kBlockThreads / 32) * 2ull * (unsigned long long)kChunk) take = 32u;
+          if (rem * SCION_GUIDED_DEN < (unsigned long long)gridDim.x * (kBlockThreads / 32) * SCION_GUIDED_NUM * (unsigned long long)kChunk) take = 32u;
+          }
 #endif
           base = atomicAdd(next, (unsigned long long)take);
         }
@@ -119,6 +130,10 @@ struct WorkFetcher {
     return got;
   }
 };
+using WorkFetcher = WorkFetcherT<true>;        // closest_hit kernels
+// closest_point keeps fixed 128-query chunks: with the guided rule C4 drops from 1246 to 1134 Mq/s (measured twice,
+// with and without the extra counter load; the cause is in the generated code, not in the policy)
+using WorkFetcherFixed = WorkFetcherT<false>;
 
 SCION_DEV RayCtx load_ray(const scion_ray* rays, uint64_t q) {
   const float4* p = reinterpret_cast<const float4*>(rays + q);
@@ -1017,7 +1032,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
   uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
   asm volatile("" : "+r"(window));
   uint32_t top = window + threadIdx.x * 4u;
-  WorkFetcher work;
+  WorkFetcherFixed work;
   (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;
