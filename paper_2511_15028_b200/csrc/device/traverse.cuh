@@ -48,6 +48,9 @@ namespace scion {
 constexpr int kBlockThreads = 128;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kChunk = SCION_CHUNK;     // queries a warp takes from the global counter at a time
+#ifndef SCION_STREAM_HITS
+#define SCION_STREAM_HITS 1
+#endif
 #ifndef SCION_GUIDED_CHUNKS
 #define SCION_GUIDED_CHUNKS 1
 #endif
@@ -135,6 +138,15 @@ using WorkFetcher = WorkFetcherT<true>;        // closest_hit kernels
 // with and without the extra counter load; the cause is in the generated code, not in the policy)
 using WorkFetcherFixed = WorkFetcherT<false>;
 
+// results are written once and never read by the kernel: streaming store (evict-first), so that 2 GB of hit
+// records do not displace node records in L2
+SCION_DEV void store_hit(scion_hit* dst, float t, uint32_t prim) {
+#if SCION_STREAM_HITS
+  __stcs(reinterpret_cast<float2*>(dst), make_float2(t, __uint_as_float(prim)));
+#else
+  *dst = scion_hit{t, prim};
+#endif
+}
 SCION_DEV RayCtx load_ray(const scion_ray* rays, uint64_t q) {
   const float4* p = reinterpret_cast<const float4*>(rays + q);
   const float4 a = __ldcs(p), b = __ldcs(p + 1);  // streaming: read once
@@ -371,7 +383,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
 
   auto retire = [&](uint32_t st) {
     const uint64_t qq = opaque(stash_q[threadIdx.x]);
-    hits[qq] = scion_hit{best_t, best_prim};
+    store_hit(hits + qq, best_t, best_prim);
     if (status) status[qq] = st;
     tally.store(counters, qq);
     mode = kFetch;
@@ -572,7 +584,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2X) chrt2x_kernel(con
 
   auto retire = [&](uint32_t st) {
     const uint64_t qq = opaque(stash_q[threadIdx.x]);
-    hits[qq] = scion_hit{best_t, best_prim};
+    store_hit(hits + qq, best_t, best_prim);
     if (status) status[qq] = st;
     tally.store(counters, qq);
     mode = kFetch;
@@ -780,7 +792,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const
 
   auto retire = [&](uint32_t st) {
     const uint64_t qq = opaque(stash_q[threadIdx.x]);
-    hits[qq] = scion_hit{best_t, best_prim};
+    store_hit(hits + qq, best_t, best_prim);
     if (status) status[qq] = st;
     tally.store(counters, qq);
     mode = kFetch;
