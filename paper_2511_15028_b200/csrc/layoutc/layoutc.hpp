@@ -208,6 +208,9 @@ struct Plan {
   std::string to_json() const;
 };
 
+// Well-formedness (check.cpp): throws LayoutError tagged with the reference's diagnostic class
+// ([DuplicateName], [MissingField], [NonExhaustiveSplit], [UnsupportedPattern]).  plan_layout runs it first.
+void check_layout(const Program& program, const Layout& layout, const TypeDecl& adt);
 Plan plan_layout(const Program& program, const std::string& registry_name);
 
 // emit_cuda: deterministic CUDA header text for the planned layout.

@@ -252,6 +252,7 @@ Plan plan_layout(const Program& program, const std::string& registry_name) {
   plan.layout = &layout;
   plan.adt = program.find_type(layout.name);
   if (!plan.adt || !plan.adt->is_adt()) throw LayoutError("layout '" + layout.name + "' does not name an ADT");
+  check_layout(program, layout, *plan.adt);
   plan.build_order = program.build_orders.empty() ? "pre" : program.build_orders.back();
   Planner p{plan, layout};
   p.run();
