@@ -81,3 +81,36 @@ def test_gpu_cd_rejects_bad_arguments(built):
         flat.collide_host(q16)
     for t in (wide, flat, q16):
         t.free()
+
+
+def test_sat_against_constructed_pairs(oracle):
+    """SPEC acceptance criterion 9: SAT vs a construction-based overlap oracle on 10^3 pairs, none inside an
+    epsilon-thick boundary band: (a) pairs separated by a gap of at least 0.05 along a random axis, (b) pairs where an
+    edge of the second triangle pierces the first one at an interior point, end points >= 0.05 off its plane."""
+    rng = np.random.default_rng(17)
+    for _ in range(500):
+        a = rng.uniform(-1, 1, (3, 3)).astype(np.float32)
+        b = rng.uniform(-1, 1, (3, 3)).astype(np.float32)
+        axis = rng.normal(size=3)
+        axis /= np.linalg.norm(axis)
+        gap = (a @ axis).max() - (b @ axis).min() + 0.05 + rng.uniform(0, 1)
+        b_far = (b + gap * axis).astype(np.float32)  # every vertex of b_far is beyond every vertex of a along `axis`
+        assert (b_far @ axis).min() - (a @ axis).max() > 0.04
+        assert not oracle.sat(a.reshape(-1), b_far.reshape(-1)) and not oracle.sat(b_far.reshape(-1), a.reshape(-1))
+    for _ in range(500):
+        a = rng.uniform(-1, 1, (3, 3))
+        w = rng.uniform(0.15, 0.7, 3)
+        w /= w.sum()
+        p = w @ a  # interior point of a
+        n = np.cross(a[1] - a[0], a[2] - a[0])
+        if np.linalg.norm(n) < 0.2:
+            continue
+        n /= np.linalg.norm(n)
+        d = n + 0.5 * rng.uniform(-1, 1, 3)
+        d /= np.linalg.norm(d)
+        q0, q1 = p + d * rng.uniform(0.1, 1.0), p - d * rng.uniform(0.1, 1.0)  # the segment q0-q1 passes through p
+        assert abs((q0 - p) @ n) > 0.05 and abs((q1 - p) @ n) > 0.05
+        q2 = q0 + rng.uniform(-1, 1, 3)
+        b = np.stack([q0, q1, q2]).astype(np.float32)
+        a32 = a.astype(np.float32)
+        assert oracle.sat(a32.reshape(-1), b.reshape(-1)) and oracle.sat(b.reshape(-1), a32.reshape(-1))
