@@ -130,7 +130,7 @@ int header_from_ptree(const scion_ptree& p, ImageHeader& h) {
     h.bytes[b] = sz;
     h.count[b] = p.counts[b];
     for (size_t s = 0; s < p.seg_bases[b].size(); s++) h.seg_base[b][s] = p.seg_bases[b][s];
-    off += (sz + 16 + 255) / 256 * 256;
+    off += (sz + 32 + 255) / 256 * 256;  // >= 32 bytes of slack behind every buffer: covering vector loads (scion_rt.cuh load_record, geometry.cuh load_triangle36)
   }
   for (size_t g = 0; g < p.globals.size(); g++) memcpy(h.glob[g], p.globals[g].data(), 16);
   h.root0 = p.root0;

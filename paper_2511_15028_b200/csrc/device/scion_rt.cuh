@@ -34,6 +34,9 @@
 // 1: node records L2 evict_last (±0);  2: 1 + primitives evict_first (+1.7 %);  3: 2 + L1::no_allocate (-3 %).
 #define SCION_CACHE_HINTS 4
 #endif
+#ifndef SCION_LDG_COVER
+#define SCION_LDG_COVER 1
+#endif
 #ifndef SCION_LDG_PARITY
 #define SCION_LDG_PARITY 1
 #endif
@@ -362,8 +365,8 @@ SCION_HOSTDEV void prefetch_to(const void* p) {
 // (ALIGN = gcd of the buffer base alignment, the segment base and the stride, computed by
 // emit_cuda).  16-byte read-only vector loads whenever the plan allows them; 8- and 4-byte
 // loads otherwise; byte-granular strides (pbrt-post 34 B, identity 41 B, shared-slab 29 B) read
-// the covering aligned words and funnel-shift.  Every device buffer is over-allocated by 16
-// bytes so the covering reads stay inside the allocation.
+// the covering aligned 16-byte quads, re-align words and funnel-shift.  Every device buffer is over-allocated by
+// 32 bytes so the covering reads stay inside the allocation.
 template <int BYTES, int ALIGN>
 SCION_HOSTDEV void load_record(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
   constexpr int NW = (BYTES + 3) / 4;
@@ -394,6 +397,33 @@ SCION_HOSTDEV void load_record(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
   } else if constexpr (ALIGN % 4 == 0 && BYTES % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < NW; i++) r.w[i] = ld32(p + 4 * i);
+  } else if constexpr (SCION_LDG_COVER && BYTES > 16) {
+    // byte-granular stride (identity 41 B, pbrt-post 34 B, shared-slab 29 B): the 16-byte-aligned quads that
+    // cover the record (4 instead of 12 loads for identity), word re-alignment by a two-level select, byte
+    // re-alignment by funnel shifts.  The last quad is only read when the record reaches into it, so the read
+    // never goes more than 31 bytes past the record (buffers carry 32 bytes of slack).
+    const uint64_t a = (uint64_t)p;
+    const uint8_t* q = (const uint8_t*)(a & ~15ull);
+    const uint32_t wsh = (uint32_t)(a >> 2) & 3u;
+    const uint32_t bsh = (uint32_t)(a & 3ull) * 8u;
+    constexpr int NR = NW + 1;           // words needed before the funnel shift
+    constexpr int K = (NR + 3 + 3) / 4;  // quads covering words [wsh, wsh + NR)
+    uint32_t w[4 * K + 3];
+#pragma unroll
+    for (int k = 0; k < K - 1; k++) ld128(q + 16 * k, w + 4 * k);
+    w[4 * (K - 1)] = w[4 * (K - 1) + 1] = w[4 * (K - 1) + 2] = w[4 * (K - 1) + 3] = 0u;
+    if (wsh + (uint32_t)NR > 4u * (uint32_t)(K - 1)) ld128(q + 16 * (K - 1), w + 4 * (K - 1));
+    w[4 * K] = w[4 * K + 1] = w[4 * K + 2] = 0u;
+    const bool s1 = (wsh & 1u) != 0u, s2 = (wsh & 2u) != 0u;
+    uint32_t raw[NR];
+#pragma unroll
+    for (int i = 0; i < NR; i++) {
+      const uint32_t lo = s1 ? w[i + 1] : w[i];
+      const uint32_t hi = s1 ? w[i + 3] : w[i + 2];
+      raw[i] = s2 ? hi : lo;
+    }
+#pragma unroll
+    for (int i = 0; i < NW; i++) r.w[i] = funnel_r(raw[i], raw[i + 1], bsh);
   } else {
     const uint64_t a = (uint64_t)p;
     const uint8_t* q = (const uint8_t*)(a & ~3ull);
