@@ -192,8 +192,26 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
 #ifndef SCION_INNER
 #define SCION_INNER 4
 #endif
+#ifndef SCION_PF_TRI
+#define SCION_PF_TRI 0
+#endif
 constexpr bool kPrefetch = SCION_PREFETCH != 0;  // L2-prefetch a node record when its reference is pushed (+3-4 % on C5, binary)
 constexpr int kInner = SCION_INNER;  // node steps between two looks at the warp (idle lanes to refill, lanes waiting with a leaf)
+
+// L2 prefetch of a parked leaf's triangles (SCION_PF_TRI: 1 = the line of the first triangle, 2 = first and last
+// line): the cooperative leaf phase runs a few steps after the lane parks, the prefetch covers that gap.
+template <class L>
+SCION_DEV void prefetch_triangles(const TreeView& T, uint32_t begin, uint32_t end) {
+#if SCION_PF_TRI > 0
+  const uint8_t* p = T.buf[L::kBuf_primitives] + (uint64_t)begin * 36ull;
+  prefetch_to<2>(p);
+#if SCION_PF_TRI > 1
+  prefetch_to<2>(p + (uint64_t)(end - begin) * 36ull - 1ull);
+#endif
+#else
+  (void)T; (void)begin; (void)end;
+#endif
+}
 
 // keeps the result-store address arithmetic inside the (rare) retire branch instead of letting the
 // compiler hoist it into every loop iteration (9 SASS instructions per iteration in v3)
@@ -443,6 +461,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     }
     if (p_prim) {  // park the primitive range (shared memory: the leaf phase reads it, the step keeps no register for it)
       asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(my_leaf), "r"((uint32_t)node.data.begin), "r"((uint32_t)node.data.end));
+      prefetch_triangles<L>(T, (uint32_t)node.data.begin, (uint32_t)node.data.end);
       mode = kPrim;
     } else if (p_push) {
       LS::store(top, node.right);
@@ -806,8 +825,12 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const
         L::decode(T, cur, leaf);  // reference-only arm: no memory access
         prim_i = (uint32_t)leaf.data.begin;
         prim_end = (uint32_t)leaf.data.end;
-        if (prim_i < prim_end) mode = kPrim;
-        else mode = -1;  // empty leaf: nothing to do, take the next entry
+        if (prim_i < prim_end) {
+          mode = kPrim;
+          prefetch_triangles<L>(T, prim_i, prim_end);
+        } else {
+          mode = -1;  // empty leaf: nothing to do, take the next entry
+        }
       }
     }
   };
