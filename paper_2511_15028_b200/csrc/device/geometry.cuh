@@ -217,9 +217,17 @@ SCION_DEV void load_triangle36(const uint8_t* prims, uint64_t index, float (&v)[
 #if SCION_CACHE_HINTS >= 3
   uint4 a, b, c;
   const uint64_t pol = l2_policy_stream();
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(q), "l"(pol));
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(q + 1), "l"(pol));
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "l"(q + 2), "l"(pol));
+#ifndef SCION_L2_PROMO_TRI
+#define SCION_L2_PROMO_TRI 0
+#endif
+#if SCION_L2_PROMO_TRI > 0
+#define SCION_TRI_Q ".L2::" SCION_STR(SCION_L2_PROMO_TRI) "B"
+#else
+#define SCION_TRI_Q ""
+#endif
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint" SCION_TRI_Q ".v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(q), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint" SCION_TRI_Q ".v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(q + 1), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint" SCION_TRI_Q ".v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w) : "l"(q + 2), "l"(pol));
 #elif SCION_CACHE_HINTS >= 2
   uint4 a, b, c;
   const uint64_t pol = l2_policy_stream();

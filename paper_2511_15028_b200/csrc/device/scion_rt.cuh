@@ -322,8 +322,23 @@ SCION_HOSTDEV void ld64(const uint8_t* p, uint32_t* o) {
 __device__ __forceinline__ uint64_t l2_policy_keep() { uint64_t p; asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p)); return p; }
 __device__ __forceinline__ uint64_t l2_policy_stream() { uint64_t p; asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p; }
 #endif
+// SCION_L2_PROMO (0 | 64 | 128 | 256): L2 sector promotion of node-record loads — a miss fetches the whole 64 / 128 /
+// 256-byte block into L2, so a left descent through a cold stretch of the preorder array pays one DRAM access per block
+// instead of one per 32-byte sector.
+#ifndef SCION_L2_PROMO
+#define SCION_L2_PROMO 0
+#endif
+#define SCION_STR2(x) #x
+#define SCION_STR(x) SCION_STR2(x)
+#if SCION_L2_PROMO > 0
+#define SCION_PROMO_Q ".L2::" SCION_STR(SCION_L2_PROMO) "B"
+#else
+#define SCION_PROMO_Q ""
+#endif
 SCION_HOSTDEV void ld128(const uint8_t* p, uint32_t* o) {
-#if defined(__CUDA_ARCH__) && (SCION_CACHE_HINTS == 1 || SCION_CACHE_HINTS == 2 || SCION_CACHE_HINTS == 3)
+#if defined(__CUDA_ARCH__) && SCION_L2_PROMO > 0
+  asm volatile("ld.global.nc" SCION_PROMO_Q ".v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p));
+#elif defined(__CUDA_ARCH__) && (SCION_CACHE_HINTS == 1 || SCION_CACHE_HINTS == 2 || SCION_CACHE_HINTS == 3)
   asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p), "l"(l2_policy_keep()));
 #elif defined(__CUDA_ARCH__)
   uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
@@ -336,7 +351,7 @@ SCION_HOSTDEV void ld128(const uint8_t* p, uint32_t* o) {
 // the f32 layouts are L1-tag-bound (profiles/r1_ncu_v8_c5_pbrt.txt: l1tex throughput 98 %)
 SCION_HOSTDEV void ld256(const uint8_t* p, uint32_t* o) {
 #if defined(__CUDA_ARCH__)
-  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile("ld.global.nc" SCION_PROMO_Q ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7])
                : "l"(p));
 #else
