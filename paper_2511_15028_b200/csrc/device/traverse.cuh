@@ -195,6 +195,9 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
 #ifndef SCION_PF_TRI
 #define SCION_PF_TRI 0
 #endif
+#ifndef SCION_PF8
+#define SCION_PF8 0
+#endif
 constexpr bool kPrefetch = SCION_PREFETCH != 0;  // L2-prefetch a node record when its reference is pushed (+3-4 % on C5, binary)
 constexpr int kInner = SCION_INNER;  // node steps between two looks at the warp (idle lanes to refill, lanes waiting with a leaf)
 
@@ -908,6 +911,19 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const
         }
       }
     }
+#if SCION_PF8 == 1  // L2-prefetch the record of the entry that pops first (the second passing slot)
+    if (rest) {
+      Ref second = node.children[1];
+#pragma unroll
+      for (int k = 7; k >= 1; k--)
+        if ((rest >> k) & 1u) second = node.children[k];
+      L::prefetch(T, second);
+    }
+#elif SCION_PF8 == 2  // ... of every pushed entry
+#pragma unroll
+    for (int k = 1; k < 8; k++)
+      if ((rest >> k) & 1u) L::prefetch(T, node.children[k]);
+#endif
     top += (m - 1u) * LS::kSlot;
     Ref first = node.children[0];
 #pragma unroll

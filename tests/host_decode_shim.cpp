@@ -4,6 +4,7 @@
 #include <cstring>
 #include <string>
 
+#include "device/geometry.cuh"
 #include "gen/bvh8.cuh"
 #include "gen/bvh8_q16.cuh"
 #include "gen/bvh8_q16_ci.cuh"
@@ -80,6 +81,71 @@ extern "C" int host_decode2(const char* layout, const TreeView* T, uint64_t ref,
 extern "C" int host_decode8(const char* layout, const TreeView* T, uint64_t ref, float* f, uint64_t* u) {
   std::string n = layout;
 #define L8(NAME, T_) if (n == NAME) return dec8<g::T_>(T, ref, f, u);
+  L8("bvh8", L_bvh8) L8("bvh8-q8", L_bvh8_q8) L8("bvh8-q8-ci", L_bvh8_q8_ci) L8("bvh8-q16", L_bvh8_q16) L8("bvh8-q16-ci", L_bvh8_q16_ci)
+#undef L8
+  return -1;
+}
+// ---- emitted-code differential (SPEC acceptance 8): closest_hit on the HOST through the generated
+// decoders and the product's geometry header — a plain recursive restatement of chrt.scion / chrt8.scion /
+// chrt_dop14.scion, nothing shared with the kernels' state machines.  TEST-ONLY.
+struct Hit { float t; uint32_t prim; };
+template <class L> void leaf_tris(const TreeView& T, const scion::RayCtx& ray, uint64_t b, uint64_t e, Hit& best) {
+  for (uint64_t i = b; i < e; i++) {
+    float tri[9];
+    std::memcpy(tri, T.buf[L::kBuf_primitives] + i * 36ull, 36);
+    float t;
+    if (scion::ray_tri_mt(ray, tri, t) && t < best.t) best = Hit{t, (uint32_t)i};
+  }
+}
+template <class L> void visit2(const TreeView& T, const scion::RayCtx& ray, const typename L::Ref& ref, Hit& best) {
+  typename L::Node n{};
+  L::decode(T, ref, n);
+  float tn, tf;
+  bool hit;
+  if constexpr (L::kFamily == 1) {
+    bool some = scion::ray_aabb(ray, n.lo1, n.hi1, tn, tf);
+    if (some) { L::decode_cold(T, ref, n); some = scion::dop_diagonals(ray, n.lo2, n.hi2, tn, tf); }
+    hit = scion::interval_intersects(ray, some, tn, tf);
+  } else {
+    const bool some = scion::ray_aabb(ray, n.low, n.high, tn, tf);
+    hit = scion::interval_intersects(ray, some, tn, tf);
+    if (hit) L::decode_cold(T, ref, n);
+  }
+  if (!hit) return;
+  if (n.variant == L::kLeaf) { leaf_tris<L>(T, ray, n.data.begin, n.data.end, best); return; }
+  if (!(tn < best.t)) return;
+  visit2<L>(T, ray, n.left, best);
+  visit2<L>(T, ray, n.right, best);
+}
+template <class L> void visit8(const TreeView& T, const scion::RayCtx& ray, const typename L::Ref& ref, Hit& best) {
+  typename L::Node n{};
+  L::decode(T, ref, n);
+  if (n.variant == L::kLeaf) { leaf_tris<L>(T, ray, n.data.begin, n.data.end, best); return; }
+  for (int k = 0; k < 8; k++) {
+    float tn, tf;
+    const bool some = scion::ray_aabb(ray, n.lo[k], n.hi[k], tn, tf);
+    if (scion::interval_intersects(ray, some, tn, tf) && tn < best.t) visit8<L>(T, ray, n.children[k], best);
+  }
+}
+template <class L, bool WIDE> int run_chrt(const TreeView* T, const float* rays8, uint64_t nrays, Hit* out) {
+  for (uint64_t q = 0; q < nrays; q++) {
+    const float* r = rays8 + 8 * q;
+    const scion::RayCtx ray = scion::make_ray(r[0], r[1], r[2], r[3], r[4], r[5], r[6]);
+    Hit best{scion::inf(), 0xFFFFFFFFu};
+    if constexpr (WIDE) visit8<L>(*T, ray, L::root(*T), best);
+    else visit2<L>(*T, ray, L::root(*T), best);
+    out[q] = best;
+  }
+  return 0;
+}
+extern "C" int host_closest_hit(const char* layout, const TreeView* T, const float* rays8, uint64_t nrays, void* hits) {
+  std::string n = layout;
+  Hit* out = (Hit*)hits;
+#define L2(NAME, T_) if (n == NAME) return run_chrt<g::T_, false>(T, rays8, nrays, out);
+  L2("pbrt", L_pbrt) L2("pbrt-align16", L_pbrt_align16) L2("pbrt-soa", L_pbrt_soa) L2("pbrt-post", L_pbrt_post) L2("pbrt-q16", L_pbrt_q16)
+  L2("sg-eq", L_sg_eq) L2("sg-eq-align16", L_sg_eq_align16) L2("ptr", L_ptr) L2("identity", L_identity) L2("shared-slab", L_shared_slab) L2("dop14", L_dop14)
+#undef L2
+#define L8(NAME, T_) if (n == NAME) return run_chrt<g::T_, true>(T, rays8, nrays, out);
   L8("bvh8", L_bvh8) L8("bvh8-q8", L_bvh8_q8) L8("bvh8-q8-ci", L_bvh8_q8_ci) L8("bvh8-q16", L_bvh8_q16) L8("bvh8-q16-ci", L_bvh8_q16_ci)
 #undef L8
   return -1;

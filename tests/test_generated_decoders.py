@@ -99,3 +99,27 @@ def test_generated_decoders_match_oracle(built, oracle, shim):
                         if wn["child"][k] != built.W_SENTINEL:
                             stack.append(int(u1[3 + k]))
             assert visited == len(lt.wnodes()) + len(lt.wleaves()), name
+
+
+def test_emitted_code_differential(built, oracle, shim):
+    """SPEC acceptance 8 ("emitted-C differential"), for the CUDA backend: the emitted per-layout
+    headers, compiled by the HOST compiler, drive a plain recursive closest_hit (tests/host_decode_shim.cpp) —
+    same chosen primitive and bitwise-equal t as the oracle for 1,024 primary + 1,024 incoherent rays, all 16
+    layouts (the SPEC asks for 2 layouts and 1 ulp)."""
+    shim.host_closest_hit.argtypes = [C.c_char_p, C.POINTER(TreeView), C.c_void_p, C.c_uint64, C.c_void_p]
+    scene = built.Scene.terrain(20, 5)
+    lt = scene.build_sah(32, 4).collapse8()
+    lo, hi = scene.bounds()
+    cam = built.default_camera(lo, hi, True, 32, 32)
+    rays = np.concatenate([built.gen_primary_host(cam, 0, 1024), built.gen_secondary_host(lt.triangles(), 9, 0, 1024)])
+    flat = np.ascontiguousarray(rays).view(np.float32).reshape(-1, 8)
+    for l in built.layouts():
+        name = l["name"]
+        pt = lt.encode(name)
+        tb, tv = oracle.tree_bytes(pt), make_view(pt)
+        want, _ = oracle.closest_hit(tb, rays)
+        got = np.zeros(len(rays), built.HIT_DTYPE)
+        assert shim.host_closest_hit(name.encode(), C.byref(tv), flat.ctypes.data, len(rays), got.ctypes.data) == 0, name
+        assert np.array_equal(got["prim"], want["prim"]), name
+        assert np.array_equal(got["t"].view(np.uint32), want["t"].view(np.uint32)), name
+        assert (got["prim"] != built.MISS_PRIM).sum() > 256, name
