@@ -198,6 +198,12 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
 #ifndef SCION_PF8
 #define SCION_PF8 0
 #endif
+#ifndef SCION_CPQ_PFY
+#define SCION_CPQ_PFY 0
+#endif
+#ifndef SCION_CPQ_BOTH
+#define SCION_CPQ_BOTH -1  // -1: per layout (records fetched by ONE vector load), 0: never, 1: always
+#endif
 constexpr bool kPrefetch = SCION_PREFETCH != 0;  // L2-prefetch a node record when its reference is pushed (+3-4 % on C5, binary)
 constexpr int kInner = SCION_INNER;  // node steps between two looks at the warp (idle lanes to refill, lanes waiting with a leaf)
 
@@ -1152,11 +1158,18 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
         return;
       }
     }
-    Node nx;
-    const float dx = cpq_node_distmin<L>(T, p, rx, nx, tally);
-    if (go) {
-      Node ny;
-      const float dy = cpq_node_distmin<L>(T, p, ry, ny, tally);
+#if SCION_CPQ_PFY > 0  // start the (far) right child's fetch before the left child's record is awaited: the compiler keeps
+    // the Y load inside the `go` branch, behind X's load + decode (profiles/r1_ncu_v11_c4_q16.txt: 24 % of the stall samples)
+    if (go) L::template prefetch<SCION_CPQ_PFY>(T, ry);
+#endif
+    // Both decode slots unconditional where the record is ONE vector load (pbrt, pbrt-align16, pbrt-q16, sg-eq-align16):
+    // a popping lane decodes its X record twice (same address, no extra sector).  The Y instructions are issued for the
+    // warp anyway as soon as one lane descends, and without the `go` branch around them the Y load is in flight together
+    // with the X load instead of behind X's decode (r1_ncu_v11_c4_q16.txt: 24 % of the stall samples sat on that second,
+    // serialised load): C4 pbrt-q16 1305 -> 1389, pbrt 1253 -> 1427 Mq/s.  Multi-load records lose (pbrt-soa -14 %,
+    // pbrt-post -16 %, ptr -6 %, identity -11 %, dop14 -11 %, sg-eq -3 %): they keep the branch.
+    constexpr bool kBoth = SCION_CPQ_BOTH < 0 ? (L::kCanStage && !L::kHasCold) : (SCION_CPQ_BOTH != 0);
+    auto descend = [&](const Node& nx, float dx, const Node& ny, float dy) {
       const bool left_first = dx < dy;  // ties: the right child is visited first (cpq.scion:17 `L < R`)
       const Ref far = left_first ? ry : rx;
       if (rel < LS::kSmemBytes) LS::store(top, far);
@@ -1165,11 +1178,35 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
       if (left_first) { node = nx; d = dx; cur = rx; }
       else { node = ny; d = dy; cur = ry; }
       carried = true;
-    } else {
+    };
+    auto stay = [&](const Node& nx, float dx) {
       node = nx;
       d = dx;
       cur = rx;
       carried = false;
+    };
+    Node nx;
+    if constexpr (kBoth) {
+      Node ny;
+      Tally<false> quiet;
+      const float dx = cpq_node_distmin<L>(T, p, rx, nx, quiet);
+      const float dy = cpq_node_distmin<L>(T, p, go ? ry : rx, ny, quiet);
+      if (COUNT) {
+        const uint32_t k = go ? 2u : 1u;
+        tally.node_visits += k;
+        if (L::kHasCold) tally.cold_loads += k;
+      }
+      if (go) descend(nx, dx, ny, dy);
+      else stay(nx, dx);
+    } else {
+      const float dx = cpq_node_distmin<L>(T, p, rx, nx, tally);
+      if (go) {
+        Node ny;
+        const float dy = cpq_node_distmin<L>(T, p, ry, ny, tally);
+        descend(nx, dx, ny, dy);
+      } else {
+        stay(nx, dx);
+      }
     }
     mode = kNode;
   };
