@@ -155,13 +155,20 @@ SCION_DEV RayCtx load_ray(const scion_ray* rays, uint64_t q) {
 
 // bounds test of one binary / DOP node against the ray.  Loads the cold segment only when the
 // reference semantics would evaluate it (dop.scion:20-21 `if I {...}`).
+// SCION_COLD_EAGER: fetch the cold segment together with the hot one instead of after the hot test.  The loads are pure
+// (any node index is a valid address in every segment), so only the timing changes: one dependent memory round trip
+// per passing node instead of two.  The counters still count a cold load only where the reference evaluates it.
+#ifndef SCION_COLD_EAGER
+#define SCION_COLD_EAGER 0
+#endif
 template <class L, class TallyT>
 SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L::Ref& ref, typename L::Node& n, float& t_near, TallyT& tally) {
   float t_far;
+  if constexpr (L::kHasCold && SCION_COLD_EAGER != 0) L::decode_cold(T, ref, n);
   if constexpr (L::kFamily == SCION_FAMILY_DOP14) {
     bool some = ray_aabb(ray, n.lo1, n.hi1, t_near, t_far);
     if (some) {
-      L::decode_cold(T, ref, n);
+      if constexpr (SCION_COLD_EAGER == 0) L::decode_cold(T, ref, n);
       tally.cold();
       some = dop_diagonals(ray, n.lo2, n.hi2, t_near, t_far);
     }
@@ -171,7 +178,7 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
     const bool hit = interval_intersects(ray, some, t_near, t_far);
     if constexpr (L::kHasCold) {
       if (hit) {
-        L::decode_cold(T, ref, n);
+        if constexpr (SCION_COLD_EAGER == 0) L::decode_cold(T, ref, n);
         tally.cold();
       }
     }
