@@ -34,7 +34,9 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5")
     ap.add_argument("--layout", default="pbrt-q16", help="headline layout (the paper's Pareto-optimal layout)")
-    ap.add_argument("--sweep", default="pbrt,pbrt-soa,sg-eq,bvh8,bvh8-q8-ci", help="extra layouts reported in `layouts` (at every N); '' disables")
+    ap.add_argument("--sweep", default="all", help="extra layouts reported in `layouts` (at every N): comma list, '' disables, 'all' = every corpus layout "
+                    "except shared-slab (one slab per node: ~2600 node visits per ray on a terrain, minutes per step at this size; "
+                    "it is measured in profiles/r1_all_layouts_*.csv at 1 M triangles)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink query counts (debug)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -318,7 +320,8 @@ def main():
     peak, peak_src = measured_peak()
     results = {}
     # the sweep runs at every N: BASELINE's metric is Mrays/s *per layout* at 1/2/4/8 GPUs (same code path as the headline)
-    layouts = [args.layout] + [l for l in args.sweep.split(",") if l and l != args.layout]
+    sweep = [l["name"] for l in sb.layouts() if l["name"] != "shared-slab"] if args.sweep == "all" else args.sweep.split(",")
+    layouts = [args.layout] + [l for l in sweep if l and l != args.layout]
     if wl.algorithm != "chrt":  # closest point is defined for the binary families only (cpq.scion, cpq_dop14.scion)
         cpq_ok = {l["name"] for l in sb.layouts() if l["has_cpq"]}
         layouts = [l for l in layouts if l in cpq_ok or l == args.layout]
