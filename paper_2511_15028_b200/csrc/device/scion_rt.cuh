@@ -37,6 +37,9 @@
 #ifndef SCION_LDG_COVER
 #define SCION_LDG_COVER 1
 #endif
+#ifndef SCION_I2F_MAGIC
+#define SCION_I2F_MAGIC 0
+#endif
 #ifndef SCION_LDG_PARITY
 #define SCION_LDG_PARITY 1
 #endif
@@ -235,7 +238,15 @@ SCION_VEC_RD2(fdiv_rd)
 // `e as T` value cast (sema.cpp:753-770); `e to T` equal-width bit cast (:771-786)
 template <class To> struct as_impl;
 template <> struct as_impl<float> {
-  SCION_HOSTDEV static float go(uint32_t x) { return (float)x; }
+  // SCION_I2F_MAGIC: integers below 2^23 convert exactly as bits(0x4B000000 | x) - 2^23 — one logic op and one FADD on
+  // the full-rate pipes instead of one I2F on the quarter-rate conversion unit; the range test folds away when the
+  // compiler knows the operand is a narrow bit field (every quantised layout), the value is identical.
+  SCION_HOSTDEV static float go(uint32_t x) {
+#if defined(__CUDA_ARCH__) && SCION_I2F_MAGIC
+    if (x < 0x800000u) return __uint_as_float(0x4B000000u | x) - 8388608.0f;
+#endif
+    return (float)x;
+  }
   SCION_HOSTDEV static float go(int32_t x) { return (float)x; }
   SCION_HOSTDEV static float go(uint64_t x) { return (float)x; }
   SCION_HOSTDEV static float go(float x) { return x; }
