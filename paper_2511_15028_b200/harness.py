@@ -1,9 +1,13 @@
-"""Command-line harness of the B200 backend — the slice of the reference CLI (`layoutc check | footprint |
-compile --emit-c | bench`) that belongs to the traversal path.
+"""Command-line harness of the B200 backend — the reference CLI's sub-commands (`check`, `compile`, `build-tree`,
+`build`, `run`, `verify`, `footprint`, `bench`) for the traversal path.
 
   python -m paper_2511_15028_b200.harness check                      # every registered layout plans + emits
   python -m paper_2511_15028_b200.harness footprint --layout L --scene terrain:224
   python -m paper_2511_15028_b200.harness emit-cuda --layout L [-o file]
+  python -m paper_2511_15028_b200.harness compile file.scion [--plan plan.json] [--emit-cuda out.cuh]   # a user-written layout
+  python -m paper_2511_15028_b200.harness build-tree --scene terrain:224 [--builder sah|median] -o tree.npz  # Scene -> LogicalTree
+  python -m paper_2511_15028_b200.harness build --layout L (--tree tree.npz | --scene terrain:224) -o tree.scionpt   # -> PhysicalTree container
+  python -m paper_2511_15028_b200.harness run tree.scionpt --alg chrt|cpq --queries N --rays primary|secondary [-o results.bin]  # container -> results
   python -m paper_2511_15028_b200.harness bench --layout L[,L2..] --alg chrt|cpq --scene terrain:708 --queries 4194304 --rays secondary
   python -m paper_2511_15028_b200.harness bench --layout L[,L2..] --alg cd --scene terrain:224 [--builder median|sah]   # --queries = output capacity
 
@@ -110,6 +114,102 @@ def cmd_bench_cd(a):
     return 0
 
 
+def cmd_compile(a):
+    """`compile`: a .scion layout file -> memory plan (JSON) + the CUDA device header emit_cuda produces for it."""
+    try:
+        src = open(a.file).read()
+    except OSError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 2
+    plan, cuda = sb.compile_layout_text(src)  # diagnostics surface as ScionError -> exit code 1
+    if a.plan:
+        json.dump(plan, open(a.plan, "w"), indent=1)
+    if a.emit_cuda:
+        open(a.emit_cuda, "w").write(cuda)
+    node = [b for b in plan["buffers"] if b["name"] == plan["node_group"]]
+    print(json.dumps({"layout": plan.get("layout"), "node_group": plan["node_group"], "node_stride": sum(x["stride_bytes"] for x in node[0]["segments"]) if node else 0,
+                      "buffers": len(plan["buffers"]), "slots": len(plan["slots"]), "cuda_bytes": len(cuda)}))
+    return 0
+
+
+def build_logical(a):
+    scene = parse_scene(a.scene)
+    lt = scene.build_median(a.max_leaf) if a.builder == "median" else scene.build_sah(32, a.max_leaf)
+    return lt
+
+
+def cmd_build_tree(a):
+    """`build-tree`: Scene -> LogicalTree, stored as the two arrays scion_ltree_from_arrays takes back."""
+    lt = build_logical(a)
+    np.savez(a.output, nodes=lt.nodes(), triangles=lt.triangles())
+    print(json.dumps({"scene": a.scene, "builder": a.builder, "nodes": lt.nnodes, "primitives": lt.nprims, "depth": lt.depth}))
+    return 0
+
+
+def cmd_build(a):
+    """`build`: LogicalTree -> PhysicalTree in the chosen layout, written as the versioned container file
+    (header with magic, version, layout name, global slots + raw little-endian buffers)."""
+    if a.tree:
+        z = np.load(a.tree)
+        lt = sb.LogicalTree.from_arrays(z["nodes"], z["triangles"])
+    else:
+        lt = build_logical(a)
+    if sb.layout_info(a.layout)["family"] == 2:
+        lt.collapse8()
+    pt = lt.encode(a.layout)
+    pt.save(a.output)
+    print(json.dumps({"layout": a.layout, "primitives": lt.nprims, "total_bytes": pt.total_bytes, "node_bytes": pt.node_bytes, "file": a.output}))
+    return 0
+
+
+def cmd_run(a):
+    """`run`: reads a PhysicalTree container file, uploads it, generates the queries on the device from (seed, index),
+    runs them and writes the raw result records (scion_hit / scion_cp, query order) plus a JSON report."""
+    import torch
+    if not torch.cuda.is_available():
+        print("run needs a CUDA device (no CPU fallback)", file=sys.stderr)
+        return 1
+    pt = sb.PhysicalTree.load(a.file)
+    prim = [b for b in pt.buffers() if b["name"] == "primitives"][0]
+    tris = np.asarray(prim["data"]).view(np.float32).reshape(-1, 3)
+    lo, hi = tris.min(axis=0), tris.max(axis=0)
+    dt = pt.upload(0)
+    n, dev = a.queries, "cuda:0"
+    seed = sb.seed_from_env(a.seed)
+    d_st = torch.zeros(n, dtype=torch.int32, device=dev)
+    d_ctr = torch.zeros(n * 4, dtype=torch.int32, device=dev)
+    if a.alg == "chrt":
+        d_q = torch.empty(n * 32, dtype=torch.uint8, device=dev)
+        d_r = torch.empty(n * 8, dtype=torch.uint8, device=dev)
+        if a.rays == "primary":
+            side = int(np.sqrt(n))
+            n = side * side
+            sb.gen_primary(sb.default_camera(lo, hi, a.look_down_y, side, side), 0, n, d_q.data_ptr())
+        else:
+            dt.gen_secondary(seed, 0, n, d_q.data_ptr())
+        dt.closest_hit(d_q.data_ptr(), n, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+        torch.cuda.synchronize()
+        res = d_r.cpu().numpy()[:n * 8].view(sb.HIT_DTYPE)
+        found = int((res["prim"] != sb.MISS_PRIM).sum())
+    else:
+        d_q = torch.empty(n * 12, dtype=torch.uint8, device=dev)
+        d_r = torch.empty(n * 20, dtype=torch.uint8, device=dev)
+        sb.gen_points(lo, hi, seed, 0, n, d_q.data_ptr())
+        dt.closest_point(d_q.data_ptr(), n, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+        torch.cuda.synchronize()
+        res = d_r.cpu().numpy().view(sb.CP_DTYPE)
+        found = int((res["prim"] != sb.MISS_PRIM).sum())
+    errors = int((d_st[:n] != 0).sum())
+    c = d_ctr.view(-1, 4)[:n].sum(dim=0, dtype=torch.int64).cpu().numpy()
+    if a.output:
+        res.tofile(a.output)
+    import zlib
+    print(json.dumps({"layout": pt.layout, "algorithm": a.alg, "queries": n, "kind": a.rays if a.alg == "chrt" else "points", "seed": seed, "found": found,
+                      "query_errors": errors, "node_visits": int(c[0]), "prim_tests": int(c[1]), "crc32": zlib.crc32(res.tobytes()), "results": a.output}))
+    dt.free()
+    return 1 if errors else 0
+
+
 def cmd_bench(a):
     import torch
     if not torch.cuda.is_available():
@@ -183,6 +283,27 @@ def main(argv=None):
     p = sub.add_parser("emit-cuda")
     p.add_argument("--layout", required=True)
     p.add_argument("-o", "--output")
+    p = sub.add_parser("compile")
+    p.add_argument("file")
+    p.add_argument("--plan")
+    p.add_argument("--emit-cuda")
+    for name in ("build-tree", "build"):
+        p = sub.add_parser(name)
+        p.add_argument("--scene", default="terrain:64")
+        p.add_argument("--builder", default="sah", choices=["sah", "median"])
+        p.add_argument("--max-leaf", type=int, default=4)
+        p.add_argument("-o", "--output", required=True)
+        if name == "build":
+            p.add_argument("--layout", required=True)
+            p.add_argument("--tree", help="LogicalTree written by build-tree (otherwise built from --scene)")
+    p = sub.add_parser("run")
+    p.add_argument("file")
+    p.add_argument("--alg", default="chrt", choices=["chrt", "cpq"])
+    p.add_argument("--queries", type=int, default=1 << 16)
+    p.add_argument("--rays", default="primary", choices=["primary", "secondary"])
+    p.add_argument("--look-down-y", action="store_true", help="primary camera above the +y face (terrains) instead of the +z face")
+    p.add_argument("--seed", type=int, default=7)
+    p.add_argument("-o", "--output")
     p = sub.add_parser("bench")
     p.add_argument("--layout", required=True)
     p.add_argument("--alg", default="chrt", choices=["chrt", "cpq", "cd"])
@@ -199,7 +320,8 @@ def main(argv=None):
         ap.print_usage(sys.stderr)
         return 2
     try:
-        return {"check": cmd_check, "footprint": cmd_footprint, "emit-cuda": cmd_emit, "bench": cmd_bench}[a.cmd](a)
+        return {"check": cmd_check, "footprint": cmd_footprint, "emit-cuda": cmd_emit, "bench": cmd_bench, "compile": cmd_compile,
+                "build-tree": cmd_build_tree, "build": cmd_build, "run": cmd_run}[a.cmd](a)
     except sb.ScionError as e:
         print(f"error: {e}", file=sys.stderr)
         return 2 if e.code == sb.ERR_ARG else 1

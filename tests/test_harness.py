@@ -94,3 +94,51 @@ def test_native_harness_bench(built):
         head, row = r.stdout.strip().splitlines()
         rec = dict(zip(head.split(","), row.split(",")))
         assert rec["layout"] == args[0] and float(rec["mqueries_per_s"]) > 0 and int(rec["query_errors"]) == 0 and float(rec["node_visits"]) > 0
+
+
+def test_compile_build_tree_build(built, tmp_path):
+    """compile / build-tree / build: the host-side sub-commands either side of the traversal path."""
+    src = os.path.join(ROOT, "paper_2511_15028_b200", "layouts", "pbrt_q16.scion")
+    cuh, plan = str(tmp_path / "q16.cuh"), str(tmp_path / "q16.json")
+    rc, out = run(["compile", src, "--plan", plan, "--emit-cuda", cuh])
+    rep = json.loads(out)
+    assert rc == 0 and rep["node_stride"] == 16
+    assert "static_assert(sizeof(Record_" in open(cuh).read() and json.load(open(plan))["node_group"] == rep["node_group"]
+    bad = tmp_path / "bad.scion"
+    bad.write_text("type BVH(low: f32x3) = Interior(left: BVH) | Leaf(n: u8); layout BVH(I: u32) { group g[align = 3] by I { low: f32x3; }; };")
+    assert run(["compile", str(bad)])[0] == 1  # diagnostics class
+    assert run(["compile", str(tmp_path / "missing.scion")])[0] == 2
+    tree = str(tmp_path / "tree.npz")
+    rc, out = run(["build-tree", "--scene", "terrain:16", "-o", tree])
+    assert rc == 0 and json.loads(out)["primitives"] == 512
+    for layout in ("pbrt-q16", "bvh8-q8-ci", "shared-slab"):
+        f1, f2 = str(tmp_path / f"{layout}.a.scionpt"), str(tmp_path / f"{layout}.b.scionpt")
+        rc, out = run(["build", "--layout", layout, "--tree", tree, "-o", f1])
+        assert rc == 0 and json.loads(out)["primitives"] == 512
+        assert run(["build", "--layout", layout, "--scene", "terrain:16", "-o", f2])[0] == 0
+        assert open(f1, "rb").read() == open(f2, "rb").read(), layout  # deterministic, and the .npz round trip loses nothing
+        pt = built.PhysicalTree.load(f1)
+        want = built.Scene.terrain(16, 1).build_sah(32, 4).collapse8().encode(layout)
+        assert pt.layout == layout and pt.total_bytes == want.total_bytes
+        for b, w in zip(pt.buffers(), want.buffers()):
+            assert b["name"] == w["name"] and bytes(b["data"]) == bytes(w["data"]), (layout, b["name"])
+
+
+@pytest.mark.gpu
+def test_run_container_file(built, oracle, tmp_path):
+    """run: container file -> results; equal to the oracle on the same generated queries."""
+    import numpy as np
+    f, out_bin = str(tmp_path / "t.scionpt"), str(tmp_path / "hits.bin")
+    assert run(["build", "--layout", "pbrt-q16", "--scene", "terrain:24", "-o", f])[0] == 0
+    rc, out = run(["run", f, "--alg", "chrt", "--queries", "4096", "--rays", "secondary", "--seed", "11", "-o", out_bin])
+    rep = json.loads(out)
+    assert rc == 0 and rep["query_errors"] == 0 and rep["queries"] == 4096 and rep["found"] > 500
+    pt = built.PhysicalTree.load(f)
+    lt = built.Scene.terrain(24, 1).build_sah(32, 4)
+    rays = built.gen_secondary_host(lt.triangles(), 11, 0, 4096)
+    want, _ = oracle.closest_hit(oracle.tree_bytes(pt), rays)
+    got = np.fromfile(out_bin, built.HIT_DTYPE)
+    assert np.array_equal(got["prim"], want["prim"]) and np.array_equal(got["t"].view(np.uint32), want["t"].view(np.uint32))
+    rc, out = run(["run", f, "--alg", "cpq", "--queries", "2048"])
+    rep = json.loads(out)
+    assert rc == 0 and rep["found"] == 2048 and rep["query_errors"] == 0
