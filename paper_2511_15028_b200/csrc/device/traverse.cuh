@@ -1067,7 +1067,7 @@ SCION_DEV uint32_t coop_points2(const TreeView& T, bool own, const f32x3& p, uin
 #define SCION_PRIM_MINC 6
 #endif
 #ifndef SCION_INNERC
-#define SCION_INNERC 4
+#define SCION_INNERC 8  // 4 -> 8 after v13: +1 % (pbrt-q16 1388 -> 1401, pbrt 1424 -> 1439), >= 0 on every other binary layout
 #endif
 // closest_point kernel v7.  The reference decodes a node three times on the way down: as the
 // child peek of its parent (cpq.scion:9-16), again when it is visited, and its own two children.
