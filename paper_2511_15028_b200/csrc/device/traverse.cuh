@@ -186,7 +186,13 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
   }
 }
 
-enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes
+enum : int { kFetch = 0, kNode = 1, kPrim = 2, kDone = 4 };  // lane modes (3 = kPop of the closest-point kernel)
+// SCION_DEFER_RETIRE: a lane whose stack runs empty only marks itself kDone; the result stores (~23 instructions that ran
+// for ONE lane at a time: 3.4 % of all warp instructions in profiles/r1_ncu_v11_c5_q16.txt) happen at the next refill,
+// for all finished lanes of the warp together.
+#ifndef SCION_DEFER_RETIRE
+#define SCION_DEFER_RETIRE 0
+#endif
 #ifndef SCION_PREFETCH
 #define SCION_PREFETCH 1
 #endif
@@ -432,7 +438,11 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
       LS::load(top, cur);
       mode = kNode;
     } else if (rel < LS::kSlot) {  // empty: the query is done
+#if SCION_DEFER_RETIRE
+      mode = kDone;
+#else
       retire(SCION_Q_OK);
+#endif
     } else {
       top -= LS::kSlot;
       cur = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
@@ -505,8 +515,15 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
       if (mode == kNode) step();
     }
     // ---- FETCH: refill idle lanes
+#if SCION_DEFER_RETIRE
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch || mode == kDone);
+#else
     const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+#endif
     if (idle && (__popc(idle) >= kRefillMin || work.exhausted)) {
+#if SCION_DEFER_RETIRE
+      if (mode == kDone) retire(SCION_Q_OK);
+#endif
       uint64_t nq;
       if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
         ray = load_ray(rays, nq);
