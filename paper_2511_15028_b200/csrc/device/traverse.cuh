@@ -45,7 +45,10 @@ namespace scion {
 // 2178, 10 KB 2183, 8 KB 2176, 6 KB 1979, 4 KB 1747 Mrays/s (small windows send pushes to local memory).
 #define SCION_STACK_SMEM (12 * 1024)
 #endif
-constexpr int kBlockThreads = 128;
+#ifndef SCION_BLOCK_THREADS
+#define SCION_BLOCK_THREADS 128
+#endif
+constexpr int kBlockThreads = SCION_BLOCK_THREADS;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kChunk = SCION_CHUNK;     // queries a warp takes from the global counter at a time
 #ifndef SCION_STREAM_HITS
