@@ -557,6 +557,185 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
 }
 
 // ------------------------------------------------------------------------------------------
+// closest_hit, binary family, TWO rays per lane (kernel v14, SCION_DUAL=1) — for layouts whose record is one vector load
+// (L::kCanFetch: pbrt, pbrt-align16, pbrt-q16, sg-eq-align16).
+//
+// chrt2_kernel is bound by the dependent chain of one step (pop -> address -> record load -> decode -> test -> push/pop)
+// times the visits of a ray, with the register file fixing how many chains an SM holds.  Here every lane
+// owns two independent rays ("slots").  A step of slot s consumes the record that was fetched at the END of slot s's
+// previous step and ends by issuing the fetch of its next record (emitted L::fetch / L::decode_fetched), so the load of
+// one slot is in flight while the other slot's step executes.  Everything else is the v11 machine run once per slot:
+// same visit order, same predicated push/pop, same cooperative leaf phase, same results bit for bit.  The
+// counter-instrumented build stays on chrt2_kernel (identical results by construction, tests compare the two).
+// ------------------------------------------------------------------------------------------
+#ifndef SCION_DUAL
+#define SCION_DUAL 0
+#endif
+#ifndef SCION_MINB2D
+#define SCION_MINB2D 7
+#endif
+#ifndef SCION_STACK_SMEM_D  /* shared-memory stack window of one CTA, both slots together */
+#define SCION_STACK_SMEM_D (16 * 1024)
+#endif
+template <class L>
+constexpr bool dual_ok() {
+  return L::kCanFetch && !L::kHasCold && L::kFamily != SCION_FAMILY_DOP14 && std::is_integral<typename L::Ref>::value;
+}
+template <class L>
+__global__ void __launch_bounds__(kBlockThreads, SCION_MINB2D) chrt2d_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
+                                                                scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
+                                                                scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
+  using Ref = typename L::Ref;
+  constexpr int kSlotWindow = SCION_STACK_SMEM_D / 2;
+  using LS = LaneStack<Ref, kSlotWindow>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ CoopScratch2 coop[kBlockThreads / 32];
+  __shared__ RayStash stash[2][kBlockThreads];
+  __shared__ unsigned long long stash_q[2][kBlockThreads];
+  __shared__ uint2 stash_leaf[2][kBlockThreads];
+  Ref deep[2][LS::kDeep];
+  uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  asm volatile("" : "+r"(window));
+  (void)tune; (void)counters;
+  WorkFetcher work;
+  struct Slot {
+    RayCtx ray;
+    float best_t;
+    uint32_t best_prim;
+    Ref cur;
+    uint32_t top;
+    int mode;
+    typename L::Fetched rec;
+  } S[2];
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    S[s].ray = make_ray(0, 0, 0, 0, 1, 1, 1);
+    S[s].best_t = 0;
+    S[s].best_prim = 0;
+    S[s].cur = L::root(T);
+    S[s].top = window + (uint32_t)s * (uint32_t)kSlotWindow + threadIdx.x * 4u;
+    S[s].mode = kFetch;
+  }
+
+  auto retire = [&](auto SI, uint32_t st) {
+    constexpr int s = decltype(SI)::value;
+    const uint64_t qq = opaque(stash_q[s][threadIdx.x]);
+    store_hit(hits + qq, S[s].best_t, S[s].best_prim);
+    if (status) status[qq] = st;
+    S[s].mode = kFetch;
+  };
+  auto pop_or_retire = [&](auto SI) {
+    constexpr int s = decltype(SI)::value;
+    const uint32_t rel = S[s].top - (window + (uint32_t)s * (uint32_t)kSlotWindow);
+    if (rel - LS::kSlot < LS::kSmemBytes) {
+      S[s].top -= LS::kSlot;
+      LS::load(S[s].top, S[s].cur);
+      S[s].mode = kNode;
+    } else if (rel < LS::kSlot) {
+      retire(SI, SCION_Q_OK);
+    } else {
+      S[s].top -= LS::kSlot;
+      S[s].cur = deep[s][rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+      S[s].mode = kNode;
+    }
+  };
+  // one node step of slot s; ends by putting the next record's load in flight
+  auto step = [&](auto SI) {
+    constexpr int s = decltype(SI)::value;
+    Slot& X = S[s];
+    typename L::Node node;
+    L::decode_fetched(T, X.cur, X.rec, node);
+    float t_near, t_far;
+    const bool some = ray_aabb(X.ray, node.low, node.high, t_near, t_far);
+    const bool hit = interval_intersects(X.ray, some, t_near, t_far);
+    const bool leaf = node.variant == L::kLeaf;
+    const bool p_prim = hit && leaf && (uint32_t)node.data.begin < (uint32_t)node.data.end;
+    const bool p_push = hit && !leaf && t_near < X.best_t;
+    const uint32_t rel = X.top - (window + (uint32_t)s * (uint32_t)kSlotWindow);
+    const bool fast = p_push ? rel < LS::kSmemBytes : rel - LS::kSlot < LS::kSmemBytes;
+    if (!(fast || p_prim)) {
+      if (p_push) {
+        const uint32_t depth = rel / LS::kSlot;
+        if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
+          retire(SI, SCION_Q_STACK_OVERFLOW);
+        } else {
+          deep[s][depth - (uint32_t)LS::kSmem] = node.right;
+          X.top += LS::kSlot;
+          X.cur = node.left;
+        }
+      } else {
+        pop_or_retire(SI);
+      }
+    } else if (p_prim) {
+      const uint32_t my_leaf = (uint32_t)__cvta_generic_to_shared(&stash_leaf[s][threadIdx.x]);
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(my_leaf), "r"((uint32_t)node.data.begin), "r"((uint32_t)node.data.end));
+      X.mode = kPrim;
+    } else if (p_push) {
+      LS::store(X.top, node.right);
+      if constexpr (kPrefetch) L::prefetch(T, node.right);
+      X.top += LS::kSlot;
+      X.cur = node.left;
+    } else {
+      X.top -= LS::kSlot;
+      LS::load(X.top, X.cur);
+    }
+    if (X.mode == kNode) L::fetch(T, X.cur, X.rec);
+  };
+  auto refill = [&](auto SI) {
+    constexpr int s = decltype(SI)::value;
+    Slot& X = S[s];
+    const unsigned idle = __ballot_sync(kFullMask, X.mode == kFetch);
+    if (idle && (__popc(idle) >= kRefillMin || work.exhausted)) {
+      uint64_t nq;
+      if (!work.exhausted && work.refill(X.mode == kFetch, next, n, nq)) {
+        X.ray = load_ray(rays, nq);
+        stash[s][threadIdx.x] = RayStash{X.ray.dx, X.ray.dy, X.ray.dz, 0u};
+        stash_q[s][threadIdx.x] = nq;
+        X.best_t = scion::inf();
+        X.best_prim = SCION_MISS_PRIM;
+        X.top = window + (uint32_t)s * (uint32_t)kSlotWindow + threadIdx.x * 4u;
+        X.cur = L::root(T);
+        X.mode = kNode;
+        L::fetch(T, X.cur, X.rec);
+      }
+    }
+  };
+  auto prims = [&](auto SI, bool nothing_else) {
+    constexpr int s = decltype(SI)::value;
+    Slot& X = S[s];
+    const unsigned pmask = __ballot_sync(kFullMask, X.mode == kPrim);
+    if (pmask && (__popc(pmask) >= kPrimMin || nothing_else)) {
+      const bool own = X.mode == kPrim;
+      uint2 range = make_uint2(0u, 0u);
+      if (own) range = stash_leaf[s][threadIdx.x];
+      uint32_t prim_i = range.x;
+      coop_triangles2<L>(T, own, X.ray.ox, X.ray.oy, X.ray.oz, X.ray.tmax, stash[s] + (threadIdx.x & ~31u), prim_i, range.y, X.best_t, X.best_prim,
+                         coop[threadIdx.x >> 5]);
+      if (own) {
+        pop_or_retire(SI);
+        if (X.mode == kNode) L::fetch(T, X.cur, X.rec);
+      }
+    }
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+
+  for (;;) {
+#pragma unroll 1
+    for (int k = 0; k < kInner; k++) {
+      if (S[0].mode == kNode) step(I0{});
+      if (S[1].mode == kNode) step(I1{});
+    }
+    refill(I0{});
+    refill(I1{});
+    if (work.exhausted && __ballot_sync(kFullMask, S[0].mode != kFetch || S[1].mode != kFetch) == 0u) break;
+    const bool nothing_else = __ballot_sync(kFullMask, S[0].mode == kNode || S[1].mode == kNode) == 0u;
+    prims(I0{}, nothing_else);
+    prims(I1{}, nothing_else);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // closest_hit, binary family, PAIR step (kernel v10) — for layouts whose reference is a plain
 // integer and whose node has no cold segment.
 //

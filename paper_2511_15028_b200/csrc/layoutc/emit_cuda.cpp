@@ -631,10 +631,24 @@ struct Emitter {
     out << "  static constexpr bool kCanStage = " << (can_stage ? "true" : "false") << ";  // first records may be staged in shared memory\n";
     out << "  static constexpr uint32_t kStageStride = " << (can_stage ? primary_buf->segments[0].stride_bytes : 0) << "u;\n";
     out << "  static constexpr int kStageBuffer = " << (can_stage ? primary_buf->id : 0) << ";\n";
+    // split form of decode() for single-segment records fetched by one vector load: fetch() issues the load, decode_fetched()
+    // consumes the words later — lets a kernel keep a record in flight while it works on something else
+    const bool can_fetch = can_stage && !has_cold;
+    out << "  static constexpr bool kCanFetch = " << (can_fetch ? "true" : "false") << ";  // fetch() + decode_fetched() == decode()\n";
+    if (can_fetch) {
+      const Buffer& b = *primary_buf;
+      const uint64_t bytes = b.segments[0].stride_bytes;
+      std::string index_expr = ref_is_struct ? "ref__." + primary->index_binding : std::string("ref__");
+      out << "  using Fetched = scion::Words<" << (bytes + 3) / 4 << ">;\n";
+      out << "  SCION_HOSTDEV static void fetch(const scion::TreeView& tree__, const Ref& ref__, Fetched& w_0) {\n";
+      out << "    scion::load_record<" << bytes << ", " << gcd_align(b, 0) << ">(tree__.buf[" << b.id << "] + (uint64_t)(" << index_expr << ") * " << bytes << "ull, w_0);\n";
+      out << "  }\n";
+    }
     auto emit_decode = [&](const char* name, Mode mode) {
       const bool main = std::string(name) == "decode";
+      const bool fetched = std::string(name) == "decode_fetched";
       if (main) out << "  template <bool STAGED = false>\n";
-      out << "  SCION_HOSTDEV static void " << name << "(const scion::TreeView& tree__, const Ref& ref__, Node& node__"
+      out << "  SCION_HOSTDEV static void " << name << "(const scion::TreeView& tree__, const Ref& ref__, " << (fetched ? "const Fetched& w_0, " : "") << "Node& node__"
           << (main ? ", const scion::Stage& stage__ = scion::Stage()" : "") << ") {\n";
       // globals referenced by layout expressions
       std::set<std::string> ids;
@@ -653,7 +667,7 @@ struct Emitter {
         if (ids.count(plan.globals[g].name) && !plan.globals[g].inferred)
           out << "    const " << ctype(plan.globals[g].type) << " " << plan.globals[g].name << " = scion::glob<" << ctype(plan.globals[g].type) << ">(tree__, " << g << ");\n";
       std::string index_expr = ref_is_struct ? "ref__." + primary->index_binding : std::string("ref__");
-      if (primary_buf && !primary_buf->segments.empty()) emit_record_loads(*primary_buf, index_expr, "", 2, mode == Mode::Hot, main && can_stage);
+      if (primary_buf && !primary_buf->segments.empty() && !fetched) emit_record_loads(*primary_buf, index_expr, "", 2, mode == Mode::Hot, main && can_stage);
       emit_members(primary->members, primary_buf, "", 2, mode, {}, {}, nullptr, false);
       out << "  }\n";
     };
@@ -662,6 +676,7 @@ struct Emitter {
       emit_decode("decode_cold", Mode::Cold);
     } else {
       emit_decode("decode", Mode::All);
+      if (can_fetch) emit_decode("decode_fetched", Mode::All);
       out << "  SCION_HOSTDEV static void decode_cold(const scion::TreeView&, const Ref&, Node&) {}\n";
     }
     // prefetch(): pull the record a reference designates into L2 ahead of its visit (issued by the

@@ -38,6 +38,14 @@ template <class L> int dec2(const TreeView* T, uint64_t ref, const float* carrie
   auto r = make_ref<typename L::Ref>(ref, carried);
   L::decode(*T, r, n);
   L::decode_cold(*T, r, n);
+  if constexpr (L::kCanFetch) {  // split form: fetch() + decode_fetched() must be decode()
+    typename L::Fetched w;
+    typename L::Node m{};
+    L::fetch(*T, r, w);
+    L::decode_fetched(*T, r, w, m);
+    if (m.variant != n.variant || std::memcmp(&m.low, &n.low, sizeof(n.low)) != 0 || std::memcmp(&m.high, &n.high, sizeof(n.high)) != 0) return 3;
+    if (n.variant == L::kLeaf ? (m.data.begin != n.data.begin || m.data.end != n.data.end) : (ref_id(m.left) != ref_id(n.left) || ref_id(m.right) != ref_id(n.right))) return 3;
+  }
   std::memset(f, 0, 20 * sizeof(float));
   if constexpr (L::kFamily == 1) {
     float v[14] = {n.lo1.x, n.lo1.y, n.lo1.z, n.hi1.x, n.hi1.y, n.hi1.z, n.lo2.x, n.lo2.y, n.lo2.z, n.lo2.w, n.hi2.x, n.hi2.y, n.hi2.z, n.hi2.w};

@@ -252,6 +252,27 @@ def test_staged_prefix_variant_is_identical(built, torch_cuda, world):
         dt.free()
 
 
+def test_two_rays_per_lane_variant_is_identical(built, torch_cuda, world):
+    """experimental kernel variant 3 (two rays per lane, the next record's load of one ray in flight while the other
+    ray's step executes; emitted fetch() / decode_fetched()) must return exactly the default kernel's records and
+    per-query status"""
+    sb, torch = built, torch_cuda
+    n = world["rays"].shape[0]
+    d_rays = dev_bytes(torch, world["rays"])
+    for layout in ("pbrt", "pbrt-q16"):
+        dt = world["lt"].encode(layout).upload(0)
+        a = torch.zeros(n * 8, dtype=torch.uint8, device="cuda:0")
+        b = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+        sa = torch.full((n,), 7, dtype=torch.int32, device="cuda:0")
+        sb_ = torch.full((n,), 9, dtype=torch.int32, device="cuda:0")
+        dt.closest_hit(d_rays.data_ptr(), n, a.data_ptr(), sa.data_ptr())
+        dt.closest_hit(d_rays.data_ptr(), n, b.data_ptr(), sb_.data_ptr(), variant=3)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), layout
+        assert torch.equal(sa, sb_), layout
+        dt.free()
+
+
 def test_fault_injection_changes_results(built, oracle, torch_cuda, world):
     """corrupting one c_o byte must surface as >= 1 mismatch against the oracle of the intact tree"""
     sb = built
