@@ -572,7 +572,10 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
 #define SCION_DUAL 0
 #endif
 #ifndef SCION_MINB2D
-#define SCION_MINB2D 7
+#define SCION_MINB2D 6
+#endif
+#ifndef SCION_DUAL_MERGED
+#define SCION_DUAL_MERGED 0
 #endif
 #ifndef SCION_STACK_SMEM_D  /* shared-memory stack window of one CTA, both slots together */
 #define SCION_STACK_SMEM_D (16 * 1024)
@@ -681,11 +684,11 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2D) chrt2d_kernel(con
     }
     if (X.mode == kNode) L::fetch(T, X.cur, X.rec);
   };
-  auto refill = [&](auto SI) {
+  auto refill = [&](auto SI, bool force) {
     constexpr int s = decltype(SI)::value;
     Slot& X = S[s];
     const unsigned idle = __ballot_sync(kFullMask, X.mode == kFetch);
-    if (idle && (__popc(idle) >= kRefillMin || work.exhausted)) {
+    if (idle && (force || __popc(idle) >= kRefillMin || work.exhausted)) {
       uint64_t nq;
       if (!work.exhausted && work.refill(X.mode == kFetch, next, n, nq)) {
         X.ray = load_ray(rays, nq);
@@ -726,10 +729,18 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2D) chrt2d_kernel(con
       if (S[0].mode == kNode) step(I0{});
       if (S[1].mode == kNode) step(I1{});
     }
-    refill(I0{});
-    refill(I1{});
+#if SCION_DUAL_MERGED  // thresholds on the two slots of the warp together (a slot's own events are half as frequent)
+    const bool many_idle = __popc(__ballot_sync(kFullMask, S[0].mode == kFetch)) + __popc(__ballot_sync(kFullMask, S[1].mode == kFetch)) >= kRefillMin;
+#else
+    const bool many_idle = false;
+#endif
+    refill(I0{}, many_idle);
+    refill(I1{}, many_idle);
     if (work.exhausted && __ballot_sync(kFullMask, S[0].mode != kFetch || S[1].mode != kFetch) == 0u) break;
-    const bool nothing_else = __ballot_sync(kFullMask, S[0].mode == kNode || S[1].mode == kNode) == 0u;
+    bool nothing_else = __ballot_sync(kFullMask, S[0].mode == kNode || S[1].mode == kNode) == 0u;
+#if SCION_DUAL_MERGED
+    nothing_else = nothing_else || __popc(__ballot_sync(kFullMask, S[0].mode == kPrim)) + __popc(__ballot_sync(kFullMask, S[1].mode == kPrim)) >= kPrimMin;
+#endif
     prims(I0{}, nothing_else);
     prims(I1{}, nothing_else);
   }
