@@ -393,6 +393,24 @@ SCION_HOSTDEV void prefetch_to(const void* p) {
 // loads otherwise; byte-granular strides (pbrt-post 34 B, identity 41 B, shared-slab 29 B) read
 // the covering aligned 16-byte quads, re-align words and funnel-shift.  Every device buffer is over-allocated by
 // 32 bytes so the covering reads stay inside the allocation.
+// load_record for the records of the *cold* part of a tree (experiment SCION_HOT_L1, traverse.cuh): same bytes, but the
+// line is not allocated in L1, so that the few thousand records of the top levels stay there.  Only for records that
+// are one 16- or 32-byte vector load.
+template <int BYTES, int ALIGN>
+SCION_HOSTDEV void load_record_na(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
+  static_assert((BYTES == 16 && ALIGN % 16 == 0) || (BYTES == 32 && ALIGN % 32 == 0), "single vector load records only");
+#if defined(__CUDA_ARCH__)
+  if constexpr (BYTES == 16) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]) : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7])
+                 : "l"(p));
+  }
+#else
+  memcpy(r.w, p, BYTES);
+#endif
+}
 template <int BYTES, int ALIGN>
 SCION_HOSTDEV void load_record(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
   constexpr int NW = (BYTES + 3) / 4;

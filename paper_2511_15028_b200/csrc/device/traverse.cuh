@@ -214,6 +214,13 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2, kDone = 4 };  // lane modes (3 = 
 #ifndef SCION_PF8
 #define SCION_PF8 0
 #endif
+// SCION_HOT_L1 = N > 0 (binary kernel, single-vector-load layouts with a 32-bit index reference): records of subtrees with
+// fewer than N nodes are fetched with L1::no_allocate, so that the top of the tree (a few thousand records) stays in L1
+// instead of being evicted by the cold bottom levels (L1 hit rate 15.8 %).  The "hot" flag travels in bit 31 of the
+// reference (children inherit it from the size of their parent's left subtree, c_offset).
+#ifndef SCION_HOT_L1
+#define SCION_HOT_L1 0
+#endif
 #ifndef SCION_CPQ_PFY
 #define SCION_CPQ_PFY 0
 #endif
@@ -453,9 +460,28 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     }
   };
 
+  constexpr bool kHot = SCION_HOT_L1 > 0 && STAGE == 0 && L::kCanFetch && !L::kHasCold && std::is_same<Ref, uint32_t>::value;
+  constexpr uint32_t kHotBit = 0x80000000u;
   auto step = [&]() {
     typename L::Node node;
-    L::template decode<(STAGE > 0)>(T, cur, node, stage);
+    uint32_t child_flag = 0u;
+    auto tagged = [&](const Ref& r) -> Ref {  // the child reference with the hot flag of this node's children
+      if constexpr (kHot) return (Ref)(r | (Ref)child_flag);
+      else return r;
+    };
+    if constexpr (kHot) {
+      const Ref idx = (Ref)((uint32_t)cur & ~kHotBit);
+      typename L::Fetched w;
+      if ((uint32_t)cur & kHotBit) L::template fetch<false>(T, idx, w);
+      else L::template fetch<true>(T, idx, w);
+      L::decode_fetched(T, idx, w, node);
+      if (node.variant != L::kLeaf) {
+        child_flag = (uint32_t)(node.right - idx) >= (uint32_t)SCION_HOT_L1 ? kHotBit : 0u;
+      }
+      cur = idx;
+    } else {
+      L::template decode<(STAGE > 0)>(T, cur, node, stage);
+    }
 #if SCION_PF_NEXT == 1
     if constexpr (std::is_integral<Ref>::value) L::template prefetch<1>(T, (Ref)(cur + 1));
 #elif SCION_PF_NEXT > 1  // L2 prefetch SCION_PF_NEXT records ahead in the (preorder) array
@@ -479,9 +505,9 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
         if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
           retire(SCION_Q_STACK_OVERFLOW);
         } else {
-          deep[depth - (uint32_t)LS::kSmem] = node.right;
+          deep[depth - (uint32_t)LS::kSmem] = tagged(node.right);
           top += LS::kSlot;
-          cur = node.left;
+          cur = tagged(node.left);
         }
       } else {
         pop_or_retire();
@@ -493,7 +519,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
       prefetch_triangles<L>(T, (uint32_t)node.data.begin, (uint32_t)node.data.end);
       mode = kPrim;
     } else if (p_push) {
-      LS::store(top, node.right);
+      LS::store(top, tagged(node.right));
       if constexpr (kPrefetch) {
         // L2-prefetch the pushed child, but only when it is far: a right sibling a few records away shares
         // its lines with what this lane just fetched, and every prefetch costs an L1 tag lookup per lane
@@ -504,7 +530,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
         }
       }
       top += LS::kSlot;
-      cur = node.left;
+      cur = tagged(node.left);
     } else {
       top -= LS::kSlot;
       LS::load(top, cur);
@@ -537,6 +563,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
         tally.reset();
         top = window + threadIdx.x * 4u;
         cur = L::root(T);
+        if constexpr (kHot) cur = (Ref)((uint32_t)cur | kHotBit);
         mode = kNode;
       }
       if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;

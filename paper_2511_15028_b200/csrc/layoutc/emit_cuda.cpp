@@ -640,8 +640,16 @@ struct Emitter {
       const uint64_t bytes = b.segments[0].stride_bytes;
       std::string index_expr = ref_is_struct ? "ref__." + primary->index_binding : std::string("ref__");
       out << "  using Fetched = scion::Words<" << (bytes + 3) / 4 << ">;\n";
+      const bool one_vector = (bytes == 16 && gcd_align(b, 0) % 16 == 0) || (bytes == 32 && gcd_align(b, 0) % 32 == 0);
+      out << "  template <bool COLD = false>  // COLD: do not allocate the line in L1\n";
       out << "  SCION_HOSTDEV static void fetch(const scion::TreeView& tree__, const Ref& ref__, Fetched& w_0) {\n";
-      out << "    scion::load_record<" << bytes << ", " << gcd_align(b, 0) << ">(tree__.buf[" << b.id << "] + (uint64_t)(" << index_expr << ") * " << bytes << "ull, w_0);\n";
+      out << "    const uint8_t* p__ = tree__.buf[" << b.id << "] + (uint64_t)(" << index_expr << ") * " << bytes << "ull;\n";
+      if (one_vector) {
+        out << "    if constexpr (COLD) scion::load_record_na<" << bytes << ", " << gcd_align(b, 0) << ">(p__, w_0);\n";
+        out << "    else scion::load_record<" << bytes << ", " << gcd_align(b, 0) << ">(p__, w_0);\n";
+      } else {
+        out << "    scion::load_record<" << bytes << ", " << gcd_align(b, 0) << ">(p__, w_0);\n";
+      }
       out << "  }\n";
     }
     auto emit_decode = [&](const char* name, Mode mode) {
