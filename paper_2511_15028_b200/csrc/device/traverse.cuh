@@ -1300,6 +1300,22 @@ SCION_DEV uint32_t coop_points2(const TreeView& T, bool own, const f32x3& p, uin
 #ifndef SCION_MINBC
 #define SCION_MINBC 6
 #endif
+// SCION_CPQ_STORE_D: a pushed far child carries the distance its parent's peek computed (8-byte stack entries for 32-bit
+// references).  The reference decodes a popped node, computes the same (pure) distance and skips the node unless it is
+// < best[0]; with the distance on the stack that cull needs no record: culled entries cost one LDS.64 instead of a step
+// with a dependent load.  The instrumented build still counts the decode the reference performs.
+#ifndef SCION_CPQ_STORE_D
+#define SCION_CPQ_STORE_D 0
+#endif
+#ifndef SCION_STACK_SMEM_C  /* shared-memory stack window of one closest-point CTA */
+#define SCION_STACK_SMEM_C SCION_STACK_SMEM
+#endif
+constexpr int kStackSmemBytesPerBlockC = SCION_STACK_SMEM_C;
+template <class Ref>
+struct CpqEntryD {
+  Ref ref;
+  float d;
+};
 #ifndef SCION_PRIM_MINC
 #define SCION_PRIM_MINC 6
 #endif
@@ -1323,13 +1339,19 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   using Node = typename L::Node;
-  using LS = LaneStack<Ref>;
+  constexpr bool kStoreD = SCION_CPQ_STORE_D != 0 && std::is_integral<Ref>::value;
+  using Entry = typename std::conditional<kStoreD, CpqEntryD<Ref>, Ref>::type;
+  using LS = LaneStack<Entry, kStackSmemBytesPerBlockC>;
   enum : int { kPop = 3 };  // stepping lanes: kNode (record + distance of `node` are valid) or kPop (take the next pending reference first)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CoopScratchCp2 coop[kBlockThreads / 32];
   __shared__ float4 best_pt[kBlockThreads];
   __shared__ unsigned long long stash_q[kBlockThreads];
-  Ref deep[LS::kDeep];
+  Entry deep[LS::kDeep];
+  auto make_entry = [](const Ref& r, float dist) -> Entry {
+    if constexpr (kStoreD) return Entry{r, dist};
+    else return r;
+  };
   uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
   asm volatile("" : "+r"(window));
   uint32_t top = window + threadIdx.x * 4u;
@@ -1384,15 +1406,38 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
     }
     const uint32_t rel = top - window;
     if (!go) {  // pop the next pending reference, or retire
-      if (rel - LS::kSlot < LS::kSmemBytes) {
-        top -= LS::kSlot;
-        LS::load(top, rx);
-      } else if (rel < LS::kSlot) {
-        retire(SCION_Q_OK);
-        return;
+      if constexpr (kStoreD) {
+        for (;;) {
+          const uint32_t r2 = top - window;
+          Entry e;
+          if (r2 - LS::kSlot < LS::kSmemBytes) {
+            top -= LS::kSlot;
+            LS::load(top, e);
+          } else if (r2 < LS::kSlot) {
+            retire(SCION_Q_OK);
+            return;
+          } else {
+            top -= LS::kSlot;
+            e = deep[r2 / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+          }
+          if (e.d < best_d) {
+            rx = e.ref;
+            break;
+          }
+          tally.visit();  // culled without its record: the reference decodes the node, then skips it (cpq.scion:5)
+          if (L::kHasCold) tally.cold();
+        }
       } else {
-        top -= LS::kSlot;
-        rx = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+        if (rel - LS::kSlot < LS::kSmemBytes) {
+          top -= LS::kSlot;
+          LS::load(top, rx);
+        } else if (rel < LS::kSlot) {
+          retire(SCION_Q_OK);
+          return;
+        } else {
+          top -= LS::kSlot;
+          rx = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+        }
       }
     } else {
       const uint32_t depth = rel / LS::kSlot;
@@ -1415,7 +1460,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
     constexpr bool kBoth = SCION_CPQ_BOTH < 0 ? (L::kCanStage && !L::kHasCold) : (SCION_CPQ_BOTH != 0);
     auto descend = [&](const Node& nx, float dx, const Node& ny, float dy) {
       const bool left_first = dx < dy;  // ties: the right child is visited first (cpq.scion:17 `L < R`)
-      const Ref far = left_first ? ry : rx;
+      const Entry far = make_entry(left_first ? ry : rx, left_first ? dy : dx);
       if (rel < LS::kSmemBytes) LS::store(top, far);
       else deep[rel / LS::kSlot - (uint32_t)LS::kSmem] = far;
       top += LS::kSlot;
@@ -1470,7 +1515,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
         best_d = scion::inf();
         tally.reset();
         top = window + threadIdx.x * 4u;
-        LS::store(top, root);  // the root is "popped" by the first step
+        LS::store(top, make_entry(root, 0.0f));  // the root is "popped" by the first step (0 < inf: never culled there)
         top += LS::kSlot;
         mode = kPop;
       }
