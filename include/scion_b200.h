@@ -216,6 +216,36 @@ uint64_t scion_ptree_node_bytes(const scion_ptree* p);  /* all buffers except pr
  * name, global slots) + raw little-endian buffers"; read by the `run` subcommand) */
 int scion_ptree_save(const scion_ptree* p, const char* path);
 int scion_ptree_load(const char* path, scion_ptree** out);
+/* In-memory import of a PhysicalTree produced by another build_physical (one descriptor per
+ * BufferDesc / GlobalDesc of the MemoryPlan, /root/reference/proj/include/layoutc/plan.hpp:31-48).  Descriptors
+ * are matched by name, in any order; the library copies, the caller keeps ownership.  Sizes are validated against
+ * the plan (buffer bytes == footprint() for the stated count, /root/reference/proj/src/plan.cpp:333-347; segment
+ * bases; root reference inside the node group); anything else is SCION_ERR_ARG, never a silent upload. */
+typedef struct scion_buffer_desc {
+  const char* name;          /* plan buffer name: "primitives", "nodes", "Interiors", "node" (arena) ... */
+  const void* data;
+  uint64_t bytes;
+  uint64_t count;            /* elements (arena: nodes allocated in it; not checked against the bytes) */
+  const uint64_t* seg_bases; /* nullable: byte offset of every segment; must equal the plan's if given */
+  uint32_t n_seg_bases;
+} scion_buffer_desc;
+typedef struct scion_global_desc {
+  const char* name;          /* plan global slot name: "world_low", "N", "__ref_plo" ... */
+  uint8_t raw[16];           /* little-endian bits, zero padded */
+} scion_global_desc;
+typedef struct scion_tree_desc {
+  const char* layout;
+  const scion_buffer_desc* buffers;
+  uint32_t nbuffers;
+  const scion_global_desc* globals;
+  uint32_t nglobals;
+  uint64_t root_ref;         /* primary component of the root reference */
+  float carried[6];          /* tree-carried components (shared-slab: plo, phi), else zeros */
+  uint64_t nprims;           /* 0 = take the primitives buffer's count */
+} scion_tree_desc;
+int scion_ptree_from_buffers(const scion_tree_desc* desc, scion_ptree** out);
+/* import + upload in one call (the host descriptor stays the caller's) */
+int scion_tree_upload(const scion_tree_desc* host, int device, scion_dtree** out);
 /* fault injection for verify tests: xor one byte of a buffer */
 int scion_ptree_corrupt(scion_ptree* p, int buffer, uint64_t byte_offset, uint8_t xor_mask);
 void scion_ptree_free(scion_ptree* p);

@@ -46,6 +46,19 @@ class LayoutInfo(C.Structure):
                 ("n_segments", C.c_uint32), ("ref_bits", C.c_uint32), ("max_leaf", C.c_uint32), ("has_cpq", C.c_int)]
 
 
+class BufferDesc(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("data", C.c_void_p), ("bytes", C.c_uint64), ("count", C.c_uint64), ("seg_bases", C.POINTER(C.c_uint64)), ("n_seg_bases", C.c_uint32)]
+
+
+class GlobalDesc(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("raw", C.c_uint8 * 16)]
+
+
+class TreeDesc(C.Structure):
+    _fields_ = [("layout", C.c_char_p), ("buffers", C.POINTER(BufferDesc)), ("nbuffers", C.c_uint32), ("globals", C.POINTER(GlobalDesc)), ("nglobals", C.c_uint32),
+                ("root_ref", C.c_uint64), ("carried", C.c_float * 6), ("nprims", C.c_uint64)]
+
+
 class CdStats(C.Structure):
     _fields_ = [("node_pairs", C.c_uint64), ("tri_tests", C.c_uint64), ("levels", C.c_uint64), ("max_frontier", C.c_uint64)]
 
@@ -121,6 +134,8 @@ def lib() -> C.CDLL:
         "scion_ptree_corrupt": (i32, [vp, i32, u64, C.c_uint8]),
         "scion_ptree_save": (i32, [vp, cp]),
         "scion_ptree_load": (i32, [cp, P(vp)]),
+        "scion_ptree_from_buffers": (i32, [P(TreeDesc), P(vp)]),
+        "scion_tree_upload": (i32, [P(TreeDesc), i32, P(vp)]),
         "scion_ptree_free": (None, [vp]),
         "scion_device_count": (i32, [P(i32)]),
         "scion_dtree_upload": (i32, [vp, i32, P(vp)]),
@@ -411,6 +426,54 @@ class PhysicalTree:
         _check(lib().scion_ptree_load(path.encode(), C.byref(h)))
         return PhysicalTree(h)
 
+    @staticmethod
+    def _desc(layout: str, buffers, globals_, root_ref: int, carried=None, nprims: int = 0):
+        """TreeDesc for scion_ptree_from_buffers: buffers = [{name, data (uint8 array), count, seg_bases?}], globals_ = [{name, raw}]."""
+        keep = []
+        bd = (BufferDesc * max(1, len(buffers)))()
+        for i, b in enumerate(buffers):
+            data = np.ascontiguousarray(b["data"], dtype=np.uint8)
+            keep.append(data)
+            bd[i].name = b["name"].encode()
+            bd[i].data = data.ctypes.data if data.size else None
+            bd[i].bytes = b.get("bytes", data.size)
+            bd[i].count = b.get("count", 0)
+            sb_ = b.get("seg_bases")
+            if sb_ is not None:
+                arr = (C.c_uint64 * max(1, len(sb_)))(*sb_)
+                keep.append(arr)
+                bd[i].seg_bases = arr
+                bd[i].n_seg_bases = len(sb_)
+        gd = (GlobalDesc * max(1, len(globals_)))()
+        for i, g in enumerate(globals_):
+            gd[i].name = g["name"].encode()
+            raw = bytes(g["raw"])[:16].ljust(16, b"\0")
+            for k in range(16):
+                gd[i].raw[k] = raw[k]
+        d = TreeDesc()
+        d.layout = layout.encode()
+        d.buffers, d.nbuffers = bd, len(buffers)
+        d.globals, d.nglobals = gd, len(globals_)
+        d.root_ref = root_ref
+        for k in range(6):
+            d.carried[k] = float(carried[k]) if carried is not None else 0.0
+        d.nprims = nprims
+        d._keep = (keep, bd, gd)
+        return d
+
+    @staticmethod
+    def from_buffers(layout: str, buffers, globals_, root_ref: int, carried=None, nprims: int = 0) -> "PhysicalTree":
+        """In-memory import of a PhysicalTree built elsewhere (validated against the plan; the library copies)."""
+        d = PhysicalTree._desc(layout, buffers, globals_, root_ref, carried, nprims)
+        h = C.c_void_p()
+        _check(lib().scion_ptree_from_buffers(C.byref(d), C.byref(h)))
+        return PhysicalTree(h)
+
+    def export(self):
+        """(layout, buffers, globals, root_ref, carried) — the arguments from_buffers() takes."""
+        r0, carried = self.root()
+        return self.layout, [dict(name=b["name"], data=b["data"], count=b["count"], seg_bases=b["seg_bases"]) for b in self.buffers()], self.globals(), r0, carried
+
     def corrupt(self, buffer: int, byte_offset: int, xor_mask: int = 0xFF):
         _check(lib().scion_ptree_corrupt(self._h, buffer, byte_offset, xor_mask))
 
@@ -438,6 +501,14 @@ class PhysicalTree:
         if getattr(self, "_h", None) and _lib is not None:
             _lib.scion_ptree_free(self._h)
             self._h = None
+
+
+def tree_upload(layout: str, buffers, globals_, root_ref: int, carried=None, device: int = 0) -> "DeviceTree":
+    """scion_tree_upload: in-memory import + upload in one call."""
+    d = PhysicalTree._desc(layout, buffers, globals_, root_ref, carried)
+    h = C.c_void_p()
+    _check(lib().scion_tree_upload(C.byref(d), device, C.byref(h)))
+    return DeviceTree(h, device)
 
 
 def device_count() -> int:

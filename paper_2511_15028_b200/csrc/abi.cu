@@ -74,7 +74,75 @@ struct ImageHeader {
 };
 static_assert(sizeof(ImageHeader) % 16 == 0, "image header must keep 16-byte alignment");
 constexpr uint64_t kHeaderBytes = (sizeof(ImageHeader) + 255) / 256 * 256;
-constexpr int kCounterSlots = 64;
+constexpr int kCounterBlock = 64;  // work-fetch counters are allocated in blocks of this many
+
+// One work-fetch counter per LAUNCH IN FLIGHT.  A slot is handed out again only after the event
+// recorded behind the launch that used it has completed, so no launch — on any stream, from any host
+// thread — can zero or share the counter of a kernel that is still running; the pool grows when every
+// slot is busy (concurrent queries on a shared immutable tree).
+struct CounterSlot {
+  unsigned long long* ctr = nullptr;
+  cudaEvent_t done = nullptr;  // recorded on the launch stream right behind the kernel
+  bool pending = false;        // handed out, event not recorded yet
+};
+struct CounterPool {
+  std::mutex mu;
+  std::vector<CounterSlot> slots;
+  std::vector<void*> blocks;
+  size_t cursor = 0;
+  cudaError_t grow() {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, kCounterBlock * sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    blocks.push_back(p);
+    for (int i = 0; i < kCounterBlock; i++) {
+      CounterSlot s;
+      s.ctr = (unsigned long long*)p + i;
+      e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+      slots.push_back(s);
+    }
+    return cudaSuccess;
+  }
+  // index of a slot no live kernel uses; marks it pending
+  cudaError_t take(size_t* out, unsigned long long** ctr) {
+    std::lock_guard<std::mutex> lock(mu);
+    for (int pass = 0; pass < 2; pass++) {
+      const size_t n = slots.size();
+      for (size_t k = 0; k < n; k++) {
+        const size_t i = (cursor + k) % n;
+        CounterSlot& s = slots[i];
+        if (s.pending) continue;
+        const cudaError_t q = cudaEventQuery(s.done);
+        if (q == cudaSuccess) {
+          s.pending = true;
+          cursor = (i + 1) % n;
+          *out = i;
+          *ctr = s.ctr;
+          return cudaSuccess;
+        }
+        if (q != cudaErrorNotReady) return q;
+      }
+      cursor = n;  // first slot of the new block
+      const cudaError_t e = grow();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaErrorUnknown;
+  }
+  // the launch (or its failure) is behind us: record the guard event on its stream
+  cudaError_t release(size_t i, cudaStream_t stream, bool launched) {
+    std::lock_guard<std::mutex> lock(mu);
+    cudaError_t e = launched ? cudaEventRecord(slots[i].done, stream) : cudaSuccess;
+    slots[i].pending = false;
+    return e;
+  }
+  void destroy() {
+    for (auto& s : slots) if (s.done) cudaEventDestroy(s.done);
+    for (void* p : blocks) cudaFree(p);
+    slots.clear();
+    blocks.clear();
+  }
+};
 
 }  // namespace
 
@@ -86,8 +154,7 @@ struct scion_dtree {
   bool owns_image = true;
   ImageHeader header{};
   scion::TreeView view{};
-  unsigned long long* counters = nullptr;  // kCounterSlots work-fetch counters
-  std::atomic<uint32_t> next_slot{0};
+  CounterPool counters;  // one work-fetch counter per launch in flight
   // staging for the host entry points
   static constexpr int kSlots = 4;  // staging slots of the host entry points: H2D(k+1) || kernel(k) || D2H(k-1)
   void* h2d[kSlots] = {};
@@ -143,14 +210,12 @@ int header_from_ptree(const scion_ptree& p, ImageHeader& h) {
 int finish_dtree(scion_dtree* t) {
   t->kernels = scion::find_kernels(t->layout->name.c_str());
   if (!t->kernels) return fail(SCION_ERR_LAYOUT, "no kernels were compiled for layout '" + t->layout->name + "'");
-  CUDA_OK(cudaMalloc(&t->counters, kCounterSlots * sizeof(unsigned long long)));
+  {
+    std::lock_guard<std::mutex> lock(t->counters.mu);
+    CUDA_OK(t->counters.grow());
+  }
   fill_view(*t);
   return SCION_OK;
-}
-
-unsigned long long* take_counter(const scion_dtree* t) {
-  scion_dtree* m = const_cast<scion_dtree*>(t);
-  return m->counters + (m->next_slot.fetch_add(1) % kCounterSlots);
 }
 
 }  // namespace
@@ -348,6 +413,123 @@ uint64_t scion_ptree_node_bytes(const scion_ptree* p) {
     if (!p->plan->buffers[b].is_global_array) s += p->buffers[b].size();
   return s;
 }
+// ---- validation shared by every way a PhysicalTree built elsewhere enters the library (container file,
+// in-memory import): sizes must be the planner's footprint() for the stated counts (plan.cpp:333-347), segment
+// bases the planner's, the primitive range and the root reference inside their buffers — a tree that passes
+// cannot make a kernel read outside the device image through its ROOT; child links inside node records are the
+// producer's contract ("buffers sized exactly footprint()").
+static int validate_ptree(scion_ptree& p, std::string& why) {
+  const scion::lc::Plan& plan = *p.plan;
+  const size_t nb = plan.buffers.size();
+  if (p.buffers.size() != nb || p.counts.size() != nb || p.seg_bases.size() != nb) { why = "buffer table does not match the layout's plan"; return 1; }
+  if (p.globals.size() != plan.globals.size()) { why = "global slot table does not match the layout's plan"; return 1; }
+  if (nb > SCION_MAX_BUFFERS || plan.globals.size() > SCION_MAX_GLOBALS) { why = "layout exceeds the device view limits"; return 1; }
+  p.sizes.resize(nb);
+  for (size_t b = 0; b < nb; b++) {
+    const scion::lc::Buffer& pb = plan.buffers[b];
+    const uint64_t have = p.buffers[b].size();
+    p.sizes[b] = have;
+    if (pb.is_arena) {
+      if (p.seg_bases[b].empty()) p.seg_bases[b] = {0};
+      if (p.seg_bases[b].size() != 1 || p.seg_bases[b][0] != 0) { why = "arena buffer '" + pb.name + "' must have the single segment base 0"; return 1; }
+      continue;
+    }
+    if (pb.segments.size() > SCION_MAX_SEGMENTS) { why = "too many segments"; return 1; }
+    std::vector<uint64_t> bases;
+    const uint64_t stride = pb.node_stride();
+    if (stride && p.counts[b] > (~0ull >> 8) / stride) { why = "element count of buffer '" + pb.name + "' is absurd"; return 1; }
+    const uint64_t want = pb.bytes(p.counts[b], &bases);
+    if (have != want) { why = "buffer '" + pb.name + "': " + std::to_string(have) + " bytes, footprint() says " + std::to_string(want) + " for " + std::to_string(p.counts[b]) + " elements"; return 1; }
+    if (p.seg_bases[b].empty()) p.seg_bases[b] = bases;
+    if (p.seg_bases[b] != bases) { why = "segment bases of buffer '" + pb.name + "' disagree with the plan (plan.cpp:333-347)"; return 1; }
+  }
+  const scion::lc::Buffer* prim = plan.buffer_named("primitives");
+  if (!prim) { why = "layout has no primitives array"; return 1; }
+  if (p.nprims == 0) p.nprims = p.counts[(size_t)prim->id];
+  if (p.nprims != p.counts[(size_t)prim->id]) { why = "nprims disagrees with the primitives buffer"; return 1; }
+  const scion::lc::Buffer* nodes = plan.buffer_named(plan.node_group);
+  if (!nodes) { why = "layout has no node group"; return 1; }
+  const uint64_t ncount = p.counts[(size_t)nodes->id], nbytes = p.buffers[(size_t)nodes->id].size();
+  if (plan.family == scion::lc::Family::Bvh8) {  // tagged reference: bit 0 = Interior, else Leaf(O, nprims) (bvh8*.scion)
+    const bool ci = plan.type_bits(plan.ref[0].type) <= 32;
+    const uint64_t r = p.root0;
+    if (r & 1ull) {
+      const uint64_t key = ci ? ((r & 0xffffffffull) >> 2) : (r >> 2);
+      if (key >= ncount) { why = "root reference names interior " + std::to_string(key) + " of " + std::to_string(ncount); return 1; }
+    } else {
+      const uint64_t o = ci ? ((r & 0xffffffffull) >> 7) : (r >> 7), n = ((r >> 2) & 31ull) + 1ull;
+      if (p.nprims && o + n > p.nprims) { why = "root leaf reference exceeds the primitives array"; return 1; }
+    }
+  } else if (nodes->is_arena) {
+    if (ncount && p.root0 + nodes->segments[0].stride_bytes > nbytes) { why = "root reference lies outside the node arena"; return 1; }
+  } else {
+    if (ncount == 0 || p.root0 >= ncount) { why = "root reference " + std::to_string(p.root0) + " is not a node index (node count " + std::to_string(ncount) + ")"; return 1; }
+  }
+  return 0;
+}
+
+// In-memory import of a PhysicalTree produced by someone else's build_physical (buffer id ->
+// byte array; global slot -> scalar; root reference): one descriptor per BufferDesc / GlobalDesc of the plan
+// (/root/reference/proj/include/layoutc/plan.hpp:31-48), matched by NAME, any order.  The library copies.
+int scion_ptree_from_buffers(const scion_tree_desc* d, scion_ptree** out) {
+  if (!d || !out || !d->layout || (!d->buffers && d->nbuffers) || (!d->globals && d->nglobals)) return fail(SCION_ERR_ARG, "null argument");
+  SCION_TRY(
+    const scion::LayoutEntry* e = scion::find_layout(d->layout);
+    if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + d->layout + "'");
+    const scion::lc::Plan& plan = *e->plan;
+    auto p = std::make_unique<scion_ptree>();
+    p->layout = e->name;
+    p->plan = &plan;
+    const size_t nb = plan.buffers.size();
+    p->buffers.resize(nb); p->counts.assign(nb, 0); p->seg_bases.resize(nb);
+    p->globals.resize(plan.globals.size());
+    for (auto& g : p->globals) g.fill(0);
+    std::vector<char> seen_b(nb, 0), seen_g(plan.globals.size(), 0);
+    for (uint32_t i = 0; i < d->nbuffers; i++) {
+      const scion_buffer_desc& bd = d->buffers[i];
+      if (!bd.name) return fail(SCION_ERR_ARG, "buffer descriptor without a name");
+      const scion::lc::Buffer* pb = plan.buffer_named(bd.name);
+      if (!pb) return fail(SCION_ERR_ARG, std::string("layout '") + e->name + "' has no buffer '" + bd.name + "'");
+      if (seen_b[(size_t)pb->id]) return fail(SCION_ERR_ARG, std::string("buffer '") + bd.name + "' given twice");
+      if (!bd.data && bd.bytes) return fail(SCION_ERR_ARG, std::string("buffer '") + bd.name + "' has bytes but no data");
+      seen_b[(size_t)pb->id] = 1;
+      p->buffers[(size_t)pb->id].assign((const uint8_t*)bd.data, (const uint8_t*)bd.data + bd.bytes);
+      p->counts[(size_t)pb->id] = bd.count;
+      if (bd.seg_bases) p->seg_bases[(size_t)pb->id].assign(bd.seg_bases, bd.seg_bases + bd.n_seg_bases);
+    }
+    for (size_t b = 0; b < nb; b++)
+      if (!seen_b[b] && plan.buffers[b].node_stride() != 0) return fail(SCION_ERR_ARG, "missing buffer '" + plan.buffers[b].name + "'");
+    for (uint32_t i = 0; i < d->nglobals; i++) {
+      const scion_global_desc& gd = d->globals[i];
+      if (!gd.name) return fail(SCION_ERR_ARG, "global descriptor without a name");
+      size_t g = 0;
+      while (g < plan.globals.size() && plan.globals[g].name != gd.name) g++;
+      if (g == plan.globals.size()) return fail(SCION_ERR_ARG, std::string("layout '") + e->name + "' has no global slot '" + gd.name + "'");
+      if (seen_g[g]) return fail(SCION_ERR_ARG, std::string("global '") + gd.name + "' given twice");
+      seen_g[g] = 1;
+      memcpy(p->globals[g].data(), gd.raw, 16);
+    }
+    for (size_t g = 0; g < plan.globals.size(); g++)
+      if (!seen_g[g]) return fail(SCION_ERR_ARG, "missing global slot '" + plan.globals[g].name + "'");
+    p->root0 = d->root_ref;
+    memcpy(p->carried, d->carried, sizeof(p->carried));
+    p->nprims = d->nprims;
+    std::string why;
+    if (validate_ptree(*p, why)) return fail(SCION_ERR_ARG, "scion_ptree_from_buffers: " + why);
+    *out = p.release();
+    return SCION_OK;
+  )
+}
+// the survey's one-call form: import + upload; the host descriptor stays the caller's
+int scion_tree_upload(const scion_tree_desc* host, int device, scion_dtree** out) {
+  scion_ptree* p = nullptr;
+  int rc = scion_ptree_from_buffers(host, &p);
+  if (rc) return rc;
+  rc = scion_dtree_upload(p, device, out);
+  scion_ptree_free(p);
+  return rc;
+}
+
 // ---- container file: "SCIONPT1" | u32 version | u32 name_len | name | u64 nprims | u64 root0 | 6 x f32 carried |
 //      u32 nglob | nglob x { u32 len, name, 16 raw bytes } | u32 nbuf | nbuf x { u32 len, name, u64 count, u64 bytes,
 //      u32 nseg, nseg x u64 base } | raw buffers, each padded to 16 bytes.  Little-endian throughout.
@@ -380,10 +562,14 @@ int scion_ptree_save(const scion_ptree* p, const char* path) {
 }
 int scion_ptree_load(const char* path, scion_ptree** out) {
   if (!path || !out) return fail(SCION_ERR_ARG, "null argument");
-  FILE* f = fopen(path, "rb");
-  if (!f) return fail(SCION_ERR_ARG, std::string("cannot open ") + path);
-  FileR r{f};
-  auto bail = [&](const std::string& why) { fclose(f); return fail(SCION_ERR_ARG, std::string(path) + ": " + why); };
+  struct Closer { void operator()(FILE* f) const { if (f) fclose(f); } };
+  std::unique_ptr<FILE, Closer> file(fopen(path, "rb"));  // closed on every path, exceptions included
+  if (!file) return fail(SCION_ERR_ARG, std::string("cannot open ") + path);
+  FileR r{file.get()};
+  auto bail = [&](const std::string& why) { return fail(SCION_ERR_ARG, std::string(path) + ": " + why); };
+  uint64_t file_bytes = 0;
+  if (fseek(file.get(), 0, SEEK_END) == 0) { long e = ftell(file.get()); if (e > 0) file_bytes = (uint64_t)e; }
+  if (fseek(file.get(), 0, SEEK_SET) != 0) return bail("cannot seek");
   char magic[8];
   r.raw(magic, 8);
   if (!r.ok || memcmp(magic, "SCIONPT1", 8) != 0) return bail("not a scion PhysicalTree container");
@@ -406,26 +592,27 @@ int scion_ptree_load(const char* path, scion_ptree** out) {
     if (!r.ok || nb != p->plan->buffers.size()) return bail("buffer table does not match the layout's plan");
     p->buffers.resize(nb); p->counts.resize(nb); p->seg_bases.resize(nb);
     std::vector<uint64_t> sizes(nb);
+    uint64_t payload = 0;
     for (uint32_t b = 0; b < nb; b++) {
       if (r.str() != p->plan->buffers[b].name) return bail("buffer name mismatch");
       p->counts[b] = r.val<uint64_t>();
       sizes[b] = r.val<uint64_t>();
       uint32_t ns = r.val<uint32_t>();
-      if (!r.ok || ns > 8) return bail("corrupt segment table");
-      for (uint32_t s = 0; s < ns; s++) p->seg_bases[b].push_back(r.val<uint64_t>());
       const scion::lc::Buffer& pb = p->plan->buffers[b];
-      if (!pb.is_arena && sizes[b] != pb.bytes(p->counts[b])) return bail("buffer size disagrees with footprint() for its count");
+      if (!r.ok || ns != (pb.is_arena ? 1u : (uint32_t)pb.segments.size())) return bail("segment table does not match the layout's plan");
+      for (uint32_t s = 0; s < ns; s++) p->seg_bases[b].push_back(r.val<uint64_t>());
+      if (!r.ok || sizes[b] > file_bytes || payload + sizes[b] > file_bytes) return bail("buffer sizes exceed the file");  // before any allocation
+      payload += sizes[b];
     }
     for (uint32_t b = 0; b < nb; b++) {
       p->buffers[b].resize(sizes[b]);
-      p->sizes.resize(nb);
-      p->sizes[b] = sizes[b];
       r.raw(p->buffers[b].data(), sizes[b]);
       char pad[16];
       r.raw(pad, (16 - sizes[b] % 16) % 16);
     }
     if (!r.ok) return bail("truncated container");
-    fclose(f);
+    std::string why;
+    if (validate_ptree(*p, why)) return bail(why);
     *out = p.release();
     return SCION_OK;
   )
@@ -458,19 +645,23 @@ static int dtree_create(const scion_ptree* p, int device, bool copy, scion_dtree
   t->device = device;
   int rc = header_from_ptree(*p, t->header);
   if (rc) { delete t; return rc; }
-  CUDA_OK(cudaSetDevice(device));
+  // every failure below releases what was acquired so far (scion_dtree_free respects owns_image)
+#define CREATE_OK(expr) do { cudaError_t ce__ = (expr); if (ce__ != cudaSuccess) { scion_dtree_free(t); \
+    return fail(ce__ == cudaErrorNoDevice || ce__ == cudaErrorInsufficientDriver ? SCION_ERR_NO_DEVICE : SCION_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(ce__)); } } while (0)
+  CREATE_OK(cudaSetDevice(device));
   if (into) {
     if (into_bytes < t->header.total_bytes || ((uintptr_t)into & 255u)) { delete t; return fail(SCION_ERR_ARG, "upload_into: buffer too small or not 256-byte aligned"); }
     t->image = (uint8_t*)into;
     t->owns_image = false;
   } else {
-    CUDA_OK(cudaMalloc(&t->image, t->header.total_bytes));
+    CREATE_OK(cudaMalloc(&t->image, t->header.total_bytes));
   }
-  CUDA_OK(cudaMemset(t->image, 0, t->header.total_bytes));
-  CUDA_OK(cudaMemcpy(t->image, &t->header, sizeof(ImageHeader), cudaMemcpyHostToDevice));
+  CREATE_OK(cudaMemset(t->image, 0, t->header.total_bytes));
+  CREATE_OK(cudaMemcpy(t->image, &t->header, sizeof(ImageHeader), cudaMemcpyHostToDevice));
   if (copy)
     for (size_t b = 0; b < p->buffers.size(); b++)
-      if (!p->buffers[b].empty()) CUDA_OK(cudaMemcpy(t->image + t->header.offset[b], p->buffers[b].data(), p->buffers[b].size(), cudaMemcpyHostToDevice));
+      if (!p->buffers[b].empty()) CREATE_OK(cudaMemcpy(t->image + t->header.offset[b], p->buffers[b].data(), p->buffers[b].size(), cudaMemcpyHostToDevice));
+#undef CREATE_OK
   rc = finish_dtree(t);
   if (rc) { scion_dtree_free(t); return rc; }
   *out = t;
@@ -580,6 +771,13 @@ int scion_dtree_from_image(const char* layout, void* d_image, uint64_t bytes, in
   cudaError_t ce = cudaMemcpy(&t->header, d_image, sizeof(ImageHeader), cudaMemcpyDeviceToHost);
   if (ce != cudaSuccess) { t->owns_image = false; delete t; return fail(SCION_ERR_CUDA, cudaGetErrorString(ce)); }
   if (t->header.magic != kImageMagic || t->header.total_bytes > bytes) { t->owns_image = false; delete t; return fail(SCION_ERR_ARG, "not a scion device image"); }
+  {  // the header came from device memory someone else filled: range-check it before fill_view indexes fixed-size arrays
+    const ImageHeader& h = t->header;
+    bool ok = ((uintptr_t)d_image & 255u) == 0 && h.nbuf >= 1 && h.nbuf <= SCION_MAX_BUFFERS && h.nglob >= 0 && h.nglob <= SCION_MAX_GLOBALS && h.total_bytes >= kHeaderBytes;
+    for (int b = 0; ok && b < h.nbuf; b++)
+      ok = h.offset[b] >= kHeaderBytes && (h.offset[b] & 255u) == 0 && h.bytes[b] <= h.total_bytes && h.offset[b] <= h.total_bytes - h.bytes[b];
+    if (!ok) { t->owns_image = false; delete t; return fail(SCION_ERR_ARG, "corrupt device image header (buffer table out of range, or image not 256-byte aligned)"); }
+  }
   t->header.layout[sizeof(t->header.layout) - 1] = 0;
   if (layout && strcmp(layout, t->header.layout) != 0) { t->owns_image = false; delete t; return fail(SCION_ERR_ARG, "image holds a different layout"); }
   t->layout = scion::find_layout(t->header.layout);
@@ -601,7 +799,7 @@ void scion_dtree_free(scion_dtree* t) {
     if (t->d2h[i]) cudaFree(t->d2h[i]);
     if (t->d_status[i]) cudaFree(t->d_status[i]);
   }
-  if (t->counters) cudaFree(t->counters);
+  t->counters.destroy();
   if (t->cd_scratch.ptr) cudaFree(t->cd_scratch.ptr);
   if (t->image && t->owns_image) cudaFree(t->image);
   delete t;
@@ -621,11 +819,16 @@ static int run_query(const scion_dtree* t, bool hit, const void* in, uint64_t n,
   a.out = out;
   a.status = status;
   a.counters = counters;
-  a.next = take_counter(t);
+  CounterPool& pool = const_cast<scion_dtree*>(t)->counters;
+  size_t slot = 0;
+  CUDA_OK(pool.take(&slot, &a.next));
   a.stream = (cudaStream_t)stream;
   a.variant = variant;
   a.grid = 0;
-  CUDA_OK(cudaMemsetAsync(a.next, 0, sizeof(unsigned long long), a.stream));
+  {
+    cudaError_t e0 = cudaMemsetAsync(a.next, 0, sizeof(unsigned long long), a.stream);
+    if (e0 != cudaSuccess) { pool.release(slot, a.stream, false); CUDA_OK(e0); }
+  }
   // Experiment (SCION_L2_PERSIST=1): pin the node buffer in the persisting L2 carve-out.
   static const bool l2_persist = [] { const char* e = getenv("SCION_L2_PERSIST"); return e && e[0] == '1'; }();
   if (l2_persist && t->header.nbuf > 1) {
@@ -649,7 +852,13 @@ static int run_query(const scion_dtree* t, bool hit, const void* in, uint64_t n,
     attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     cudaStreamSetAttribute(a.stream, cudaStreamAttributeAccessPolicyWindow, &attr);
   }
-  CUDA_OK(fn(a));
+  {
+    const cudaError_t e1 = fn(a);
+    // the guard event goes behind the memset even if the launch itself failed
+    const cudaError_t e2 = pool.release(slot, a.stream, true);
+    CUDA_OK(e1);
+    CUDA_OK(e2);
+  }
   g_launches.fetch_add(1);
   return SCION_OK;
 }
@@ -724,6 +933,7 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
   else while (kChunk < (1ull << 23) && kChunk * 8 < n) kChunk <<= 1;
   constexpr int S = scion_dtree::kSlots;
   if (t->chunk < kChunk) {
+    t->chunk = 0;  // a failure below must not leave a stale size next to freed / null staging slots
     for (int i = 0; i < S; i++) {
       if (!t->streams[i]) {
         CUDA_OK(cudaStreamCreateWithFlags(&t->streams[i], cudaStreamNonBlocking));
@@ -743,25 +953,38 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
   // kernels alternate between two streams: the ragged tail of chunk c (a persistent grid drains at the
   // pace of its longest queries) overlaps the head of chunk c + 1
   cudaStream_t s_in = t->streams[0], s_out = t->streams[3];
-  uint64_t c = 0;
-  for (uint64_t off = 0; off < n; off += kChunk, c++) {
-    const int k = (int)(c % S);
-    cudaStream_t s_run = t->streams[1 + (c & 1)];
-    const uint64_t m = std::min(kChunk, n - off);
-    if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_in, t->ev_run[k], 0));
-    CUDA_OK(cudaMemcpyAsync(t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
-    CUDA_OK(cudaEventRecord(t->ev_in[k], s_in));
-    CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_in[k], 0));
-    if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_out[k], 0));
-    int rc = run_query(t, hit, t->h2d[k], m, t->d2h[k], h_status ? t->d_status[k] : nullptr, nullptr, 0, s_run);
-    if (rc) return rc;
-    CUDA_OK(cudaEventRecord(t->ev_run[k], s_run));
-    CUDA_OK(cudaStreamWaitEvent(s_out, t->ev_run[k], 0));
-    CUDA_OK(cudaMemcpyAsync((uint8_t*)h_out + off * out_sz, t->d2h[k], m * out_sz, cudaMemcpyDeviceToHost, s_out));
-    if (h_status) CUDA_OK(cudaMemcpyAsync(h_status + off, t->d_status[k], m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_out));
-    CUDA_OK(cudaEventRecord(t->ev_out[k], s_out));
+  // on any failure the four streams are drained before returning: async D2H copies into the caller's
+  // h_out / h_status may still be in flight
+  auto pipeline = [&]() -> int {
+    uint64_t c = 0;
+    for (uint64_t off = 0; off < n; off += kChunk, c++) {
+      const int k = (int)(c % S);
+      cudaStream_t s_run = t->streams[1 + (c & 1)];
+      const uint64_t m = std::min(kChunk, n - off);
+      if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_in, t->ev_run[k], 0));
+      CUDA_OK(cudaMemcpyAsync(t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
+      CUDA_OK(cudaEventRecord(t->ev_in[k], s_in));
+      CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_in[k], 0));
+      if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_out[k], 0));
+      int rc = run_query(t, hit, t->h2d[k], m, t->d2h[k], h_status ? t->d_status[k] : nullptr, nullptr, 0, s_run);
+      if (rc) return rc;
+      CUDA_OK(cudaEventRecord(t->ev_run[k], s_run));
+      CUDA_OK(cudaStreamWaitEvent(s_out, t->ev_run[k], 0));
+      CUDA_OK(cudaMemcpyAsync((uint8_t*)h_out + off * out_sz, t->d2h[k], m * out_sz, cudaMemcpyDeviceToHost, s_out));
+      if (h_status) CUDA_OK(cudaMemcpyAsync(h_status + off, t->d_status[k], m * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_out));
+      CUDA_OK(cudaEventRecord(t->ev_out[k], s_out));
+    }
+    return SCION_OK;
+  };
+  const int rc = pipeline();
+  const std::string why = rc ? g_error : std::string();
+  cudaError_t se = cudaSuccess;
+  for (int i = 0; i < S; i++) {
+    const cudaError_t e = cudaStreamSynchronize(t->streams[i]);
+    if (e != cudaSuccess && se == cudaSuccess) se = e;
   }
-  for (int i = 0; i < S; i++) CUDA_OK(cudaStreamSynchronize(t->streams[i]));
+  if (rc) return fail(rc, why);
+  CUDA_OK(se);
   return SCION_OK;
 }
 int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64_t n, scion_hit* h_hits, uint32_t* h_status) {
