@@ -11,6 +11,13 @@ copies inside the timed region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload c1|c3|c4|c5] [--layout pbrt-q16] [--sweep a,b,c] [--scale f]
+
+Multi-GPU: one process per GPU.  Either launch it under torchrun yourself
+  python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+or just pass --gpus N: with WORLD_SIZE unset the script re-executes itself under torch.distributed.run with N
+ranks (and fails loudly if the node has fewer than N GPUs).  torch.distributed only provides the rendezvous, the
+barrier and the max-over-ranks of the timings; the tree is replicated and the hit records are gathered by the
+C ABI's own NCCL calls (scion_dtree_broadcast / scion_gather_results, csrc/comm.cu).
 """
 import argparse
 import json
@@ -111,6 +118,19 @@ class ClockSampler:
         return {"sm_mhz": (s[len(s) // 2] if s else None), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(s)}
 
 
+def kernel_sources_sha():
+    """sha1 over the device sources the traversal kernels are compiled from (profiles/traffic.json carries the value
+    its ncu captures were taken at, so a stale capture is visible in the bench line)"""
+    import glob
+    import hashlib
+    h = hashlib.sha1()
+    base = os.path.join(ROOT, "paper_2511_15028_b200", "csrc")
+    for f in sorted(glob.glob(os.path.join(base, "device", "*")) + glob.glob(os.path.join(base, "gen", "*.cuh"))):
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
 def spread_sample(total, n_sample, chunks=64):
     """`chunks` equal contiguous pieces spread evenly over [0,total) — a representative bounded sample."""
     n_sample = min(n_sample, total)
@@ -154,7 +174,9 @@ def build_host_side(args, wl_name):
     return sb, W, wl, scene, ltree, lo, hi, build_s
 
 
-def run_reference(args, rank):
+def run_reference(args, rank, n_label):
+    """CPU arm.  Under torchrun rank 0 alone runs; `n_label` = the launcher's world size (or --gpus without a launcher):
+    it only labels which GPU run this line sits beside — the CPU arm touches no GPU."""
     if rank != 0:
         return
     import __graft_entry__ as g
@@ -183,7 +205,7 @@ def run_reference(args, rank):
     val = nq / t_step / 1e6
     unit = "Mrays/s" if wl.algorithm == "chrt" else "Mqueries/s"
     sample = f"{nq} queries per step = 64 contiguous chunks spread evenly over the {wl.total}-query workload, layout {args.layout}"
-    line = {"impl": "reference", "metric": f"{unit} ({args.layout}, {wl.name})", "value": val, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
+    line = {"impl": "reference", "metric": f"{unit} ({args.layout}, {wl.name})", "value": val, "unit": unit, "n_gpus": n_label, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": f"{wl.name}: {wl.description}", "layout": args.layout, "queries_per_step": nq},
             "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "port", "sample": sample},
@@ -191,25 +213,58 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def respawn_under_torchrun(args):
+    """--gpus N with no launcher around us: start N ranks (one per GPU) and relay their exit code."""
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: this node exposes {have} CUDA device(s); one process per GPU is required "
+                         "(the B200 backend has no CPU fallback and does not oversubscribe a GPU)")
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")         # communicator setup lines: one "Init COMPLETE" per rank and communicator
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd, env=env))
+
+
 def main():
     args = parse_args()
+    launched = "WORLD_SIZE" in os.environ
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world if launched else args.gpus)
         return
+    if args.gpus > 1 and not launched:
+        respawn_under_torchrun(args)
+    if launched and world != args.gpus and rank == 0:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s); reporting n_gpus={world}\n")
 
     import torch
     import torch.distributed as dist
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the B200 backend has no CPU fallback (use --impl reference for the CPU arm)")
+    if local_rank >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: local rank {local_rank} has no GPU ({torch.cuda.device_count()} visible); one process per GPU is required")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     force_dist = os.environ.get("SCION_FORCE_DIST") == "1"  # exercise the NCCL code path with a single rank (tests)
     if world > 1 or force_dist:
         if "MASTER_ADDR" not in os.environ:
-            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29511", RANK="0", WORLD_SIZE="1")
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()), RANK="0", WORLD_SIZE="1")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__ as g
     if rank == 0:
@@ -235,30 +290,28 @@ def main():
     q_bytes, r_bytes = (32, 8) if wl.algorithm == "chrt" else (12, 20)
     first, count = sb.partition(wl.total, rank, world)
 
+    # ---- the C ABI's own communicator (csrc/comm.cu): rank 0 makes the NCCL unique id, torch.distributed ships it
+    comm = None
+    if world > 1 or force_dist:
+        uid = torch.zeros(sb.NCCL_UNIQUE_ID_BYTES, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(sb.Comm.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = sb.Comm.init_rank(bytes(uid.cpu().numpy().tobytes()), world, rank, local_rank)
+
     def replicate(layout):
-        """rank 0 encodes + uploads into a torch tensor; one ncclBroadcast replicates the image."""
-        nbytes = torch.zeros(1, dtype=torch.int64, device=dev)
-        pt = None
+        """rank 0 encodes + uploads; scion_dtree_broadcast (one ncclBroadcast of the packed image) replicates the tree"""
+        pt, dt = None, None
         if rank == 0:
-            t0 = time.time()
             pt = ltree.encode(layout)
-            nbytes[0] = pt.image_bytes
-            enc_s = time.time() - t0
-        if world > 1 or force_dist:
-            dist.broadcast(nbytes, 0)
-        img = torch.empty(int(nbytes.item()) + 256, dtype=torch.uint8, device=dev)
-        off = (-img.data_ptr()) % 256
-        ptr = img.data_ptr() + off
-        tb0 = time.time()
-        if rank == 0:
-            dt = pt.upload_into(local_rank, ptr, int(nbytes.item()))
-        if world > 1 or force_dist:
-            dist.broadcast(img[off:off + int(nbytes.item())], 0)
+            dt = pt.upload(local_rank)
+        torch.cuda.synchronize()
+        tb0 = time.perf_counter()
+        if comm is not None:
+            dt = comm.broadcast_tree(dt, 0)
             torch.cuda.synchronize()
-        if rank != 0:
-            dt = sb.DeviceTree.from_image(ptr, int(nbytes.item()), local_rank, layout)
-        bcast_s = time.time() - tb0
-        return dt, img, pt, bcast_s
+        bcast_s = time.perf_counter() - tb0
+        return dt, None, pt, bcast_s
 
     d_q = torch.empty(count * q_bytes, dtype=torch.uint8, device=dev)
     d_r = torch.empty(count * r_bytes, dtype=torch.uint8, device=dev)
@@ -381,16 +434,31 @@ def main():
         except Exception as ex:  # e.g. not enough pinnable host memory on the box
             e2e = {"value": None, "unit": unit, "error": str(ex)[:200]}
 
-    # ---- gather of hit records: all ranks -> every rank, checksum of checksums
+    # ---- gather of hit records by query index (scion_gather_results): every rank receives all records
     gather = None
-    if world > 1 or force_dist:
+    if comm is not None:
+        run_step(dt)  # the device-path result of the headline layout (the e2e leg reused d_r)
+        full = torch.empty(wl.total * r_bytes, dtype=torch.uint8, device=dev)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        sizes = [sb.partition(wl.total, r, world)[1] * r_bytes for r in range(world)]
-        full = [torch.empty(s, dtype=torch.uint8, device=dev) for s in sizes]
-        dist.all_gather(full, d_r)
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        comm.gather(d_r.data_ptr(), wl.total, r_bytes, full.data_ptr())
+        g1.record()
         torch.cuda.synchronize()
-        gather = {"ms": (time.perf_counter() - t0) * 1e3, "bytes": int(sum(sizes))}
+        g_ms = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(g_ms, op=dist.ReduceOp.MAX)
+        # every rank must hold the same bytes, and its own slice unchanged at its own offset: checksum of checksums
+        own = bool(torch.equal(full[first * r_bytes:(first + count) * r_bytes], d_r))
+        cs = full.view(torch.int32).to(torch.int64).sum().reshape(1)
+        lo_cs, hi_cs = cs.clone(), cs.clone()
+        dist.all_reduce(lo_cs, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi_cs, op=dist.ReduceOp.MAX)
+        ok = torch.tensor([1 if own and int(lo_cs) == int(hi_cs) else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        gather = {"ms": float(g_ms.item()), "bytes": int(wl.total * r_bytes), "checksum": int(cs.item()), "identical_on_all_ranks": bool(int(ok.item())),
+                  "how": "scion_gather_results (ncclAllGather / grouped ncclBroadcast), CUDA events, max over ranks"}
+        del full
 
     if rank == 0:
         cpu = None
@@ -407,11 +475,17 @@ def main():
                        "sample": f"{n1} queries = 64 contiguous chunks spread evenly over the {wl.total}-query workload, layout {args.layout}, {t1:.1f} s"}
             except Exception as ex:
                 cpu = {"value": None, "unit": unit, "cores": os.cpu_count() or 1, "kind": "port", "sample": f"failed: {str(ex)[:160]}"}
-        traffic = None
+        # ncu DRAM bytes per launch of the headline kernel: a figure CAPTURED at a stated commit (ncu cannot run inside a
+        # timed bench), so the line says which capture it quotes and flags it when the kernel sources changed since
+        traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(f"{wl.name}:{args.layout}:{world}")
+                ent = json.load(open(tp)).get(f"{wl.name}:{args.layout}:{world}")
+                if isinstance(ent, dict):
+                    traffic = ent.get("bytes")
+                    traffic_src = {k: ent.get(k) for k in ("capture", "commit", "kernel_sha")}
+                    traffic_src["kernel_sources_unchanged_since_capture"] = ent.get("kernel_sha") == kernel_sources_sha()
             except Exception:
                 traffic = None
         h = headline
@@ -419,16 +493,22 @@ def main():
                 "ms_per_step": h["ms"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": f"{wl.name}: {wl.description}", "layout": args.layout, "queries": wl.total, "queries_per_gpu": count,
                            "l2_policy": "inputs larger than L2 (rays %.1f GB + tree %.2f GB per GPU vs 126 MB L2); no explicit flush" % (count * q_bytes / 1e9, h["pt"].total_bytes / 1e9),
-                           "partition": "contiguous query ranges per rank; tree replicated by one ncclBroadcast", "build_s": build_s},
-                "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s", "frac": h["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
+                           "partition": "contiguous query ranges per rank; tree replicated by one ncclBroadcast of the packed image (scion_dtree_broadcast)", "build_s": build_s,
+                           "e2e_note": "e2e is PCIe-bound: 32 B in + 8 B out per ray over a Gen5 x16 link (measured ~55 GB/s H2D with both directions busy, tools/pcie_probe.py) "
+                                       "puts the floor of this call shape at ~162 ms for 2^28 rays; the 3-stream pipeline runs within a few % of it"},
+                "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s", "frac": h["gbs"] / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                              "bytes_per_query": h["bpq"], "frac_of_nominal_8tbs": h["gbs"] / 8000.0},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(h["launches"]), "clocks": h["clocks"], "layouts": results}
         if gather:
             line["gather"] = gather
-        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.free()
     if world > 1 or force_dist:
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:  # last thing on stdout (NCCL's INFO lines, if any, come before it)
+        sys.stdout.flush()
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

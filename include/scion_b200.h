@@ -273,7 +273,8 @@ int scion_dtree_download_image(const scion_dtree* t, void* h_dst, uint64_t bytes
  * resulting image is byte-identical to scion_encode + scion_dtree_upload.  Same builder faults
  * (SCION_ERR_BUILD) as scion_encode; SCION_ERR_NO_DEVICE without a GPU. */
 int scion_encode_device(const scion_ltree* t, const char* layout, int device, scion_dtree** out);
-/* rebuild a device tree around a received image (no copy; image owned by caller unless adopt=1) */
+/* rebuild a device tree around a received image (no copy; image owned by caller unless adopt=1; on failure the
+ * image always stays the caller's).  The image must be 256-byte aligned. */
 int scion_dtree_from_image(const char* layout, void* d_image, uint64_t bytes, int device, int adopt,
                            scion_dtree** out);
 void scion_dtree_free(scion_dtree* t);
@@ -356,6 +357,38 @@ int scion_gen_points_host(const float lo[3], const float hi[3], uint64_t seed, u
 
 /* contiguous query partition for rank r of nranks: [first, first+count) */
 void scion_partition(uint64_t n, int rank, int nranks, uint64_t* first, uint64_t* count);
+
+/* ------------------------------------------------------------------------- */
+/* Multi-GPU (SPEC.md:416 concurrent queries on a shared immutable tree; :645 "the query loop may fan out across
+ * workers ... reports are merged deterministically by query index").  The tree is replicated with ONE
+ * ncclBroadcast of its packed image, queries are partitioned contiguously (scion_partition), results are gathered
+ * by query index; no collective runs inside a traversal launch.  NCCL is bound at run time (libnccl.so.2 of the
+ * process): without it these calls return SCION_ERR_ARG and everything else keeps working. */
+/* ------------------------------------------------------------------------- */
+#define SCION_NCCL_UNIQUE_ID_BYTES 128
+typedef struct scion_comm scion_comm; /* one NCCL communicator bound to one device */
+int scion_nccl_version(int* out);
+/* one process per GPU: rank 0 creates the id, ships it to the others out of band, every rank calls init_rank */
+int scion_comm_unique_id(uint8_t id[SCION_NCCL_UNIQUE_ID_BYTES]);
+int scion_comm_init_rank(const uint8_t id[SCION_NCCL_UNIQUE_ID_BYTES], int nranks, int rank, int device, scion_comm** out);
+/* one process, ndev GPUs (ncclCommInitAll): fills out[0..ndev); devices NULL = 0..ndev-1 */
+int scion_comm_init_all(int ndev, const int* devices, scion_comm** out);
+/* wrap a communicator the caller created (an ncclComm_t of the same libnccl instance); never destroyed by us */
+int scion_comm_adopt(void* nccl_comm, scion_comm** out);
+int scion_comm_rank(const scion_comm* c);
+int scion_comm_size(const scion_comm* c);
+int scion_comm_device(const scion_comm* c);
+void scion_comm_free(scion_comm* c);
+/* Replicate a resident tree.  Exactly the root rank passes its tree (others NULL); every rank returns with a tree on
+ * its communicator's device (*out == root_tree on the root).  Collective: all ranks must call. */
+int scion_dtree_broadcast(scion_dtree* root_tree, int root, scion_comm* comm, void* stream, scion_dtree** out);
+/* single-process form over the array of scion_comm_init_all: out[root] = root_tree, the others are created */
+int scion_dtree_broadcast_all(scion_dtree* root_tree, int root, scion_comm* const* comms, int n, void* const* streams, scion_dtree** out);
+/* Gather result records by query index: this rank's d_part holds the records of scion_partition(n_total, rank,
+ * nranks); d_full (n_total records, may contain d_part at its own offset) receives all of them on every rank. */
+int scion_gather_results(scion_comm* comm, const void* d_part, uint64_t n_total, uint32_t record_bytes, void* d_full, void* stream);
+int scion_gather_results_all(scion_comm* const* comms, int n, const void* const* d_parts, uint64_t n_total, uint32_t record_bytes,
+                             void* const* d_fulls, void* const* streams);
 
 /* number of product kernels launched by this process so far (bench `gpu_launches`) */
 uint64_t scion_kernel_launches(void);

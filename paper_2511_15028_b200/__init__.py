@@ -162,6 +162,19 @@ def lib() -> C.CDLL:
         "scion_gen_secondary_host": (i32, [vp, u64, u64, u64, u64, vp]),
         "scion_gen_points_host": (i32, [P(C.c_float * 3), P(C.c_float * 3), u64, u64, u64, vp]),
         "scion_partition": (None, [u64, i32, i32, P(u64), P(u64)]),
+        "scion_nccl_version": (i32, [P(i32)]),
+        "scion_comm_unique_id": (i32, [P(C.c_uint8)]),
+        "scion_comm_init_rank": (i32, [P(C.c_uint8), i32, i32, i32, P(vp)]),
+        "scion_comm_init_all": (i32, [i32, P(i32), P(vp)]),
+        "scion_comm_adopt": (i32, [vp, P(vp)]),
+        "scion_comm_rank": (i32, [vp]),
+        "scion_comm_size": (i32, [vp]),
+        "scion_comm_device": (i32, [vp]),
+        "scion_comm_free": (None, [vp]),
+        "scion_dtree_broadcast": (i32, [vp, i32, vp, vp, P(vp)]),
+        "scion_dtree_broadcast_all": (i32, [vp, i32, P(vp), i32, P(vp), P(vp)]),
+        "scion_gather_results": (i32, [vp, vp, u64, u32, vp, vp]),
+        "scion_gather_results_all": (i32, [P(vp), i32, P(vp), u64, u32, P(vp), P(vp)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)  # AttributeError here == the library does not export a declared symbol
@@ -640,6 +653,92 @@ def partition(n: int, rank: int, nranks: int):
     a, b = C.c_uint64(), C.c_uint64()
     lib().scion_partition(n, rank, nranks, C.byref(a), C.byref(b))
     return a.value, b.value
+
+
+# --------------------------------------------------------------------------------------- multi-GPU
+NCCL_UNIQUE_ID_BYTES = 128
+
+
+def nccl_version() -> int:
+    v = C.c_int()
+    _check(lib().scion_nccl_version(C.byref(v)))
+    return v.value
+
+
+class Comm:
+    """One NCCL communicator bound to one device (scion_comm): tree replication and result gather of the C ABI."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * NCCL_UNIQUE_ID_BYTES)()
+        _check(lib().scion_comm_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def init_rank(unique_id: bytes, nranks: int, rank: int, device: int) -> "Comm":
+        assert len(unique_id) == NCCL_UNIQUE_ID_BYTES
+        buf = (C.c_uint8 * NCCL_UNIQUE_ID_BYTES)(*unique_id)
+        h = C.c_void_p()
+        _check(lib().scion_comm_init_rank(buf, nranks, rank, device, C.byref(h)))
+        return Comm(h)
+
+    @staticmethod
+    def init_all(ndev: int, devices=None):
+        out = (C.c_void_p * ndev)()
+        devs = (C.c_int * ndev)(*devices) if devices is not None else None
+        _check(lib().scion_comm_init_all(ndev, devs, out))
+        return [Comm(C.c_void_p(out[i])) for i in range(ndev)]
+
+    @property
+    def rank(self) -> int:
+        return lib().scion_comm_rank(self._h)
+
+    @property
+    def size(self) -> int:
+        return lib().scion_comm_size(self._h)
+
+    @property
+    def device(self) -> int:
+        return lib().scion_comm_device(self._h)
+
+    def broadcast_tree(self, tree: Optional["DeviceTree"], root: int = 0, stream: int = 0) -> "DeviceTree":
+        """Collective.  The root passes its resident tree, every other rank None; all ranks get a tree."""
+        h = C.c_void_p()
+        _check(lib().scion_dtree_broadcast(tree._h if tree is not None else None, root, self._h, stream or None, C.byref(h)))
+        if tree is not None:
+            return tree
+        return DeviceTree(h, self.device)
+
+    def gather(self, d_part: int, n_total: int, record_bytes: int, d_full: int, stream: int = 0):
+        _check(lib().scion_gather_results(self._h, d_part, n_total, record_bytes, d_full, stream or None))
+
+    def free(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.scion_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.free()
+
+
+def broadcast_tree_all(tree: "DeviceTree", root: int, comms) -> list:
+    """single-process form (Comm.init_all): returns one DeviceTree per communicator, trees[root] is `tree`"""
+    n = len(comms)
+    arr = (C.c_void_p * n)(*[c._h for c in comms])
+    out = (C.c_void_p * n)()
+    _check(lib().scion_dtree_broadcast_all(tree._h, root, arr, n, None, out))
+    return [tree if i == root else DeviceTree(C.c_void_p(out[i]), comms[i].device) for i in range(n)]
+
+
+def gather_results_all(comms, d_parts, n_total: int, record_bytes: int, d_fulls):
+    n = len(comms)
+    arr = (C.c_void_p * n)(*[c._h for c in comms])
+    parts = (C.c_void_p * n)(*d_parts)
+    fulls = (C.c_void_p * n)(*d_fulls)
+    _check(lib().scion_gather_results_all(arr, n, parts, n_total, record_bytes, fulls, None))
 
 
 def kernel_launches() -> int:

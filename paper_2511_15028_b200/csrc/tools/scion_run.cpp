@@ -4,7 +4,10 @@
 // CUDA runtime (device buffers, events).
 //   scion_run layouts
 //   scion_run footprint <layout> <terrain|sphere|cloud>:<N>
-//   scion_run bench     <layout> <scene>:<N> <queries> [primary|secondary|points] [--host-encode]
+//   scion_run bench     <layout> <scene>:<N> <queries> [primary|secondary|points] [--host-encode] [--gpus G]
+// `--gpus G` (G > 1): ONE process drives G devices — ncclCommInitAll, the tree encoded on device 0 and replicated with
+// one ncclBroadcast (scion_dtree_broadcast_all), queries partitioned contiguously (scion_partition) and generated on
+// each device from (seed, global index), results gathered by query index (scion_gather_results_all); n_gpus = G in the row.
 // `bench` follows the paper's protocol: 1 warm-up + 9 runs, drop the 2
 // lowest and 2 highest, mean of the remaining 5; prints one CSV row; the un-timed instrumented pass gives
 // the reference's counters (node visits, primitive tests) and the algorithmic bytes per query.
@@ -36,6 +39,96 @@ static int make_scene(const std::string& spec, scion_scene** out, bool* terrain)
   if (kind == "sphere") return scion_scene_sphere((uint32_t)n, 1, out);
   if (kind == "cloud") return scion_scene_cloud(n, 1, out);
   return SCION_ERR_ARG;
+}
+
+// ---- multi-GPU bench (single process, G devices): SURVEY §8e
+static int bench_multi(int G, scion_dtree* dt0, const scion_layout_info& li, const char* layout, const char* scene_spec, uint64_t n, const std::string& kind, bool terrain,
+                       const float lo[3], const float hi[3], uint64_t node_bytes, uint64_t nprims) {
+  const bool cpq = kind == "points";
+  const uint32_t q_sz = cpq ? 12 : (uint32_t)sizeof(scion_ray), r_sz = cpq ? (uint32_t)sizeof(scion_cp) : (uint32_t)sizeof(scion_hit);
+  std::vector<scion_comm*> comms((size_t)G, nullptr);
+  CK(scion_comm_init_all(G, nullptr, comms.data()));
+  std::vector<scion_dtree*> trees((size_t)G, nullptr);
+  cudaEvent_t b0, b1;
+  CU(cudaSetDevice(0));
+  CU(cudaEventCreate(&b0));
+  CU(cudaEventCreate(&b1));
+  CU(cudaEventRecord(b0));
+  CK(scion_dtree_broadcast_all(dt0, 0, comms.data(), G, nullptr, trees.data()));
+  CU(cudaSetDevice(0));
+  CU(cudaEventRecord(b1));
+  CU(cudaEventSynchronize(b1));
+  float bcast_ms = 0;
+  CU(cudaEventElapsedTime(&bcast_ms, b0, b1));
+  std::vector<void*> d_q((size_t)G), d_r((size_t)G), d_full((size_t)G);
+  std::vector<uint64_t> first((size_t)G), count((size_t)G);
+  std::vector<cudaEvent_t> e0((size_t)G), e1((size_t)G);
+  uint32_t side = 1;
+  while ((uint64_t)(side + 1) * (side + 1) <= n) side++;
+  scion_camera cam;
+  scion_camera_default(lo, hi, terrain ? 1 : 0, side, side, &cam);
+  for (int g = 0; g < G; g++) {
+    CU(cudaSetDevice(g));
+    scion_partition(n, g, G, &first[(size_t)g], &count[(size_t)g]);
+    CU(cudaMalloc(&d_q[(size_t)g], (count[(size_t)g] + 1) * q_sz));
+    CU(cudaMalloc(&d_full[(size_t)g], (n + 1) * r_sz));
+    d_r[(size_t)g] = (uint8_t*)d_full[(size_t)g] + first[(size_t)g] * r_sz;  // results land in place: the gather moves only the other ranks' slices
+    CU(cudaEventCreate(&e0[(size_t)g]));
+    CU(cudaEventCreate(&e1[(size_t)g]));
+    if (cpq) CK(scion_gen_points(lo, hi, 7, first[(size_t)g], count[(size_t)g], (float*)d_q[(size_t)g], nullptr));
+    else if (kind == "secondary") CK(scion_gen_secondary(trees[(size_t)g], 7, first[(size_t)g], count[(size_t)g], (scion_ray*)d_q[(size_t)g], nullptr));
+    else CK(scion_gen_primary(&cam, first[(size_t)g], count[(size_t)g], (scion_ray*)d_q[(size_t)g], nullptr));
+  }
+  std::vector<float> ms;
+  for (int it = 0; it < 10; it++) {
+    for (int g = 0; g < G; g++) {
+      CU(cudaSetDevice(g));
+      CU(cudaEventRecord(e0[(size_t)g]));
+      if (cpq) CK(scion_closest_point(trees[(size_t)g], (const float*)d_q[(size_t)g], count[(size_t)g], (scion_cp*)d_r[(size_t)g], nullptr, nullptr, 0, nullptr));
+      else CK(scion_closest_hit(trees[(size_t)g], (const scion_ray*)d_q[(size_t)g], count[(size_t)g], (scion_hit*)d_r[(size_t)g], nullptr, nullptr, 0, nullptr));
+      CU(cudaEventRecord(e1[(size_t)g]));
+    }
+    float worst = 0;
+    for (int g = 0; g < G; g++) {
+      CU(cudaSetDevice(g));
+      CU(cudaEventSynchronize(e1[(size_t)g]));
+      float t = 0;
+      CU(cudaEventElapsedTime(&t, e0[(size_t)g], e1[(size_t)g]));
+      worst = std::max(worst, t);
+    }
+    if (it) ms.push_back(worst);  // max over devices
+  }
+  std::sort(ms.begin(), ms.end());
+  const double mean_ms = (ms[2] + ms[3] + ms[4] + ms[5] + ms[6]) / 5.0;
+  CU(cudaSetDevice(0));
+  CU(cudaEventRecord(b0));
+  CK(scion_gather_results_all(comms.data(), G, d_r.data(), n, r_sz, d_full.data(), nullptr));
+  for (int g = 0; g < G; g++) { CU(cudaSetDevice(g)); CU(cudaDeviceSynchronize()); }
+  CU(cudaSetDevice(0));
+  CU(cudaEventRecord(b1));
+  CU(cudaEventSynchronize(b1));
+  float gather_ms = 0;
+  CU(cudaEventElapsedTime(&gather_ms, b0, b1));
+  // every device must now hold the same n records
+  std::vector<uint8_t> ref((size_t)n * r_sz), other((size_t)n * r_sz);
+  CU(cudaMemcpy(ref.data(), d_full[0], ref.size(), cudaMemcpyDeviceToHost));
+  int mismatched = 0;
+  for (int g = 1; g < G; g++) {
+    CU(cudaSetDevice(g));
+    CU(cudaMemcpy(other.data(), d_full[(size_t)g], other.size(), cudaMemcpyDeviceToHost));
+    mismatched += std::memcmp(ref.data(), other.data(), ref.size()) != 0;
+  }
+  std::printf("layout,algorithm,scene,n_gpus,queries,kind,mean_ms,mqueries_per_s,bvh_bytes_per_prim,broadcast_ms,gather_ms,gather_mismatches\n");
+  std::printf("%s,%s,%s,%d,%llu,%s,%.4f,%.2f,%.3f,%.3f,%.3f,%d\n", layout, cpq ? "cpq" : "chrt", scene_spec, G, (unsigned long long)n, kind.c_str(), mean_ms, (double)n / mean_ms / 1e3,
+              (double)node_bytes / (double)nprims, bcast_ms, gather_ms, mismatched);
+  for (int g = 0; g < G; g++) {
+    cudaSetDevice(g);
+    cudaFree(d_q[(size_t)g]); cudaFree(d_full[(size_t)g]);
+    if (g) scion_dtree_free(trees[(size_t)g]);
+    scion_comm_free(comms[(size_t)g]);
+  }
+  (void)li;
+  return mismatched ? 1 : 0;
 }
 
 int main(int argc, char** argv) {
@@ -81,7 +174,15 @@ int main(int argc, char** argv) {
   const uint64_t n = std::strtoull(argv[4], nullptr, 10);
   std::string kind = argc > 5 && argv[5][0] != '-' ? argv[5] : "primary";
   bool host_encode = false;
-  for (int i = 5; i < argc; i++) host_encode |= std::strcmp(argv[i], "--host-encode") == 0;
+  int gpus = 1;
+  for (int i = 5; i < argc; i++) {
+    host_encode |= std::strcmp(argv[i], "--host-encode") == 0;
+    if (std::strcmp(argv[i], "--gpus") == 0 && i + 1 < argc) gpus = std::atoi(argv[i + 1]);
+  }
+  if (gpus < 1) return 2;
+  int ndev = 0;
+  if (scion_device_count(&ndev) != SCION_OK) return die(1, "no CUDA device");
+  if (gpus > ndev) { std::fprintf(stderr, "scion_run: --gpus %d but this node exposes %d CUDA device(s)\n", gpus, ndev); return 2; }
   const bool cpq = kind == "points";
   if (cpq && !li.has_cpq) { std::fprintf(stderr, "scion_run: cpq requires a binary layout\n"); return 2; }
 
@@ -104,6 +205,13 @@ int main(int argc, char** argv) {
   }
   float lo[3], hi[3];
   scion_scene_bounds(scene, lo, hi);
+  if (gpus > 1 || std::getenv("SCION_RUN_FORCE_MULTI")) {  // the env switch drives the same code over a 1-device communicator (tests on a 1-GPU box)
+    const int rc = bench_multi(gpus, dt, li, layout, argv[3], n, kind, terrain, lo, hi, node_bytes, nprims);
+    scion_dtree_free(dt);
+    scion_ltree_free(lt);
+    scion_scene_free(scene);
+    return rc;
+  }
   void *d_q = nullptr, *d_r = nullptr;
   uint32_t* d_st = nullptr;
   scion_counters* d_ctr = nullptr;
