@@ -222,6 +222,14 @@ def free_port():
     return port
 
 
+def nccl_logging(env):
+    """communicator setup lines stay on (one "Init COMPLETE" line per rank and communicator): raise NCCL_DEBUG to INFO
+    unless the caller already asked for INFO / TRACE, and keep it to the INIT subsystem unless told otherwise"""
+    if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        env["NCCL_DEBUG"] = "INFO"
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+
+
 def respawn_under_torchrun(args):
     """--gpus N with no launcher around us: start N ranks (one per GPU) and relay their exit code."""
     import torch
@@ -230,8 +238,7 @@ def respawn_under_torchrun(args):
         raise SystemExit(f"bench.py --gpus {args.gpus}: this node exposes {have} CUDA device(s); one process per GPU is required "
                          "(the B200 backend has no CPU fallback and does not oversubscribe a GPU)")
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")         # communicator setup lines: one "Init COMPLETE" per rank and communicator
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    nccl_logging(env)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
            "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
     raise SystemExit(subprocess.call(cmd, env=env))
@@ -263,8 +270,7 @@ def main():
     if world > 1 or force_dist:
         if "MASTER_ADDR" not in os.environ:
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()), RANK="0", WORLD_SIZE="1")
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        nccl_logging(os.environ)
         dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__ as g
     if rank == 0:

@@ -16,7 +16,12 @@
 // tools/gen_ref_ir_golden.py drives it here (the only place /root/reference exists) and commits the
 // answers as fixtures under tests/golden/ref_ir/, which pin BOTH the oracle and the CUDA kernels.
 //
-// usage: ref_interp <corpus-layout> <alg> <tree+rays.bin> <out.bin>
+// Two builds (oracle/Makefile): `ref_interp` links the UNMODIFIED reference and serves closest_hit; `ref_interp_fx`
+// links the reference with the dangling-`Frame&` bug of src/lower_internal.hpp:1073/:890 patched at build time (one
+// token, throw-away copy) and serves closest_point, whose lowering the unpatched reference corrupts.
+//
+// usage: ref_interp <corpus-layout> <chrt|cpq> <tree+queries.bin> <out.bin>
+//        ref_interp --print-ir <corpus-layout> <chrt|cpq|cd>          (the lowered IR as text, for build-vs-build diffs)
 #include <array>
 #include <cfenv>
 #include <cmath>
@@ -481,9 +486,10 @@ std::string rds(std::ifstream& in) { uint32_t n = rd<uint32_t>(in); std::string 
 }  // namespace
 
 int main(int argc, char** argv) {
-  if (argc < 5) { std::cerr << "usage: ref_interp <corpus-layout> <alg> <in.bin> <out.bin>\n"; return 2; }
+  const bool print_only = argc >= 4 && std::string(argv[1]) == "--print-ir";
+  if (!print_only && argc < 5) { std::cerr << "usage: ref_interp <corpus-layout> <chrt|cpq> <in.bin> <out.bin> | --print-ir <corpus-layout> <alg>\n"; return 2; }
   try {
-    const std::string name = argv[1], alg = argv[2];
+    const std::string name = print_only ? argv[2] : argv[1], alg = print_only ? argv[3] : argv[2];
     SourceSet ss;
     ParseResult r = parse_corpus(corpus_files_for_pair(name, alg), &ss);
     if (!r.ok()) throw std::runtime_error("parse failed");
@@ -497,7 +503,9 @@ int main(int argc, char** argv) {
     MemoryPlan plan = plan_layout(*adt, *layout, program);
     LoweredProgram lp;
     specialize_destructors(program, plan, lp);
-    const IrFunc* entry = lp.entry(alg == "chrt" ? "closest_hit" : alg);
+    if (print_only) { std::cout << print_ir(lp); return 0; }
+    const bool cpq = alg == "cpq";
+    const IrFunc* entry = lp.entry(alg == "chrt" ? "closest_hit" : cpq ? "closest_point" : alg);
     if (!entry) throw std::runtime_error("no entry point");
 
     // ---- tree + rays (written by tools/gen_ref_ir_golden.py from this repository's encoders)
@@ -563,17 +571,31 @@ int main(int argc, char** argv) {
       Val o; o.k = Val::Agg; o.e = {Val::F(p[0]), Val::F(p[1]), Val::F(p[2])};
       Val d; d.k = Val::Agg; d.e = {Val::F(p[4]), Val::F(p[5]), Val::F(p[6])};
       ray.e = {o, d, Val::F(p[3])};
-      Val tri; tri.k = Val::Agg;  // best = (inf, <zero triangle>)
-      for (int v = 0; v < 3; v++) { Val x; x.k = Val::Agg; x.e = {Val::F(0), Val::F(0), Val::F(0)}; tri.e.push_back(x); }
-      Val best; best.k = Val::Agg; best.e = {Val::F(inf), tri};
-      fr.locals[(size_t)entry->params[0].local] = ray;
-      fr.locals[(size_t)entry->params[1].local] = root;
-      fr.locals[(size_t)entry->params[2].local] = best;
-      it.exec_block(*entry, fr, entry->body);
-      const Val& b = fr.locals[(size_t)entry->params[2].local];
-      float rec[10];
-      rec[0] = b.e[0].f;
-      for (int v = 0; v < 3; v++) for (int a = 0; a < 3; a++) rec[1 + 3 * v + a] = b.e[1].e[(size_t)v].e[(size_t)a].f;
+      float rec[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      if (cpq) {  // closest_point(p: Point, bvh, best: mut (f32, Point)), cpq.scion:3; Point(v: f32x3), geometry.scion:9
+        Val pt; pt.k = Val::Agg; pt.e = {o};
+        Val zero; zero.k = Val::Agg; zero.e = {Val::F(0), Val::F(0), Val::F(0)};
+        Val bp; bp.k = Val::Agg; bp.e = {zero};
+        Val best; best.k = Val::Agg; best.e = {Val::F(inf), bp};
+        fr.locals[(size_t)entry->params[0].local] = pt;
+        fr.locals[(size_t)entry->params[1].local] = root;
+        fr.locals[(size_t)entry->params[2].local] = best;
+        it.exec_block(*entry, fr, entry->body);
+        const Val& b = fr.locals[(size_t)entry->params[2].local];
+        rec[0] = b.e[0].f;
+        for (int a = 0; a < 3; a++) rec[1 + a] = b.e[1].e[0].e[(size_t)a].f;
+      } else {
+        Val tri; tri.k = Val::Agg;  // best = (inf, <zero triangle>)
+        for (int v = 0; v < 3; v++) { Val x; x.k = Val::Agg; x.e = {Val::F(0), Val::F(0), Val::F(0)}; tri.e.push_back(x); }
+        Val best; best.k = Val::Agg; best.e = {Val::F(inf), tri};
+        fr.locals[(size_t)entry->params[0].local] = ray;
+        fr.locals[(size_t)entry->params[1].local] = root;
+        fr.locals[(size_t)entry->params[2].local] = best;
+        it.exec_block(*entry, fr, entry->body);
+        const Val& b = fr.locals[(size_t)entry->params[2].local];
+        rec[0] = b.e[0].f;
+        for (int v = 0; v < 3; v++) for (int a = 0; a < 3; a++) rec[1 + 3 * v + a] = b.e[1].e[(size_t)v].e[(size_t)a].f;
+      }
       out.write((const char*)rec, sizeof(rec));
     }
     std::cerr << "ref_interp: " << name << " x " << alg << ": " << nrays << " queries, " << it.node_loads << " slot loads\n";

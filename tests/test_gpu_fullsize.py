@@ -1,11 +1,19 @@
-"""BASELINE-size checks on the GPU.  C1 (2^20 primary rays, 100K triangles) is compared in full
-against the oracle; the larger configs are covered through size-independent properties the domain
-offers (cross-layout invariance, brute-force agreement on a sample, monotonicity in tmax, replay
-determinism) plus an oracle comparison on a bounded spread sample."""
+"""BASELINE-size parity on the GPU ("parity is checked on the full set for C1/C2 and on >= 2^20-query
+samples per layout for C3-C5").  Every config runs at its FULL size on the device — C1 2^20 primary rays / 100 K
+triangles, C3 2^24 secondary rays / 1 M triangles, C4 2^24 query points / 10 M-point cloud, C5 2^28 mixed rays /
+10 M triangles — for EVERY layout the bench sweeps, and the answers are compared bit for bit (primitive id, t / d2 /
+closest point) with the CPU oracle: on all queries for C1, on a 2^20-query sample spread evenly over the workload
+(64 contiguous chunks) for C3, C4 and C5.  On top of that the size-independent properties the domain offers:
+cross-layout invariance on all queries, replay determinism, brute-force agreement, monotonicity in tmax."""
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
+
+SAMPLE = 1 << 20
+BINARY = ["pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "ptr", "identity", "dop14"]
+WIDE = ["bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
+EXACT_BOXES = {"pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "ptr", "identity"}  # f32 boxes of the logical tree, binary visit order
 
 
 @pytest.fixture(scope="module")
@@ -15,164 +23,215 @@ def torch_cuda():
     return torch
 
 
-def run(torch, sb, dt, d_rays, n):
-    d_hits = torch.empty(n * 8, dtype=torch.uint8, device="cuda:0")
-    d_st = torch.zeros(n, dtype=torch.int32, device="cuda:0")
+def sweep_layouts(sb, extra=()):
+    """every layout bench.py sweeps (all registered layouts except shared-slab), corpus + authored"""
+    names = [l["name"] for l in sb.layouts() if l["name"] != "shared-slab"]
+    return names + [e for e in extra if e not in names]
+
+
+def spread_index(torch, total, n_sample, chunks=64):
+    """indices of `chunks` equal contiguous pieces spread evenly over [0, total) — bench.py's spread_sample"""
+    n_sample = min(n_sample, total)
+    per = n_sample // chunks
+    starts = (torch.arange(chunks, dtype=torch.float64) * (total / chunks)).to(torch.int64)
+    return (starts[:, None] + torch.arange(per, dtype=torch.int64)[None, :]).reshape(-1).to("cuda:0")
+
+
+def run_hits(torch, dt, d_rays, n, d_hits=None):
+    if d_hits is None:
+        d_hits = torch.empty(n * 8, dtype=torch.uint8, device="cuda:0")
+    d_st = torch.ones(n, dtype=torch.int32, device="cuda:0")
     dt.closest_hit(d_rays.data_ptr(), n, d_hits.data_ptr(), d_st.data_ptr())
     torch.cuda.synchronize()
     assert int((d_st != 0).sum()) == 0
     return d_hits
 
 
+def check_hits_against_oracle(sb, oracle, pt, d_rays, d_hits, idx, what):
+    rays = d_rays.view(-1, 32)[idx].cpu().numpy().reshape(-1).view(sb.RAY_DTYPE)
+    got = d_hits.view(-1, 8)[idx].cpu().numpy().reshape(-1).view(sb.HIT_DTYPE)
+    want, st = oracle.closest_hit(oracle.tree_bytes(pt), rays)
+    assert not st.any(), what
+    bad = np.nonzero((got["prim"] != want["prim"]) | (got["t"].view(np.uint32) != want["t"].view(np.uint32)))[0]
+    assert bad.size == 0, f"{what}: {bad.size} of {len(rays)} sampled queries differ from the oracle, first at sample {bad[:5]}"
+    return rays, got
+
+
 def test_c1_full_parity(built, oracle, torch_cuda):
-    """BASELINE configs[0]/[1]: every one of the 1024x1024 primary rays, per layout, bit-exact vs the oracle"""
+    """BASELINE configs[0]/[1]: every one of the 1024x1024 primary rays, EVERY layout incl. shared-slab, bit-exact vs the oracle"""
     sb, torch = built, torch_cuda
     import paper_2511_15028_b200.workloads as W
-    wl0 = W.workload("c1")
-    scene = W.make_scene(wl0)
+    scene = W.make_scene(W.workload("c1"))
     assert scene.ntris == 100352
     lt = scene.build_sah(32, 4).collapse8()
     lo, hi = scene.bounds()
     wl = W.workload("c1", lo, hi)
     n = wl.total
+    assert n == 1 << 20
     d_rays = torch.empty(n * 32, dtype=torch.uint8, device="cuda:0")
-    ref_prim = None
-    for layout in ("pbrt", "pbrt-soa", "pbrt-q16", "sg-eq", "sg-eq-align16", "dop14", "bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci", "pbrt-post", "ptr", "identity"):
+    ref = None
+    for layout in sweep_layouts(sb, ["shared-slab"]):
         pt = lt.encode(layout)
         dt = pt.upload(0)
         W.generate_device(wl, dt, lo, hi, 0, n, d_rays.data_ptr())
         torch.cuda.synchronize()
         rays = d_rays.cpu().numpy().view(sb.RAY_DTYPE)
-        got = run(torch, sb, dt, d_rays, n).cpu().numpy().view(sb.HIT_DTYPE)
+        got = run_hits(torch, dt, d_rays, n).cpu().numpy().view(sb.HIT_DTYPE)
         want, st = oracle.closest_hit(oracle.tree_bytes(pt), rays)
+        assert not st.any()
         assert np.array_equal(got["prim"], want["prim"]) and np.array_equal(got["t"].view(np.uint32), want["t"].view(np.uint32)), layout
         assert (got["prim"] != sb.MISS_PRIM).mean() > 0.3
         # cross-layout invariant (SPEC.md:296): same logical tree => same answers for every layout
-        if ref_prim is None:
-            ref_prim, ref_t = got["prim"].copy(), got["t"].copy()
+        if ref is None:
+            ref = got.copy()
         else:
-            assert np.array_equal(got["prim"], ref_prim) and np.array_equal(got["t"], ref_t), layout
+            assert np.array_equal(got["prim"], ref["prim"]) and np.array_equal(got["t"], ref["t"]), layout
         dt.free()
 
 
-def test_c3_properties(built, oracle, torch_cuda):
-    """BASELINE configs[2]: 1M-triangle terrain, incoherent secondary rays (2^22 of the 2^24 here to keep the
-    suite short): cross-layout agreement on all rays, oracle + brute-force agreement on a spread sample."""
+def test_c3_full_size(built, oracle, torch_cuda):
+    """BASELINE configs[2] at full size: 1,002,528 triangles, all 2^24 incoherent secondary rays on the device for every
+    swept layout (+ shared-slab on the sample), 2^20-ray spread sample against the oracle per layout."""
     sb, torch = built, torch_cuda
     import paper_2511_15028_b200.workloads as W
-    wl = W.workload("c3", scale=0.25)
+    wl = W.workload("c3")
     scene = W.make_scene(wl)
     assert scene.ntris == 1002528
     lt = scene.build_sah(32, 4).collapse8()
     lo, hi = scene.bounds()
     n = wl.total
+    assert n == 1 << 24
     d_rays = torch.empty(n * 32, dtype=torch.uint8, device="cuda:0")
-    ref = None
-    for layout in ("pbrt", "pbrt-q16", "sg-eq", "bvh8-q8-ci"):
+    idx = spread_index(torch, n, SAMPLE)
+    assert idx.numel() == SAMPLE
+    exact = None
+    for layout in sweep_layouts(sb):
         pt = lt.encode(layout)
         dt = pt.upload(0)
         W.generate_device(wl, dt, lo, hi, 0, n, d_rays.data_ptr())
-        hits = run(torch, sb, dt, d_rays, n)
-        again = run(torch, sb, dt, d_rays, n)
-        assert torch.equal(hits, again)  # replay determinism
-        if ref is None:
-            ref = hits
-            idx = np.arange(0, n, n // 4096)[:4096]
-            rays = d_rays.view(-1, 32)[torch.from_numpy(idx).to("cuda:0")].cpu().numpy().reshape(-1).view(sb.RAY_DTYPE)
-            got = hits.view(-1, 8)[torch.from_numpy(idx).to("cuda:0")].cpu().numpy().reshape(-1).view(sb.HIT_DTYPE)
-            want, _ = oracle.closest_hit(oracle.tree_bytes(pt), rays)
-            assert np.array_equal(got["prim"], want["prim"]) and np.array_equal(got["t"].view(np.uint32), want["t"].view(np.uint32))
+        hits = run_hits(torch, dt, d_rays, n)
+        rays, got = check_hits_against_oracle(sb, oracle, pt, d_rays, hits, idx, f"c3/{layout}")
+        if layout == "pbrt":
+            assert torch.equal(hits, run_hits(torch, dt, d_rays, n))  # replay determinism
+            exact = hits
             brute = oracle.brute_hit(lt.triangles(), rays[:256])
             assert np.array_equal(got["t"][:256], brute["t"]) and np.array_equal(got["prim"][:256], brute["prim"])
             # monotonicity: shrinking tmax below the hit distance turns the hit into a miss
-            r2 = rays.copy()
-            hit = got["prim"] != sb.MISS_PRIM
-            r2["tmax"] = np.where(hit, got["t"] * 0.5, 1.0).astype(np.float32)
+            r2 = rays[:65536].copy()
+            g0 = got[:65536]
+            hit = g0["prim"] != sb.MISS_PRIM
+            r2["tmax"] = np.where(hit, g0["t"] * 0.5, 1.0).astype(np.float32)
             d2 = torch.from_numpy(r2.view(np.uint8).reshape(-1)).to("cuda:0")
-            g2 = run(torch, sb, dt, d2, len(r2)).cpu().numpy().view(sb.HIT_DTYPE)
+            g2 = run_hits(torch, dt, d2, len(r2)).cpu().numpy().view(sb.HIT_DTYPE)
             w2, _ = oracle.closest_hit(oracle.tree_bytes(pt), r2)
             assert np.array_equal(g2["prim"], w2["prim"]) and np.all(g2["t"][g2["prim"] != sb.MISS_PRIM] <= r2["tmax"][g2["prim"] != sb.MISS_PRIM])
-        else:
-            assert torch.equal(hits, ref), f"{layout}: differs from pbrt on the same logical tree"
+        elif exact is not None:
+            same = (hits.view(-1, 8) == exact.view(-1, 8)).all(dim=1).float().mean().item()
+            if layout in EXACT_BOXES:
+                assert same == 1.0, f"{layout}: differs from pbrt on the same logical tree"
+            else:  # conservative boxes / other visit order: equal up to equal-t ties and ulp-level culls — counted, not hidden
+                assert same > 0.9999, (layout, same)
         dt.free()
+    # shared-slab (one slab per node, ~2600 visits per ray on a terrain): the sample only, still 2^20 rays
+    pt = lt.encode("shared-slab")
+    dt = pt.upload(0)
+    W.generate_device(wl, dt, lo, hi, 0, n, d_rays.data_ptr())
+    d_s = d_rays.view(-1, 32)[idx].contiguous().view(-1)
+    hs = run_hits(torch, dt, d_s, SAMPLE)
+    check_hits_against_oracle(sb, oracle, pt, d_s, hs, torch.arange(SAMPLE, device="cuda:0"), "c3/shared-slab")
+    assert torch.equal(hs.view(-1, 8), exact.view(-1, 8)[idx])
+    dt.free()
 
 
-def test_c4_closest_point_cloud(built, oracle, torch_cuda):
-    """BASELINE configs[3] at reduced size (1M points, 2^18 queries): point cloud as degenerate triangles"""
-    sb, torch = built, torch_cuda
-    scene = sb.Scene.cloud(1_000_000, 1)
-    lt = scene.build_sah(32, 4)
-    lo, hi = scene.bounds()
-    n = 1 << 18
-    d_p = torch.empty(n * 12, dtype=torch.uint8, device="cuda:0")
-    sb.gen_points(lo, hi, 21, 0, n, d_p.data_ptr())
-    ref = None
-    for layout in ("pbrt", "pbrt-q16", "sg-eq"):
-        pt = lt.encode(layout)
-        dt = pt.upload(0)
-        d_o = torch.empty(n * 20, dtype=torch.uint8, device="cuda:0")
-        dt.closest_point(d_p.data_ptr(), n, d_o.data_ptr())
-        torch.cuda.synchronize()
-        out = d_o.cpu().numpy().view(sb.CP_DTYPE)
-        pts = d_p.cpu().numpy().view(np.float32).reshape(-1, 3)
-        idx = np.arange(0, n, n // 2048)[:2048]
-        want, _ = oracle.closest_point(oracle.tree_bytes(pt), pts[idx])
-        assert np.array_equal(out[idx].view(np.uint32).reshape(-1, 5), want.view(np.uint32).reshape(-1, 5)), layout
-        brute = oracle.brute_point(lt.triangles(), pts[idx[:64]])
-        assert np.array_equal(out["d2"][idx[:64]], brute["d2"])
-        if ref is None:
-            ref = out["d2"].copy()
-        else:
-            assert np.array_equal(out["d2"], ref), layout  # d2 is layout-invariant (ties may pick other ids)
-        dt.free()
-
-
-def test_c5_properties(built, oracle, torch_cuda):
-    """BASELINE configs[4] scene at full size (9,999,392 triangles, 7.3 M nodes); the 2^28-ray workload at
-    1/16 scale (8 cameras x 1024^2 primary + 2^23 secondary, same generators and seeds): cross-layout agreement
-    on all rays for layouts whose boxes are exact, agreement of every layout where it must hold by construction
-    (align16 variants, device-encoded image), oracle agreement on a spread sample per layout, brute force on a
-    handful, replay determinism, and the checksum the multi-GPU gather uses."""
+def test_c4_full_size(built, oracle, torch_cuda):
+    """BASELINE configs[3] at FULL size: 10,000,000-point cloud (degenerate triangles), all 2^24 query points on the
+    device for every binary layout, 2^20-query spread sample against the oracle (d2, closest point, primitive: bit-exact)."""
     sb, torch = built, torch_cuda
     import paper_2511_15028_b200.workloads as W
-    wl0 = W.workload("c5")
+    wl0 = W.workload("c4")
     scene = W.make_scene(wl0)
+    assert scene.ntris == 10_000_000
+    lt = scene.build_sah(32, 4)
+    lo, hi = scene.bounds()
+    wl = W.workload("c4", lo, hi)
+    n = wl.total
+    assert n == 1 << 24
+    d_p = torch.empty(n * 12, dtype=torch.uint8, device="cuda:0")
+    idx = spread_index(torch, n, SAMPLE)
+    ref = None
+    cpq_layouts = [l["name"] for l in sb.layouts() if l["has_cpq"] and l["name"] != "shared-slab"]
+    assert set(BINARY) <= set(cpq_layouts)
+    for layout in cpq_layouts:
+        pt = lt.encode(layout)
+        dt = pt.upload(0)
+        W.generate_device(wl, dt, lo, hi, 0, n, d_p.data_ptr())
+        d_o = torch.empty(n * 20, dtype=torch.uint8, device="cuda:0")
+        d_st = torch.ones(n, dtype=torch.int32, device="cuda:0")
+        dt.closest_point(d_p.data_ptr(), n, d_o.data_ptr(), d_st.data_ptr())
+        torch.cuda.synchronize()
+        assert int((d_st != 0).sum()) == 0
+        pts = d_p.view(-1, 12)[idx].cpu().numpy().reshape(-1).view(np.float32).reshape(-1, 3)
+        got = d_o.view(-1, 20)[idx].cpu().numpy().reshape(-1).view(sb.CP_DTYPE)
+        want, st = oracle.closest_point(oracle.tree_bytes(pt), pts)
+        assert not st.any()
+        bad = np.nonzero((got.view(np.uint32).reshape(-1, 5) != want.view(np.uint32).reshape(-1, 5)).any(axis=1))[0]
+        assert bad.size == 0, f"c4/{layout}: {bad.size} of {SAMPLE} sampled queries differ from the oracle, first {bad[:5]}"
+        d2 = d_o.view(torch.float32).view(-1, 5)[:, 0]
+        if ref is None:
+            brute = oracle.brute_point(lt.triangles(), pts[:16])
+            assert np.array_equal(got["d2"][:16], brute["d2"])
+            ref = d2.clone()
+        else:
+            assert torch.equal(d2, ref), layout  # d2 is layout-invariant on ALL 2^24 queries (ties may pick other ids)
+        dt.free()
+        del d_o
+
+
+def test_c5_full_size(built, oracle, torch_cuda):
+    """BASELINE configs[4] = the bench workload at FULL size: 9,999,392 triangles, all 2^28 rays (8 cameras x 4096^2
+    primary + 2^27 secondary) on the device for every layout of the bench sweep; 2^20-ray spread sample against the oracle
+    per layout; cross-layout agreement on all 2^28 rays; device-encoded image answers identically; replay determinism."""
+    sb, torch = built, torch_cuda
+    import paper_2511_15028_b200.workloads as W
+    scene = W.make_scene(W.workload("c5"))
     assert scene.ntris == 9999392
     lt = scene.build_sah(32, 4).collapse8()
     lo, hi = scene.bounds()
-    wl = W.workload("c5", lo, hi, scale=1.0 / 16)
+    wl = W.workload("c5", lo, hi)
     n = wl.total
-    assert n == 1 << 24
+    assert n == 1 << 28
     d_rays = torch.empty(n * 32, dtype=torch.uint8, device="cuda:0")
-    idx = np.arange(0, n, n // 2048)[:2048]
-    d_idx = torch.from_numpy(idx).to("cuda:0")
-    exact = {}
-    for layout in ("pbrt", "pbrt-align16", "pbrt-q16", "bvh8", "bvh8-q8-ci"):
+    hits = torch.empty(n * 8, dtype=torch.uint8, device="cuda:0")
+    exact = torch.empty(n * 8, dtype=torch.uint8, device="cuda:0")
+    idx = spread_index(torch, n, SAMPLE)
+    have_exact = False
+    order = ["pbrt"] + [l for l in sweep_layouts(sb) if l != "pbrt"]
+    for layout in order:
         pt = lt.encode(layout)
         dt = pt.upload(0)
-        W.generate_device(wl, dt, lo, hi, 0, n, d_rays.data_ptr())
-        hits = run(torch, sb, dt, d_rays, n)
-        assert torch.equal(hits, run(torch, sb, dt, d_rays, n)), layout  # replay determinism
-        rays = d_rays.view(-1, 32)[d_idx].cpu().numpy().reshape(-1).view(sb.RAY_DTYPE)
-        got = hits.view(-1, 8)[d_idx].cpu().numpy().reshape(-1).view(sb.HIT_DTYPE)
-        want, _ = oracle.closest_hit(oracle.tree_bytes(pt), rays)
-        assert np.array_equal(got["prim"], want["prim"]) and np.array_equal(got["t"].view(np.uint32), want["t"].view(np.uint32)), layout
+        if not have_exact:
+            W.generate_device(wl, dt, lo, hi, 0, n, d_rays.data_ptr())  # the rays do not depend on the layout
+        out = exact if not have_exact else hits
+        run_hits(torch, dt, d_rays, n, out)
+        rays, got = check_hits_against_oracle(sb, oracle, pt, d_rays, out, idx, f"c5/{layout}")
         assert 0.3 < (got["prim"] != sb.MISS_PRIM).mean() < 1.0
-        if layout == "pbrt":
+        if not have_exact:
+            have_exact = True
             brute = oracle.brute_hit(lt.triangles(), rays[:16])
             assert np.array_equal(got["t"][:16], brute["t"]) and np.array_equal(got["prim"][:16], brute["prim"])
-            exact["pbrt"] = hits
-        elif layout == "pbrt-align16":  # same boxes, other stride: identical answers on every ray
-            assert torch.equal(hits, exact["pbrt"])
-        elif layout in ("bvh8", "bvh8-q8-ci"):  # other visit order / conservative boxes: equal up to equal-t ties and ulp-level culls
-            same = (hits.view(-1, 8) == exact["pbrt"].view(-1, 8)).all(dim=1).float().mean().item()
-            assert same > 0.9999, (layout, same)
-        elif layout == "pbrt-q16":  # device-side encode of the same tree answers identically
+            run_hits(torch, dt, d_rays, n, hits)
+            assert torch.equal(hits, exact)  # replay determinism on all 2^28 rays
+        else:
+            same = (hits.view(torch.int64) == exact.view(torch.int64)).float().mean().item()
+            if layout in EXACT_BOXES:
+                assert same == 1.0, f"{layout}: differs from pbrt on the same logical tree"
+            else:
+                assert same > 0.9999, (layout, same)
+        if layout == "pbrt-q16":  # device-side encode of the same tree answers identically on every ray
+            mine = hits.clone()
             dev = lt.encode_device(layout, 0)
-            assert torch.equal(run(torch, sb, dev, d_rays, n), hits)
+            run_hits(torch, dev, d_rays, n, hits)
+            assert torch.equal(hits, mine)
             dev.free()
-            # quantised boxes enclose the originals: t can only differ where a conservative box admits an
-            # equal-t tie earlier in visit order; count, do not hide (DESIGN §4, L2 parity)
-            same = (hits.view(-1, 8) == exact["pbrt"].view(-1, 8)).all(dim=1).float().mean().item()
-            assert same > 0.9999, same
+            del mine
         dt.free()

@@ -13,6 +13,10 @@ import numpy as np
 import paper_2511_15028_b200 as sb
 
 INTERP = os.path.join(ROOT, "oracle", "_ref", "ref_interp")
+# closest_point needs the reference with its dangling-Frame& bug patched at build time (oracle/Makefile: one token,
+# throw-away copy); both builds lower closest_hit to byte-identical IR (tests/test_ref_ir_golden.py checks it)
+INTERP_FX = os.path.join(ROOT, "oracle", "_ref", "ref_interp_fx")
+BINARY = ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14"]
 CORPUS = ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14",
           "bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
 
@@ -102,5 +106,59 @@ def main():
     print("tests/golden/ref_ir.npz written")
 
 
+def special_points(lt, lo, hi):
+    """points ON triangle vertices / edges / faces (d2 = 0 and exact ties between neighbouring triangles), the centre,
+    points far outside the bounds, and points whose two child boxes are equidistant (the `L < R` tie rule of cpq.scion:17)"""
+    tris = np.ascontiguousarray(lt.triangles(), np.float32).reshape(-1, 3, 3)
+    out = []
+    for k in (0, len(tris) // 3, len(tris) // 2, len(tris) - 1):
+        a, b, c = tris[k]
+        out += [a, b, c, np.float32(0.5) * (a + b), (a + b + c) / np.float32(3.0)]
+    c = np.float32(0.5) * (lo + hi)
+    out += [c, lo, hi, lo - np.float32(3.0), hi + np.float32(7.5), np.array([c[0], hi[1] + 2.0, c[2]], np.float32), np.array([lo[0] - 1.0, c[1], c[2]], np.float32)]
+    for ax in range(3):  # on the split planes of the top of the tree: children at equal distance
+        q = c.copy(); q[ax] = lo[ax] + np.float32(0.25) * (hi[ax] - lo[ax]); out.append(q)
+    return np.ascontiguousarray(np.stack(out), np.float32)
+
+
+def as_rays(pts):
+    rays = np.zeros(len(pts), sb.RAY_DTYPE)
+    rays["ox"], rays["oy"], rays["oz"] = pts[:, 0], pts[:, 1], pts[:, 2]
+    return rays
+
+
+def main_cpq():
+    assert os.path.exists(INTERP_FX), "build it first: make -C oracle ref"
+    out = {}
+    for tag, scene, builder in (("terrain", sb.Scene.terrain(12, 5), "sah"), ("sphere", sb.Scene.sphere(8, 3), "median"), ("cloud", sb.Scene.cloud(600, 4), "sah")):
+        lt = scene.build_sah(32, 4) if builder == "sah" else scene.build_median(2)
+        lo, hi = (np.asarray(x, np.float32) for x in scene.bounds())
+        ext = hi - lo
+        pts = np.concatenate([sb.gen_points_host(lo - 0.3 * ext, hi + 0.3 * ext, 77, 0, 400), special_points(lt, lo, hi)])
+        tris = np.ascontiguousarray(lt.triangles(), np.float32).reshape(-1, 9)
+        out[f"{tag}:points"] = pts.copy()
+        out[f"{tag}:scene"] = np.array({"terrain": [12, 5], "sphere": [8, 3], "cloud": [600, 4]}[tag])
+        for layout in BINARY:
+            pt = lt.encode(layout)
+            with tempfile.TemporaryDirectory() as td:
+                fin, fout = os.path.join(td, "in.bin"), os.path.join(td, "out.bin")
+                write_input(fin, pt, as_rays(pts))
+                r = subprocess.run([INTERP_FX, layout, "cpq", fin, fout], capture_output=True, text=True)
+                if r.returncode != 0:
+                    raise SystemExit(f"{layout}: {r.stderr}")
+                rec = np.fromfile(fout, np.float32).reshape(-1, 10)
+            out[f"{tag}:d2:{layout}"] = rec[:, 0].copy()
+            out[f"{tag}:point:{layout}"] = rec[:, 1:4].copy()
+            print(f"{tag:8s} {layout:14s} cpq  d2 in [{rec[:, 0].min():.3g}, {rec[:, 0].max():.3g}]  zeros {int((rec[:, 0] == 0).sum())}  {r.stderr.strip()}")
+    np.savez_compressed(os.path.join(ROOT, "tests", "golden", "ref_ir_cpq.npz"), **out)
+    print("tests/golden/ref_ir_cpq.npz written")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "cpq":
+        main_cpq()
+    elif len(sys.argv) > 1 and sys.argv[1] == "chrt":
+        main()
+    else:
+        main()
+        main_cpq()
