@@ -228,6 +228,9 @@ def nccl_logging(env):
     if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
         env["NCCL_DEBUG"] = "INFO"
         env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    # NCCL logs to stdout by default (also from its exit-time destructors, i.e. AFTER our last print): send its lines to
+    # stderr so that stdout carries the JSON line and nothing else
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 
 def respawn_under_torchrun(args):

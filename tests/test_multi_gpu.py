@@ -87,7 +87,8 @@ def _bench(args, env_extra=None, timeout=1500):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True, text=True, env=env, timeout=timeout)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.strip()]
-    return json.loads(lines[-1]), r  # the JSON line is the LAST line of stdout, whatever NCCL logged before it
+    assert lines and lines[-1].startswith("{"), "the JSON line must be the LAST line of stdout:\n" + r.stdout[-2000:] + "\n--- stderr ---\n" + r.stderr[-2000:]
+    return json.loads(lines[-1]), r
 
 
 @pytest.mark.gpu
