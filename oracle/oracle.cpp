@@ -108,7 +108,7 @@ struct Query {
     } else {
       hit = intersects(ray, n.box);
       tn = distmin(ray, n.box);
-      if (hit && n.segments_touched > 1) c.cold_loads++;
+      if ((hit || n.bounds_cold) && n.segments_touched > 1) c.cold_loads++;
     }
     if (!n.leaf) {
       if (hit && tn < best.t) {
@@ -367,7 +367,8 @@ uint64_t oracle_check_encoding(const TreeBytes* T, const scion_lnode* lnodes, ui
   };
   auto same3 = [](V3 a, const float* b) { return bits_of(a.x) == bits_of(b[0]) && bits_of(a.y) == bits_of(b[1]) && bits_of(a.z) == bits_of(b[2]); };
   if (d->family != SCION_FAMILY_BVH8) {
-    const bool quant = d->id == L_PBRT_Q16 || d->id == L_SG_EQ || d->id == L_SG_EQ_ALIGN16;
+    const bool q16 = d->id == L_PBRT_Q16 || d->id == L_PBRT_Q16_SOAOS;
+    const bool quant = q16 || d->id == L_SG_EQ || d->id == L_SG_EQ_ALIGN16;
     const float* wlo = lnodes[0].lo;
     const float* whi = lnodes[0].hi;
     struct Item { uint64_t l; Ref r; V3 elo, ehi; };
@@ -391,7 +392,7 @@ uint64_t oracle_check_encoding(const TreeBytes* T, const scion_lnode* lnodes, ui
       } else {
         uint32_t codes[6];
         float box[6];
-        oracle_quantize_roundtrip(d->id == L_PBRT_Q16 ? 1 : 0, wlo, whi, l.lo, l.hi, codes, box);
+        oracle_quantize_roundtrip(q16 ? 1 : 0, wlo, whi, l.lo, l.hi, codes, box);
         if (!same3(n.box.lo, box) || !same3(n.box.hi, box + 3)) fail("quantised bounds", it.l);
         // enclosure: decoded box must contain the original
         if (!(n.box.lo.x <= l.lo[0] && n.box.lo.y <= l.lo[1] && n.box.lo.z <= l.lo[2] && n.box.hi.x >= l.hi[0] && n.box.hi.y >= l.hi[1] && n.box.hi.z >= l.hi[2]))
@@ -415,7 +416,8 @@ uint64_t oracle_check_encoding(const TreeBytes* T, const scion_lnode* lnodes, ui
           L.elo = R.elo = lo2v;
           L.ehi = R.ehi = hi2v;
         }
-        if (d->id == L_PBRT || d->id == L_PBRT_ALIGN16 || d->id == L_PBRT_SOA || d->id == L_PBRT_Q16 || d->id == L_SG_EQ || d->id == L_SG_EQ_ALIGN16 || d->id == L_DOP14) {
+        if (d->id == L_PBRT || d->id == L_PBRT_ALIGN16 || d->id == L_PBRT_SOA || d->id == L_PBRT_SOAOS || d->id == L_PBRT_SOAOS_ALIGN16 || q16 || d->id == L_SG_EQ ||
+            d->id == L_SG_EQ_ALIGN16 || d->id == L_DOP14) {
           // index-referenced preorder builds: references ARE the preorder indices
           if (n.left.r != (uint64_t)l.left || n.right.r != (uint64_t)l.right) fail("child index", it.l);
         }
@@ -448,12 +450,12 @@ uint64_t oracle_check_encoding(const TreeBytes* T, const scion_lnode* lnodes, ui
         for (int k = 6; k >= 0; k--) { mlo[a] = fminf(w.lo[k][a], mlo[a]); mhi[a] = fmaxf(w.hi[k][a], mhi[a]); }
       }
       for (int k = 0; k < 8; k++) {
-        if (d->id == L_BVH8) {
+        if (d->id == L_BVH8 || d->id == L_BVH8_ALIGN16) {
           if (!same3(n.box[k].lo, w.lo[k]) || !same3(n.box[k].hi, w.hi[k])) fail("child bounds", (uint64_t)it.c);
         } else {
           uint32_t codes[6];
           float box[6];
-          oracle_quantize_roundtrip((d->id == L_BVH8_Q8 || d->id == L_BVH8_Q8_CI) ? 2 : 1, mlo, mhi, w.lo[k], w.hi[k], codes, box);
+          oracle_quantize_roundtrip((d->id == L_BVH8_Q8 || d->id == L_BVH8_Q8_CI || d->id == L_BVH8_Q8_ALIGN16 || d->id == L_BVH8_Q8_CI_ALIGN16) ? 2 : 1, mlo, mhi, w.lo[k], w.hi[k], codes, box);
           if (!same3(n.box[k].lo, box) || !same3(n.box[k].hi, box + 3)) fail("quantised child bounds", (uint64_t)it.c);
           if (w.child[k] != SCION_W_SENTINEL &&
               !(n.box[k].lo.x <= w.lo[k][0] && n.box[k].lo.y <= w.lo[k][1] && n.box[k].lo.z <= w.lo[k][2] && n.box[k].hi.x >= w.hi[k][0] && n.box[k].hi.y >= w.hi[k][1] && n.box[k].hi.z >= w.hi[k][2]))

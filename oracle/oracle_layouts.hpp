@@ -65,11 +65,16 @@ struct Node2 {  // view of the binary / DOP ADT:  BVH(low, high[, lo2, hi2]) = I
   uint64_t prim_begin = 0;
   uint32_t nprims = 0;
   uint32_t segments_touched = 1;
+  bool bounds_cold = false;  // part of the box lies behind `---`: every visit reads the second segment (pbrt-soaos-align16)
 };
 
 enum LayoutId {
   L_PBRT, L_PBRT_ALIGN16, L_PBRT_SOA, L_PBRT_POST, L_PBRT_Q16, L_SG_EQ, L_SG_EQ_ALIGN16, L_PTR, L_IDENTITY, L_SHARED_SLAB, L_DOP14,
-  L_BVH8, L_BVH8_Q8, L_BVH8_Q8_CI, L_BVH8_Q16, L_BVH8_Q16_CI, L_UNKNOWN
+  L_BVH8, L_BVH8_Q8, L_BVH8_Q8_CI, L_BVH8_Q16, L_BVH8_Q16_CI,
+  // authored for the paper's table, not in the reference corpus: offsets from OUR planner,
+  // which is pinned against the reference planner for the corpus and checked for these files through oracle/_ref/ref_probe
+  L_PBRT_SOAOS, L_PBRT_SOAOS_ALIGN16, L_PBRT_Q16_SOAOS, L_BVH8_ALIGN16, L_BVH8_Q8_ALIGN16, L_BVH8_Q8_CI_ALIGN16, L_BVH8_Q16_ALIGN16, L_BVH8_Q16_CI_ALIGN16,
+  L_UNKNOWN
 };
 struct LayoutDesc {
   const char* name;
@@ -85,11 +90,20 @@ static const LayoutDesc kLayouts[] = {
     {"shared-slab", L_SHARED_SLAB, 0, 29, 1},     {"dop14", L_DOP14, 1, 64, 1},       {"bvh8", L_BVH8, 2, 256, 1},
     {"bvh8-q8", L_BVH8_Q8, 2, 136, 1},    {"bvh8-q8-ci", L_BVH8_Q8_CI, 2, 104, 1},    {"bvh8-q16", L_BVH8_Q16, 2, 184, 1},
     {"bvh8-q16-ci", L_BVH8_Q16_CI, 2, 152, 1},
+    {"pbrt-soaos", L_PBRT_SOAOS, 0, 32, 1}, {"pbrt-soaos-align16", L_PBRT_SOAOS_ALIGN16, 0, 32, 1}, {"pbrt-q16-soaos", L_PBRT_Q16_SOAOS, 0, 16, 1},
+    {"bvh8-align16", L_BVH8_ALIGN16, 2, 256, 1}, {"bvh8-q8-align16", L_BVH8_Q8_ALIGN16, 2, 144, 1}, {"bvh8-q8-ci-align16", L_BVH8_Q8_CI_ALIGN16, 2, 112, 1},
+    {"bvh8-q16-align16", L_BVH8_Q16_ALIGN16, 2, 192, 1}, {"bvh8-q16-ci-align16", L_BVH8_Q16_CI_ALIGN16, 2, 160, 1},
 };
 inline const LayoutDesc* find_layout(const char* name) {
   for (auto& l : kLayouts)
     if (std::string(l.name) == name) return &l;
   return nullptr;
+}
+
+inline uint32_t find_stride(LayoutId id) {
+  for (auto& l : kLayouts)
+    if (l.id == id) return l.stride;
+  return 0;
 }
 
 inline Ref root_ref(const TreeBytes& t, LayoutId id) {
@@ -116,13 +130,37 @@ inline Node2 decode2(const TreeBytes& t, LayoutId id, const Ref& ref) {
       else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b + 192, 32)); }
       break;
     }
-    case L_PBRT_SOA: {  // authored: seg0 = low@0 high@96 (24 B); seg1 = union@0 nprims@32 (8 B with align=8)
+    case L_PBRT_SOA: case L_PBRT_SOAOS: {  // authored: seg0 = low@0 high@96 (24 B); seg1 = union@0 nprims@32 (8 B with align=8)
       uint64_t b0 = (t.seg_base[1][0] + I * 24) * 8, b1 = (t.seg_base[1][1] + I * 8) * 8;
       n.box = {read_v3(nodes, b0), read_v3(nodes, b0 + 96)};
       n.segments_touched = 2;
       uint32_t np = (uint32_t)read_bits(nodes, b1 + 32, 16);
       if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b1, 32); }
       else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b1, 32)); }
+      break;
+    }
+    case L_PBRT_SOAOS_ALIGN16: {  // authored: seg0 = low@0 nprims@96:16 (16 B); seg1 = high@0 union@96:32 (16 B)
+      uint64_t b0 = (t.seg_base[1][0] + I * 16) * 8, b1 = (t.seg_base[1][1] + I * 16) * 8;
+      n.box = {read_v3(nodes, b0), read_v3(nodes, b1)};
+      n.segments_touched = 2;
+      n.bounds_cold = true;
+      uint32_t np = (uint32_t)read_bits(nodes, b0 + 96, 16);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b1 + 96, 32); }
+      else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b1 + 96, 32)); }
+      break;
+    }
+    case L_PBRT_Q16_SOAOS: {  // authored: seg0 = bounds_q@0:96 (12 B); seg1 = nprims@0:4 union@4:28 (4 B)
+      uint64_t b0 = (t.seg_base[1][0] + I * 12) * 8, b1 = (t.seg_base[1][1] + I * 4) * 8;
+      V3 wl = glob_v3(t, 1), we = glob_v3(t, 2);
+      float rcp = 1.0f / 65535.0f;
+      float q[6];
+      for (int k = 0; k < 6; k++) q[k] = (float)(uint32_t)read_bits(nodes, b0 + 16 * k, 16);
+      n.box.lo = {wl.x + (q[0] * rcp) * we.x, wl.y + (q[1] * rcp) * we.y, wl.z + (q[2] * rcp) * we.z};
+      n.box.hi = {wl.x + (q[3] * rcp) * we.x, wl.y + (q[4] * rcp) * we.y, wl.z + (q[5] * rcp) * we.z};
+      n.segments_touched = 2;
+      uint32_t np = (uint32_t)read_bits(nodes, b1, 4);
+      if (np > 0) { n.leaf = true; n.nprims = np; n.prim_begin = read_bits(nodes, b1 + 4, 28); }
+      else { n.left.r = I + 1; n.right.r = (uint32_t)(I + read_bits(nodes, b1 + 4, 28)); }
       break;
     }
     case L_PBRT_POST: {  // pbrt_post.scion:5-19: low@0 high@96 {c_l@192,c_r@224 | p_o@192} nprims@256, stride 34
@@ -225,7 +263,7 @@ struct Node8 {  // BVH = Interior(children[8], lo[8], hi[8]) | Leaf(nprims, data
 };
 inline Node8 decode8(const TreeBytes& t, LayoutId id, uint64_t I) {
   Node8 n;
-  const bool ci = id == L_BVH8_Q8_CI || id == L_BVH8_Q16_CI;
+  const bool ci = id == L_BVH8_Q8_CI || id == L_BVH8_Q16_CI || id == L_BVH8_Q8_CI_ALIGN16 || id == L_BVH8_Q16_CI_ALIGN16;
   const uint32_t rb = ci ? 32 : 64;
   if ((I & 3) != 1) {  // bvh8.scion:13-15: `_ -> Leaf { O = I[7:hi]; nprims = I[2:6] + 1 }`
     n.leaf = true;
@@ -236,7 +274,7 @@ inline Node8 decode8(const TreeBytes& t, LayoutId id, uint64_t I) {
   const uint64_t idx = ci ? ((I >> 2) & ((1ull << 30) - 1)) : (I >> 2);  // `1 -> Interior from Interiors[I[2:hi]]`
   const uint8_t* nodes = t.buf[1];
   switch (id) {
-    case L_BVH8: {  // bvh8.scion:8-10: lo@0:768 hi@768:768 children@1536:512, stride 256
+    case L_BVH8: case L_BVH8_ALIGN16: {  // bvh8.scion:8-10: lo@0:768 hi@768:768 children@1536:512, stride 256
       uint64_t b = idx * 256 * 8;
       for (int k = 0; k < 8; k++) {
         n.box[k] = {read_v3(nodes, b + 96 * k), read_v3(nodes, b + 768 + 96 * k)};
@@ -245,8 +283,8 @@ inline Node8 decode8(const TreeBytes& t, LayoutId id, uint64_t I) {
       break;
     }
     default: {  // bvh8_q8*.scion:5-38 / bvh8_q16*.scion: mlo@0 mex@96 child_bounds@192 children after
-      const uint32_t q = (id == L_BVH8_Q8 || id == L_BVH8_Q8_CI) ? 8 : 16;
-      const uint32_t stride = id == L_BVH8_Q8 ? 136 : id == L_BVH8_Q8_CI ? 104 : id == L_BVH8_Q16 ? 184 : 152;
+      const uint32_t q = (id == L_BVH8_Q8 || id == L_BVH8_Q8_CI || id == L_BVH8_Q8_ALIGN16 || id == L_BVH8_Q8_CI_ALIGN16) ? 8 : 16;
+      const uint32_t stride = find_stride(id);  // 136 / 104 / 184 / 152, rounded up to 16 for the -align16 files (144 / 112 / 192 / 160)
       const float rcp = q == 8 ? 1 / 255.0f : 1 / 65535.0f;
       uint64_t b = idx * stride * 8;
       V3 mlo = read_v3(nodes, b), mex = read_v3(nodes, b + 96);

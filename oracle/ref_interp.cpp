@@ -20,7 +20,7 @@
 // links the reference with the dangling-`Frame&` bug of src/lower_internal.hpp:1073/:890 patched at build time (one
 // token, throw-away copy) and serves closest_point, whose lowering the unpatched reference corrupts.
 //
-// usage: ref_interp <corpus-layout> <chrt|cpq> <tree+queries.bin> <out.bin>
+// usage: ref_interp <corpus-layout | @family:/abs/layout.scion> <chrt|cpq> <tree+queries.bin> <out.bin>
 //        ref_interp --print-ir <corpus-layout> <chrt|cpq|cd>          (the lowered IR as text, for build-vs-build diffs)
 #include <array>
 #include <cfenv>
@@ -491,12 +491,29 @@ int main(int argc, char** argv) {
   try {
     const std::string name = print_only ? argv[2] : argv[1], alg = print_only ? argv[3] : argv[2];
     SourceSet ss;
-    ParseResult r = parse_corpus(corpus_files_for_pair(name, alg), &ss);
+    // <corpus-layout>, or an authored layout file of this repository: "@<bvh2|dop14|bvh8>:/abs/path/layout.scion" — the
+    // reference's own library + algorithm sources (same pairing rule as corpus_files_for_pair) with that layout file
+    std::vector<std::string> files;
+    if (!name.empty() && name[0] == '@') {
+      const size_t colon = name.find(':');
+      if (colon == std::string::npos) throw std::runtime_error("expected @<family>:<path>");
+      const std::string fam = name.substr(1, colon - 1), path = name.substr(colon + 1);
+      files.push_back("lib/geometry.scion");
+      if (fam == "dop14") files.push_back("lib/dop.scion");
+      if (alg == "chrt") files.push_back(fam == "bvh8" ? "alg/chrt8.scion" : fam == "dop14" ? "alg/chrt_dop14.scion" : "alg/chrt.scion");
+      else if (alg == "cpq") files.push_back(fam == "dop14" ? "alg/cpq_dop14.scion" : "alg/cpq.scion");
+      else throw std::runtime_error("unknown algorithm");
+      files.push_back(path);
+    } else {
+      files = corpus_files_for_pair(name, alg);
+    }
+    ParseResult r = parse_corpus(files, &ss);
     if (!r.ok()) throw std::runtime_error("parse failed");
     Program program = std::move(r.program);
     LayoutSpec* layout = nullptr;
     for (auto& l : program.layouts) if (program.find_build(l.name)) layout = &l;
-    if (!layout) throw std::runtime_error("no layout with a build block");
+    if (!layout && !program.layouts.empty()) layout = &program.layouts.back();  // authored files carry no build block (the destructors do not need one)
+    if (!layout) throw std::runtime_error("no layout");
     const AdtDecl* adt = layout_adt(program, *layout);
     if (!typecheck_traversal(program).empty()) throw std::runtime_error("typecheck_traversal reported diagnostics");
     if (!check_layout(*adt, *layout, program).empty()) throw std::runtime_error("check_layout reported diagnostics");

@@ -167,11 +167,13 @@ SCION_DEV RayCtx load_ray(const scion_ray* rays, uint64_t q) {
 template <class L, class TallyT>
 SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L::Ref& ref, typename L::Node& n, float& t_near, TallyT& tally) {
   float t_far;
-  if constexpr (L::kHasCold && SCION_COLD_EAGER != 0) L::decode_cold(T, ref, n);
+  // kBoundsCold: the box itself lies (partly) behind `---` (pbrt-soaos-align16), so the cold segment is part of every visit
+  constexpr bool kEager = L::kHasCold && (SCION_COLD_EAGER != 0 || L::kBoundsCold);
+  if constexpr (kEager) L::decode_cold(T, ref, n);
   if constexpr (L::kFamily == SCION_FAMILY_DOP14) {
     bool some = ray_aabb(ray, n.lo1, n.hi1, t_near, t_far);
     if (some) {
-      if constexpr (SCION_COLD_EAGER == 0) L::decode_cold(T, ref, n);
+      if constexpr (!kEager) L::decode_cold(T, ref, n);
       tally.cold();
       some = dop_diagonals(ray, n.lo2, n.hi2, t_near, t_far);
     }
@@ -180,8 +182,8 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
     const bool some = ray_aabb(ray, n.low, n.high, t_near, t_far);
     const bool hit = interval_intersects(ray, some, t_near, t_far);
     if constexpr (L::kHasCold) {
-      if (hit) {
-        if constexpr (SCION_COLD_EAGER == 0) L::decode_cold(T, ref, n);
+      if (hit || L::kBoundsCold) {
+        if constexpr (!kEager) L::decode_cold(T, ref, n);
         tally.cold();
       }
     }

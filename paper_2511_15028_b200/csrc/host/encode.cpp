@@ -153,7 +153,7 @@ void prepare(const scion_ltree& t, const std::string& name, Writer& w, EncodeJob
   j = EncodeJob();
   j.count = N;
   j.nodes = t.nodes.data();
-  if (name == "pbrt" || name == "pbrt-align16" || name == "pbrt-soa") {
+  if (name == "pbrt" || name == "pbrt-align16" || name == "pbrt-soa" || name == "pbrt-soaos" || name == "pbrt-soaos-align16") {
     check_preorder(t);
     w.copy_primitives(t, "primitives", "P");
     w.alloc("nodes", N);
@@ -170,9 +170,9 @@ void prepare(const scion_ltree& t, const std::string& name, Writer& w, EncodeJob
     j.post = post.data();
     j.f[0] = w.field("low"); j.f[1] = w.field("high"); j.f[2] = w.field("nprims"); j.f[3] = w.field("c_l"); j.f[4] = w.field("c_r"); j.f[5] = w.field("p_o");
     w.pt.root0 = post[0];
-  } else if (name == "pbrt-q16") {
-    require(N < (1ull << 28), "pbrt-q16: node count exceeds the u28 child offset");
-    require(t.tris.size() / 9 < (1ull << 28), "pbrt-q16: primitive count exceeds the u28 primitive offset");
+  } else if (name == "pbrt-q16" || name == "pbrt-q16-soaos") {
+    require(N < (1ull << 28), name + ": node count exceeds the u28 child offset");
+    require(t.tris.size() / 9 < (1ull << 28), name + ": primitive count exceeds the u28 primitive offset");
     check_preorder(t);
     w.copy_primitives(t, "primitives", "primitive_count");
     w.alloc("nodes", N);
@@ -241,8 +241,8 @@ void prepare(const scion_ltree& t, const std::string& name, Writer& w, EncodeJob
     }
     w.pt.root0 = 0;  // address of node 0
   } else if (name.rfind("bvh8", 0) == 0) {
-    const int qbits = name == "bvh8" ? 0 : (name.find("q8") != std::string::npos ? 8 : 16);
-    const int ref_bits = name.size() > 3 && name.compare(name.size() - 3, 3, "-ci") == 0 ? 32 : 64;
+    const int qbits = name.find("-q8") != std::string::npos ? 8 : (name.find("-q16") != std::string::npos ? 16 : 0);  // bvh8, bvh8-align16: f32 boxes
+    const int ref_bits = name.find("-ci") != std::string::npos ? 32 : 64;  // bvh8-q8-ci, bvh8-q8-ci-align16, ...
     require(t.has_wide, "8-wide layouts need a collapsed tree (scion_ltree_collapse8)");
     const uint64_t NI = t.wnodes.size();
     const uint64_t P = t.tris.size() / 9;

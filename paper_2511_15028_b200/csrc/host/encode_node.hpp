@@ -100,7 +100,7 @@ struct EncodeJob {
 
 SCION_ENC_HD float clamp_code(float f, float top) { return fmaxf(0.0f, fminf(f, top)); }
 
-// pbrt.scion:21-33 / pbrt_align16.scion / authored pbrt-soa: `build low; build high; build nprims [= 0];
+// pbrt.scion:21-33 / pbrt_align16.scion / authored pbrt-soa, pbrt-soaos, pbrt-soaos-align16: `build low; build high; build nprims [= 0];
 // c_o = R - this | p_o = append(data, nprims)`.  f: low high nprims c_o p_o
 SCION_ENC_HD void node_pbrt(const EncodeJob& j, uint64_t i) {
   const scion_lnode& n = j.nodes[i];
@@ -129,7 +129,7 @@ SCION_ENC_HD void node_pbrt_post(const EncodeJob& j, uint64_t i) {
     j.f[5].set(me, n.first_prim);
   }
 }
-// pbrt_q16.scion:49-73 — quantize_bounds: vu_floor((low - mlo) * rcp), vu_ceil((high - mlo) * rcp), clamp
+// pbrt_q16.scion:49-73 (and the authored pbrt-q16-soaos, same fields in two arrays) — quantize_bounds: vu_floor((low - mlo) * rcp), vu_ceil((high - mlo) * rcp), clamp
 // [0, 65535]; c0 = world_low, c1 = rcp = (1.0 / world_extent) * 65535.0.  f: bounds_q nprims c_offset p_offset
 SCION_ENC_HD void node_q16(const EncodeJob& j, uint64_t i) {
   const scion_lnode& n = j.nodes[i];

@@ -422,16 +422,18 @@ struct Emitter {
       if (!progress) throw LayoutError("cyclic derives in layout " + plan.layout_name);
     }
     // 3. ADT fields resolvable at this level
-    auto assign_fields = [&](const std::vector<Param>& fs) {
+    auto assign_fields = [&](const std::vector<Param>& fs, bool variant_fields) {
       for (auto& f : fs)
         if (bound.count(f.name) && !assigned.count(f.name)) {
-          if (assign_ok(f.name)) out << pad << "node__." << f.name << " = " << f.name << ";\n";
+          // a variant's own field is written inside its arm: when the arm is only reached in the cold pass, a HOT stored
+          // field it exposes (pbrt-soaos-align16: `nprims` sits with `low`, the split behind `---`) is written there too
+          if (assign_ok(f.name) || (variant_fields && mode == Mode::Cold)) out << pad << "node__." << f.name << " = " << f.name << ";\n";
           assigned.insert(f.name);
         }
     };
-    assign_fields(plan.adt->fields);
+    assign_fields(plan.adt->fields, false);
     if (arm_level && variant) {
-      assign_fields(variant->fields);
+      assign_fields(variant->fields, true);
       for (auto& f : variant->fields)
         if (!assigned.count(f.name) && !(mode == Mode::Hot && cold_names.count(f.name)))
           throw LayoutError("layout " + plan.layout_name + ": field '" + f.name + "' of variant " + variant->name + " is not defined");
@@ -514,6 +516,10 @@ struct Emitter {
     out << "  static constexpr int kFamily = " << (int)plan.family << ";\n";
     out << "  static constexpr uint32_t kMaxLeaf = " << plan.max_leaf << "u;\n";
     out << "  static constexpr bool kHasCold = " << (has_cold ? "true" : "false") << ";\n";
+    // the bounds the box test reads (chrt.scion:4 `node.low`, `node.high`) sit behind `---`: the traversal must read the
+    // cold segment BEFORE the test (pbrt-soaos-align16: {low, nprims} | {high, topology})
+    const bool bounds_cold = plan.family == Family::Bvh2 && (cold_names.count("low") || cold_names.count("high"));
+    out << "  static constexpr bool kBoundsCold = " << (bounds_cold ? "true" : "false") << ";\n";
     // buffers, records, slots
     for (auto& b : plan.buffers) {
       out << "  // buffer " << b.id << ": " << b.name << (b.is_arena ? " (arena, byte-offset references)" : b.is_global_array ? " (global array)" : "")

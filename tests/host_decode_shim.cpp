@@ -6,6 +6,11 @@
 
 #include "device/geometry.cuh"
 #include "gen/bvh8.cuh"
+#include "gen/bvh8_align16.cuh"
+#include "gen/bvh8_q16_align16.cuh"
+#include "gen/bvh8_q16_ci_align16.cuh"
+#include "gen/bvh8_q8_align16.cuh"
+#include "gen/bvh8_q8_ci_align16.cuh"
 #include "gen/bvh8_q16.cuh"
 #include "gen/bvh8_q16_ci.cuh"
 #include "gen/bvh8_q8.cuh"
@@ -16,7 +21,10 @@
 #include "gen/pbrt_align16.cuh"
 #include "gen/pbrt_post.cuh"
 #include "gen/pbrt_q16.cuh"
+#include "gen/pbrt_q16_soaos.cuh"
 #include "gen/pbrt_soa.cuh"
+#include "gen/pbrt_soaos.cuh"
+#include "gen/pbrt_soaos_align16.cuh"
 #include "gen/ptr.cuh"
 #include "gen/sg_eq.cuh"
 #include "gen/sg_eq_align16.cuh"
@@ -83,6 +91,7 @@ extern "C" int host_decode2(const char* layout, const TreeView* T, uint64_t ref,
 #define L2(NAME, T_) if (n == NAME) return dec2<g::T_>(T, ref, carried, f, u);
   L2("pbrt", L_pbrt) L2("pbrt-align16", L_pbrt_align16) L2("pbrt-soa", L_pbrt_soa) L2("pbrt-post", L_pbrt_post) L2("pbrt-q16", L_pbrt_q16)
   L2("sg-eq", L_sg_eq) L2("sg-eq-align16", L_sg_eq_align16) L2("ptr", L_ptr) L2("identity", L_identity) L2("shared-slab", L_shared_slab) L2("dop14", L_dop14)
+  L2("pbrt-soaos", L_pbrt_soaos) L2("pbrt-soaos-align16", L_pbrt_soaos_align16) L2("pbrt-q16-soaos", L_pbrt_q16_soaos)
 #undef L2
   return -1;
 }
@@ -90,6 +99,8 @@ extern "C" int host_decode8(const char* layout, const TreeView* T, uint64_t ref,
   std::string n = layout;
 #define L8(NAME, T_) if (n == NAME) return dec8<g::T_>(T, ref, f, u);
   L8("bvh8", L_bvh8) L8("bvh8-q8", L_bvh8_q8) L8("bvh8-q8-ci", L_bvh8_q8_ci) L8("bvh8-q16", L_bvh8_q16) L8("bvh8-q16-ci", L_bvh8_q16_ci)
+  L8("bvh8-align16", L_bvh8_align16) L8("bvh8-q8-align16", L_bvh8_q8_align16) L8("bvh8-q8-ci-align16", L_bvh8_q8_ci_align16) L8("bvh8-q16-align16", L_bvh8_q16_align16)
+  L8("bvh8-q16-ci-align16", L_bvh8_q16_ci_align16)
 #undef L8
   return -1;
 }
@@ -115,9 +126,10 @@ template <class L> void visit2(const TreeView& T, const scion::RayCtx& ray, cons
     if (some) { L::decode_cold(T, ref, n); some = scion::dop_diagonals(ray, n.lo2, n.hi2, tn, tf); }
     hit = scion::interval_intersects(ray, some, tn, tf);
   } else {
+    if constexpr (L::kBoundsCold) L::decode_cold(T, ref, n);  // part of the box lies behind `---`
     const bool some = scion::ray_aabb(ray, n.low, n.high, tn, tf);
     hit = scion::interval_intersects(ray, some, tn, tf);
-    if (hit) L::decode_cold(T, ref, n);
+    if (hit && !L::kBoundsCold) L::decode_cold(T, ref, n);
   }
   if (!hit) return;
   if (n.variant == L::kLeaf) { leaf_tris<L>(T, ray, n.data.begin, n.data.end, best); return; }
@@ -152,9 +164,12 @@ extern "C" int host_closest_hit(const char* layout, const TreeView* T, const flo
 #define L2(NAME, T_) if (n == NAME) return run_chrt<g::T_, false>(T, rays8, nrays, out);
   L2("pbrt", L_pbrt) L2("pbrt-align16", L_pbrt_align16) L2("pbrt-soa", L_pbrt_soa) L2("pbrt-post", L_pbrt_post) L2("pbrt-q16", L_pbrt_q16)
   L2("sg-eq", L_sg_eq) L2("sg-eq-align16", L_sg_eq_align16) L2("ptr", L_ptr) L2("identity", L_identity) L2("shared-slab", L_shared_slab) L2("dop14", L_dop14)
+  L2("pbrt-soaos", L_pbrt_soaos) L2("pbrt-soaos-align16", L_pbrt_soaos_align16) L2("pbrt-q16-soaos", L_pbrt_q16_soaos)
 #undef L2
 #define L8(NAME, T_) if (n == NAME) return run_chrt<g::T_, true>(T, rays8, nrays, out);
   L8("bvh8", L_bvh8) L8("bvh8-q8", L_bvh8_q8) L8("bvh8-q8-ci", L_bvh8_q8_ci) L8("bvh8-q16", L_bvh8_q16) L8("bvh8-q16-ci", L_bvh8_q16_ci)
+  L8("bvh8-align16", L_bvh8_align16) L8("bvh8-q8-align16", L_bvh8_q8_align16) L8("bvh8-q8-ci-align16", L_bvh8_q8_ci_align16) L8("bvh8-q16-align16", L_bvh8_q16_align16)
+  L8("bvh8-q16-ci-align16", L_bvh8_q16_ci_align16)
 #undef L8
   return -1;
 }

@@ -47,7 +47,8 @@ def test_oracle_cd_equals_brute_force(built, oracle):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("layout", ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14"])
+@pytest.mark.parametrize("layout", ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14",
+                                    "pbrt-soaos", "pbrt-soaos-align16", "pbrt-q16-soaos"])
 def test_gpu_cd_matches_oracle(built, oracle, layout):
     sb = built
     sa, sbn = two_meshes(sb, 24)

@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 ALL = ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14",
-       "bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
+       "bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci", "pbrt-soaos", "pbrt-soaos-align16", "pbrt-q16-soaos", "bvh8-align16", "bvh8-q8-align16",
+       "bvh8-q8-ci-align16", "bvh8-q16-align16", "bvh8-q16-ci-align16"]
 
 
 def test_device_encode_fails_loudly_without_a_device(built):

@@ -11,9 +11,9 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 SAMPLE = 1 << 20
-BINARY = ["pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "ptr", "identity", "dop14"]
-WIDE = ["bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
-EXACT_BOXES = {"pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "ptr", "identity"}  # f32 boxes of the logical tree, binary visit order
+BINARY = ["pbrt", "pbrt-align16", "pbrt-soa", "pbrt-soaos", "pbrt-soaos-align16", "pbrt-post", "pbrt-q16", "pbrt-q16-soaos", "sg-eq", "sg-eq-align16", "ptr", "identity", "dop14"]
+WIDE = ["bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci", "bvh8-align16", "bvh8-q8-align16", "bvh8-q8-ci-align16", "bvh8-q16-align16", "bvh8-q16-ci-align16"]
+EXACT_BOXES = {"pbrt", "pbrt-align16", "pbrt-soa", "pbrt-soaos", "pbrt-soaos-align16", "pbrt-post", "ptr", "identity"}  # f32 boxes of the logical tree, binary visit order
 
 
 @pytest.fixture(scope="module")

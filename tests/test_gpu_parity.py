@@ -67,7 +67,8 @@ def world(request, built, oracle):
 
 def layout_names():
     return ["pbrt", "pbrt-align16", "pbrt-soa", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "ptr", "identity", "shared-slab", "dop14", "bvh8", "bvh8-q8",
-            "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
+            "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci", "pbrt-soaos", "pbrt-soaos-align16", "pbrt-q16-soaos", "bvh8-align16", "bvh8-q8-align16",
+            "bvh8-q8-ci-align16", "bvh8-q16-align16", "bvh8-q16-ci-align16"]
 
 
 @pytest.mark.parametrize("layout", layout_names())

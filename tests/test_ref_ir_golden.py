@@ -14,6 +14,10 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CORPUS = ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14",
           "bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
+# authored here (PAPER.md:854-857, :872-880 table points + the SoA point of BASELINE config 2): the reference's own front-end,
+# planner and destructor specialiser compile OUR .scion file (ref_interp "@family:/path"), same pin as the corpus
+AUTHORED = ["pbrt-soa", "pbrt-soaos", "pbrt-soaos-align16", "pbrt-q16-soaos"] + \
+    ["bvh8-align16", "bvh8-q8-align16", "bvh8-q8-ci-align16", "bvh8-q16-align16", "bvh8-q16-ci-align16"]
 
 
 @pytest.fixture(scope="module")
@@ -38,11 +42,11 @@ def test_fixture_is_meaningful(built, gold):
         # zero direction components, finite tmax, -0.0 and a root miss are all in the set
         assert (rays["dx"] == 0).any() and np.isfinite(rays["tmax"]).any() and (np.signbit(rays["dx"]) & (rays["dx"] == 0)).any()
         # cross-layout invariant of the reference: every layout of the corpus gives the same hit set
-        for layout in CORPUS:
+        for layout in CORPUS + AUTHORED:
             assert np.array_equal(np.isfinite(gold[f"{tag}:t:{layout}"]), np.isfinite(t)), layout
 
 
-@pytest.mark.parametrize("layout", CORPUS)
+@pytest.mark.parametrize("layout", CORPUS + AUTHORED)
 def test_oracle_reproduces_the_reference_ir(built, oracle, gold, layout):
     sb = built
     for tag, lt, rays in trees(sb, gold):
@@ -54,7 +58,7 @@ def test_oracle_reproduces_the_reference_ir(built, oracle, gold, layout):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("layout", CORPUS)
+@pytest.mark.parametrize("layout", CORPUS + AUTHORED)
 def test_kernels_reproduce_the_reference_ir(built, gold, layout):
     import torch
     sb = built

@@ -19,6 +19,18 @@ INTERP_FX = os.path.join(ROOT, "oracle", "_ref", "ref_interp_fx")
 BINARY = ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14"]
 CORPUS = ["identity", "ptr", "pbrt", "pbrt-align16", "pbrt-post", "pbrt-q16", "sg-eq", "sg-eq-align16", "shared-slab", "dop14",
           "bvh8", "bvh8-q8", "bvh8-q8-ci", "bvh8-q16", "bvh8-q16-ci"]
+# layouts AUTHORED in this repository (the paper's table points that the reference corpus does not ship, PAPER.md:854-857,
+# :872-880, and the SoA point of BASELINE config 2): the reference's own front-end, planner and destructor specialiser
+# compile OUR .scion file (ref_interp "@family:/path"), so they are pinned through the reference's IR like the corpus
+AUTHORED_BINARY = ["pbrt-soa", "pbrt-soaos", "pbrt-soaos-align16", "pbrt-q16-soaos"]
+AUTHORED_WIDE = ["bvh8-align16", "bvh8-q8-align16", "bvh8-q8-ci-align16", "bvh8-q16-align16", "bvh8-q16-ci-align16"]
+
+
+def interp_name(layout):
+    if layout in CORPUS:
+        return layout
+    fam = "bvh8" if layout.startswith("bvh8") else "bvh2"
+    return f"@{fam}:" + os.path.join(ROOT, "paper_2511_15028_b200", "layouts", layout.replace("-", "_") + ".scion")
 
 
 def wstr(f, s):
@@ -85,12 +97,12 @@ def main():
             index.setdefault(t.tobytes(), i)
         out[f"{tag}:rays"] = rays.view(np.float32).reshape(-1, 8).copy()
         out[f"{tag}:scene"] = np.array([12, 5] if tag == "terrain" else [8, 3])
-        for layout in CORPUS:
+        for layout in CORPUS + AUTHORED_BINARY + AUTHORED_WIDE:
             pt = lt.encode(layout)
             with tempfile.TemporaryDirectory() as td:
                 fin, fout = os.path.join(td, "in.bin"), os.path.join(td, "out.bin")
                 write_input(fin, pt, rays)
-                r = subprocess.run([INTERP, layout, "chrt", fin, fout], capture_output=True, text=True)
+                r = subprocess.run([INTERP, interp_name(layout), "chrt", fin, fout], capture_output=True, text=True)
                 if r.returncode != 0:
                     raise SystemExit(f"{layout}: {r.stderr}")
                 rec = np.fromfile(fout, np.float32).reshape(-1, 10)
@@ -138,12 +150,12 @@ def main_cpq():
         tris = np.ascontiguousarray(lt.triangles(), np.float32).reshape(-1, 9)
         out[f"{tag}:points"] = pts.copy()
         out[f"{tag}:scene"] = np.array({"terrain": [12, 5], "sphere": [8, 3], "cloud": [600, 4]}[tag])
-        for layout in BINARY:
+        for layout in BINARY + AUTHORED_BINARY:
             pt = lt.encode(layout)
             with tempfile.TemporaryDirectory() as td:
                 fin, fout = os.path.join(td, "in.bin"), os.path.join(td, "out.bin")
                 write_input(fin, pt, as_rays(pts))
-                r = subprocess.run([INTERP_FX, layout, "cpq", fin, fout], capture_output=True, text=True)
+                r = subprocess.run([INTERP_FX, interp_name(layout), "cpq", fin, fout], capture_output=True, text=True)
                 if r.returncode != 0:
                     raise SystemExit(f"{layout}: {r.stderr}")
                 rec = np.fromfile(fout, np.float32).reshape(-1, 10)
