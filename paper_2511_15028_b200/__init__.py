@@ -17,6 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
+_ENV_HIT_VARIANT = int(os.environ.get("SCION_HIT_VARIANT", "0"))
 LIB_PATH = os.environ.get("SCION_B200_LIB", os.path.join(_HERE, "libscion_b200.so"))  # env override: kernel-variant experiments
 
 
@@ -557,6 +558,8 @@ class DeviceTree:
 
     # device-pointer entry points (asynchronous on `stream`)
     def closest_hit(self, d_rays: int, n: int, d_hits: int, d_status: int = 0, d_counters: int = 0, variant: int = 0, stream: int = 0):
+        if variant == 0 and _ENV_HIT_VARIANT:  # experiments: run a whole bench / profile on a selectable kernel variant
+            variant = _ENV_HIT_VARIANT
         _check(lib().scion_closest_hit(self._h, d_rays, n, d_hits, d_status or None, d_counters or None, variant, stream or None))
 
     def closest_point(self, d_points: int, n: int, d_out: int, d_status: int = 0, d_counters: int = 0, variant: int = 0, stream: int = 0):

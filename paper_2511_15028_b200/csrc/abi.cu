@@ -113,6 +113,15 @@ int scion::finish_dtree(scion_dtree* t) {
     CUDA_OK(t->counters.grow());
   }
   fill_view(*t);
+  // side treelet of the top levels for the layouts whose kernel can stage it (north_star: top levels in shared memory via
+  // TMA bulk copies).  The image is complete on the device here (every caller has synchronised).
+  if (t->kernels->build_treelet && t->header.nbuf > 1 && t->header.count[1] > 0 && t->header.count[1] < (1ull << 31)) {
+    uint32_t slots = 0;
+    CUDA_OK(cudaSetDevice(t->device));
+    CUDA_OK(t->kernels->build_treelet(t->view, &t->treelet, &slots));
+    t->view.treelet = t->treelet;
+    t->view.treelet_slots = slots;
+  }
   return SCION_OK;
 }
 
@@ -697,6 +706,7 @@ void scion_dtree_free(scion_dtree* t) {
   }
   t->counters.destroy();
   if (t->cd_scratch.ptr) cudaFree(t->cd_scratch.ptr);
+  if (t->treelet) cudaFree(t->treelet);
   if (t->image && t->owns_image) cudaFree(t->image);
   delete t;
 }

@@ -39,6 +39,9 @@ struct CdArgs {  // collision detection: two trees of the same layout on the sam
 };
 typedef cudaError_t (*cd_fn)(const CdArgs&, int* overflow_bits);
 typedef cudaError_t (*occupancy_fn)(int* blocks_per_sm, int* regs, size_t* smem);
+// builds the side treelet of the top levels (device/treelet.cuh) of a tree that is complete on the device: allocates
+// *d_out (caller frees) and reports the slot count; synchronous
+typedef cudaError_t (*treelet_fn)(const TreeView& view, uint8_t** d_out, uint32_t* slots);
 
 struct KernelEntry {
   const char* layout;
@@ -46,6 +49,7 @@ struct KernelEntry {
   launch_fn closest_point;  // null for 8-wide layouts (corpus.cpp:83)
   occupancy_fn hit_occupancy;
   cd_fn collide;  // null for 8-wide layouts (corpus.cpp:86)
+  treelet_fn build_treelet;  // null unless the layout supports the staged top levels (traverse.cuh treelet_ok)
 };
 
 const KernelEntry* find_kernels(const char* layout);

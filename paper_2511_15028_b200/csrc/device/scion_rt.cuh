@@ -60,6 +60,10 @@ struct TreeView {
   uint32_t glob[SCION_MAX_GLOBALS][4];
   uint64_t root0;      // root reference, primary component
   float root_carried[6];  // tree-carried components of the root reference (shared-slab)
+  // side treelet of the top levels (device/treelet.cuh; a cache, not part of the layout): `treelet_slots` records in
+  // heap order followed by their main-array indices, or null
+  const uint8_t* treelet;
+  uint32_t treelet_slots;
 };
 
 // --------------------------------------------------------------------------- vectors

@@ -114,7 +114,7 @@ struct WorkFetcherT {
           const unsigned long long seen = chunk_base;  // end of this warp's previous chunk: a lower bound of the global progress, no extra load
 #endif
           const unsigned long long rem = seen < n ? n - seen : 0ull;
-          if (rem * SCION_GUIDED_DEN < (unsigned long long)gridDim.x * (kBlockThreads / 32) * SCION_GUIDED_NUM * (unsigned long long)kChunk) take = 32u;
+          if (rem * SCION_GUIDED_DEN < (unsigned long long)gridDim.x * (blockDim.x >> 5) * SCION_GUIDED_NUM * (unsigned long long)kChunk) take = 32u;
           }
 #endif
           base = atomicAdd(next, (unsigned long long)take);
@@ -262,11 +262,11 @@ SCION_DEV uint64_t opaque(uint64_t q) {
 // nor the thread's base address occupies a register.  Entries beyond the shared-memory share go
 // to a local array (rare: the window holds the first 32 references of a 4-byte-reference layout).
 // ------------------------------------------------------------------------------------------
-template <class Entry, int kWindowBytes = kStackSmemBytesPerBlock>
+template <class Entry, int kWindowBytes = kStackSmemBytesPerBlock, int BT = kBlockThreads>
 struct LaneStack {
   static_assert(sizeof(Entry) % 4 == 0, "stack entries are stored as 32-bit words");
   static constexpr int kWords = (int)sizeof(Entry) / 4;
-  static constexpr uint32_t kSlot = (uint32_t)kBlockThreads * 4u * (uint32_t)kWords;
+  static constexpr uint32_t kSlot = (uint32_t)BT * 4u * (uint32_t)kWords;
   static constexpr int kFit = (int)((uint32_t)kWindowBytes / kSlot);
   static constexpr int kSmem = kFit < SCION_STACK_DEPTH ? kFit : SCION_STACK_DEPTH;
   static_assert(kSmem >= 1, "the shared-memory window must hold at least one entry per thread");
@@ -277,12 +277,12 @@ struct LaneStack {
     uint32_t w[kWords];
     memcpy(w, &e, sizeof(Entry));
 #pragma unroll
-    for (int i = 0; i < kWords; i++) asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + (uint32_t)(i * 4 * kBlockThreads)), "r"(w[i]));
+    for (int i = 0; i < kWords; i++) asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + (uint32_t)(i * 4 * BT)), "r"(w[i]));
   }
   SCION_DEV static void load(uint32_t a, Entry& e) {
     uint32_t w[kWords];
 #pragma unroll
-    for (int i = 0; i < kWords; i++) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(a + (uint32_t)(i * 4 * kBlockThreads)));
+    for (int i = 0; i < kWords; i++) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(a + (uint32_t)(i * 4 * BT)));
     memcpy(&e, w, sizeof(Entry));
   }
 };
@@ -373,55 +373,70 @@ SCION_DEV uint32_t coop_triangles2(const TreeView& T, bool own, float ox, float 
 // kInner steps run back to back; only then does the warp look for idle lanes (refill) and for
 // lanes waiting with a leaf (cooperative PRIM phase).
 //
-// STAGE > 0 (experimental variant 2): the first STAGE node records of the array are copied into
-// shared memory with one TMA bulk copy (cp.async.bulk + mbarrier, SASS UBLKCP) at CTA start and
-// served from there by the emitted decode<true>().  In a preorder array that prefix is the root,
-// the left spine and the left-most subtrees.  Measured effect: see DESIGN.md §5.
+// TL > 0 (kernel variant 2, north_star "stage the BVH's top levels into shared memory with TMA bulk copies"): the top TL
+// levels of the tree — a side treelet in heap order built once per tree by build_treelet_kernel (treelet.cuh): slot s
+// holds the record of one node and its index in the main array, its children sit in slots 2s+1 / 2s+2 — are copied
+// into shared memory with ONE cp.async.bulk per CTA (mbarrier completion; SASS UBLKCP) and visits of those nodes are
+// served by LDS instead of a global load.  A reference with bit 31 set designates a treelet slot; the children of a
+// slot in the last staged level are ordinary main-array references (the "escape").  The visit order, every decode
+// and every test are unchanged (the records are byte copies), so results and counters are identical.
+// The treelet is a cache, not part of the layout: it is not counted in bytes/prim.
+// BT / WIN / MINB: CTA size, shared-memory stack window and CTAs per SM — a treelet is staged once per CTA, so the
+// staged variant runs larger CTAs than the default 128 threads (see launch_hit_t).
 // ------------------------------------------------------------------------------------------
-template <class L, bool COUNT, int STAGE = 0>
-__global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
+template <class L>
+inline constexpr bool kTreeletOk = L::kCanFetch && !L::kHasCold && L::kFamily == SCION_FAMILY_BVH2 && std::is_same<typename L::Ref, uint32_t>::value;
+template <class L>
+constexpr bool treelet_ok() {
+  return kTreeletOk<L>;
+}
+constexpr uint32_t kTreeletBit = 0x80000000u;
+template <class L, bool COUNT, int TL = 0, int BT = kBlockThreads, int WIN = kStackSmemBytesPerBlock, int MINB = SCION_MINB2>
+__global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
-  using LS = LaneStack<Ref>;
+  using LS = LaneStack<Ref, WIN, BT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Stage stage;
-  if constexpr (STAGE > 0) {
+  constexpr uint32_t kTlSlots = TL > 0 ? (1u << TL) - 1u : 0u;
+  uint32_t tl_rec = 0, tl_orig = 0;  // shared-space addresses of the staged records / main-array indices
+  bool tl_on = false;
+  if constexpr (TL > 0) {
+    static_assert(kTreeletOk<L>, "the treelet needs single-vector-load records and 32-bit index references");
     __shared__ __align__(8) unsigned long long mbar;
-    unsigned char* dst = smem_raw + kStackSmemBytesPerBlock;
-    const uint64_t have = T.count[L::kStageBuffer];
-    const uint32_t cnt = (uint32_t)(have < (uint64_t)STAGE ? have : (uint64_t)STAGE);
-    const uint32_t bytes = cnt * L::kStageStride;  // multiple of 16 (kCanStage)
+    constexpr uint32_t kRecBytes = kTlSlots * L::kStageStride;
+    constexpr uint32_t kBytes = (kRecBytes + kTlSlots * 4u + 15u) & ~15u;
+    tl_rec = (uint32_t)__cvta_generic_to_shared(smem_raw + WIN);
+    tl_on = T.treelet != nullptr && T.treelet_slots == kTlSlots;
     const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
       asm volatile("fence.mbarrier_init.release.cluster;");
     }
     __syncthreads();
-    if (threadIdx.x == 0 && bytes > 0) {
-      const uint8_t* src = T.buf[L::kStageBuffer];
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       (uint32_t)__cvta_generic_to_shared(dst)),
-                   "l"(src), "r"(bytes), "r"(mb)
-                   : "memory");
-    }
-    if (bytes > 0) {
+    if (tl_on) {
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(kBytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(tl_rec), "l"(T.treelet), "r"(kBytes), "r"(mb)
+                     : "memory");
+      }
       uint32_t done = 0;
       while (!done)
         asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(mb), "r"(0u) : "memory");
     }
-    stage.base = dst;
-    stage.count = cnt;
   }
-  __shared__ CoopScratch2 coop[kBlockThreads / 32];
-  __shared__ RayStash stash[kBlockThreads];          // ray direction: only the leaf phase needs it
-  __shared__ unsigned long long stash_q[kBlockThreads];  // query index: only the retire path needs it
-  __shared__ uint2 stash_leaf[kBlockThreads];        // parked primitive range [begin, end)
+  __shared__ CoopScratch2 coop[BT / 32];
+  __shared__ RayStash stash[BT];          // ray direction: only the leaf phase needs it
+  __shared__ unsigned long long stash_q[BT];  // query index: only the retire path needs it
+  __shared__ uint2 stash_leaf[BT];        // parked primitive range [begin, end)
   Ref deep[LS::kDeep];
   uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
   asm volatile("" : "+r"(window));  // opaque: kept in a register instead of being re-derived (S2R CgaCtaId + 3) at every push and pop
   uint32_t top = window + threadIdx.x * 4u;
+  if constexpr (TL > 0) {  // addresses of the staged treelet as constant offsets from the register that holds `window`
+    tl_rec = window + (uint32_t)WIN;
+    tl_orig = tl_rec + kTlSlots * (uint32_t)L::kStageStride;
+  }
   uint32_t my_leaf = (uint32_t)__cvta_generic_to_shared(&stash_leaf[threadIdx.x]);
   asm volatile("" : "+r"(my_leaf));  // one register; re-deriving the address costs 7 instructions in a divergent branch
   WorkFetcher work;
@@ -462,7 +477,11 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
     }
   };
 
-  constexpr bool kHot = SCION_HOT_L1 > 0 && STAGE == 0 && L::kCanFetch && !L::kHasCold && std::is_same<Ref, uint32_t>::value;
+  constexpr bool kHot = SCION_HOT_L1 > 0 && TL == 0 && L::kCanFetch && !L::kHasCold && std::is_same<Ref, uint32_t>::value;
+  const Ref root = [&]() -> Ref {
+    if constexpr (TL > 0) return tl_on ? (Ref)kTreeletBit : L::root(T);  // slot 0 of the treelet is the root
+    else return L::root(T);
+  }();
   constexpr uint32_t kHotBit = 0x80000000u;
   auto step = [&]() {
     typename L::Node node;
@@ -481,8 +500,31 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
         child_flag = (uint32_t)(node.right - idx) >= (uint32_t)SCION_HOT_L1 ? kHotBit : 0u;
       }
       cur = idx;
+    } else if constexpr (TL > 0) {
+      typename L::Fetched w;
+      const bool in_t = ((uint32_t)cur & kTreeletBit) != 0u;
+      const uint32_t slot = (uint32_t)cur & ~kTreeletBit;
+      Ref idx = cur;
+      if (in_t) {
+        constexpr int NW = (int)(sizeof(typename L::Fetched) / 4);
+        const uint32_t a = tl_rec + slot * (uint32_t)L::kStageStride;  // tl_rec = window + WIN: one IMAD off the register that holds `window`
+#pragma unroll
+        for (int i = 0; i < NW; i += 4)
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(w.w[i]), "=r"(w.w[i + 1]), "=r"(w.w[i + 2]), "=r"(w.w[i + 3]) : "r"(a + 4u * (uint32_t)i));
+        uint32_t o;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(o) : "r"(tl_orig + slot * 4u));
+        idx = (Ref)o;
+      } else {
+        L::fetch(T, idx, w);
+      }
+      L::decode_fetched(T, idx, w, node);
+      const uint32_t c = 2u * slot + 1u;
+      if (in_t && c + 1u < kTlSlots) {  // both children are staged too (an interior node always has both)
+        node.left = (Ref)(kTreeletBit | c);
+        node.right = (Ref)(kTreeletBit | (c + 1u));
+      }
     } else {
-      L::template decode<(STAGE > 0)>(T, cur, node, stage);
+      L::decode(T, cur, node);
     }
 #if SCION_PF_NEXT == 1
     if constexpr (std::is_integral<Ref>::value) L::template prefetch<1>(T, (Ref)(cur + 1));
@@ -525,7 +567,9 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
       if constexpr (kPrefetch) {
         // L2-prefetch the pushed child, but only when it is far: a right sibling a few records away shares
         // its lines with what this lane just fetched, and every prefetch costs an L1 tag lookup per lane
-        if constexpr (std::is_integral<Ref>::value && SCION_PF_MIN > 0) {
+        if constexpr (TL > 0) {
+          if (((uint32_t)node.right & kTreeletBit) == 0u) L::prefetch(T, node.right);  // staged children need no prefetch
+        } else if constexpr (std::is_integral<Ref>::value && SCION_PF_MIN > 0) {
           if ((uint64_t)(node.right - cur) > (uint64_t)SCION_PF_MIN) L::prefetch(T, node.right);
         } else {
           L::prefetch(T, node.right);
@@ -564,7 +608,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
         best_prim = SCION_MISS_PRIM;
         tally.reset();
         top = window + threadIdx.x * 4u;
-        cur = L::root(T);
+        cur = root;
         if constexpr (kHot) cur = (Ref)((uint32_t)cur | kHotBit);
         mode = kNode;
       }
@@ -585,421 +629,6 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB2) chrt2_kernel(const
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// closest_hit, binary family, TWO rays per lane (kernel v14, SCION_DUAL=1) — for layouts whose record is one vector load
-// (L::kCanFetch: pbrt, pbrt-align16, pbrt-q16, sg-eq-align16).
-//
-// chrt2_kernel is bound by the dependent chain of one step (pop -> address -> record load -> decode -> test -> push/pop)
-// times the visits of a ray, with the register file fixing how many chains an SM holds.  Here every lane
-// owns two independent rays ("slots").  A step of slot s consumes the record that was fetched at the END of slot s's
-// previous step and ends by issuing the fetch of its next record (emitted L::fetch / L::decode_fetched), so the load of
-// one slot is in flight while the other slot's step executes.  Everything else is the v11 machine run once per slot:
-// same visit order, same predicated push/pop, same cooperative leaf phase, same results bit for bit.  The
-// counter-instrumented build stays on chrt2_kernel (identical results by construction, tests compare the two).
-// ------------------------------------------------------------------------------------------
-#ifndef SCION_DUAL
-#define SCION_DUAL 0
-#endif
-#ifndef SCION_MINB2D
-#define SCION_MINB2D 6
-#endif
-#ifndef SCION_DUAL_MERGED
-#define SCION_DUAL_MERGED 0
-#endif
-#ifndef SCION_STACK_SMEM_D  /* shared-memory stack window of one CTA, both slots together */
-#define SCION_STACK_SMEM_D (16 * 1024)
-#endif
-template <class L>
-constexpr bool dual_ok() {
-  return L::kCanFetch && !L::kHasCold && L::kFamily != SCION_FAMILY_DOP14 && std::is_integral<typename L::Ref>::value;
-}
-template <class L>
-__global__ void __launch_bounds__(kBlockThreads, SCION_MINB2D) chrt2d_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
-                                                                scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
-                                                                scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
-  using Ref = typename L::Ref;
-  constexpr int kSlotWindow = SCION_STACK_SMEM_D / 2;
-  using LS = LaneStack<Ref, kSlotWindow>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ CoopScratch2 coop[kBlockThreads / 32];
-  __shared__ RayStash stash[2][kBlockThreads];
-  __shared__ unsigned long long stash_q[2][kBlockThreads];
-  __shared__ uint2 stash_leaf[2][kBlockThreads];
-  Ref deep[2][LS::kDeep];
-  uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
-  asm volatile("" : "+r"(window));
-  (void)tune; (void)counters;
-  WorkFetcher work;
-  struct Slot {
-    RayCtx ray;
-    float best_t;
-    uint32_t best_prim;
-    Ref cur;
-    uint32_t top;
-    int mode;
-    typename L::Fetched rec;
-  } S[2];
-#pragma unroll
-  for (int s = 0; s < 2; s++) {
-    S[s].ray = make_ray(0, 0, 0, 0, 1, 1, 1);
-    S[s].best_t = 0;
-    S[s].best_prim = 0;
-    S[s].cur = L::root(T);
-    S[s].top = window + (uint32_t)s * (uint32_t)kSlotWindow + threadIdx.x * 4u;
-    S[s].mode = kFetch;
-  }
-
-  auto retire = [&](auto SI, uint32_t st) {
-    constexpr int s = decltype(SI)::value;
-    const uint64_t qq = opaque(stash_q[s][threadIdx.x]);
-    store_hit(hits + qq, S[s].best_t, S[s].best_prim);
-    if (status) status[qq] = st;
-    S[s].mode = kFetch;
-  };
-  auto pop_or_retire = [&](auto SI) {
-    constexpr int s = decltype(SI)::value;
-    const uint32_t rel = S[s].top - (window + (uint32_t)s * (uint32_t)kSlotWindow);
-    if (rel - LS::kSlot < LS::kSmemBytes) {
-      S[s].top -= LS::kSlot;
-      LS::load(S[s].top, S[s].cur);
-      S[s].mode = kNode;
-    } else if (rel < LS::kSlot) {
-      retire(SI, SCION_Q_OK);
-    } else {
-      S[s].top -= LS::kSlot;
-      S[s].cur = deep[s][rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
-      S[s].mode = kNode;
-    }
-  };
-  // one node step of slot s; ends by putting the next record's load in flight
-  auto step = [&](auto SI) {
-    constexpr int s = decltype(SI)::value;
-    Slot& X = S[s];
-    typename L::Node node;
-    L::decode_fetched(T, X.cur, X.rec, node);
-    float t_near, t_far;
-    const bool some = ray_aabb(X.ray, node.low, node.high, t_near, t_far);
-    const bool hit = interval_intersects(X.ray, some, t_near, t_far);
-    const bool leaf = node.variant == L::kLeaf;
-    const bool p_prim = hit && leaf && (uint32_t)node.data.begin < (uint32_t)node.data.end;
-    const bool p_push = hit && !leaf && t_near < X.best_t;
-    const uint32_t rel = X.top - (window + (uint32_t)s * (uint32_t)kSlotWindow);
-    const bool fast = p_push ? rel < LS::kSmemBytes : rel - LS::kSlot < LS::kSmemBytes;
-    if (!(fast || p_prim)) {
-      if (p_push) {
-        const uint32_t depth = rel / LS::kSlot;
-        if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
-          retire(SI, SCION_Q_STACK_OVERFLOW);
-        } else {
-          deep[s][depth - (uint32_t)LS::kSmem] = node.right;
-          X.top += LS::kSlot;
-          X.cur = node.left;
-        }
-      } else {
-        pop_or_retire(SI);
-      }
-    } else if (p_prim) {
-      const uint32_t my_leaf = (uint32_t)__cvta_generic_to_shared(&stash_leaf[s][threadIdx.x]);
-      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(my_leaf), "r"((uint32_t)node.data.begin), "r"((uint32_t)node.data.end));
-      X.mode = kPrim;
-    } else if (p_push) {
-      LS::store(X.top, node.right);
-      if constexpr (kPrefetch) L::prefetch(T, node.right);
-      X.top += LS::kSlot;
-      X.cur = node.left;
-    } else {
-      X.top -= LS::kSlot;
-      LS::load(X.top, X.cur);
-    }
-    if (X.mode == kNode) L::fetch(T, X.cur, X.rec);
-  };
-  auto refill = [&](auto SI, bool force) {
-    constexpr int s = decltype(SI)::value;
-    Slot& X = S[s];
-    const unsigned idle = __ballot_sync(kFullMask, X.mode == kFetch);
-    if (idle && (force || __popc(idle) >= kRefillMin || work.exhausted)) {
-      uint64_t nq;
-      if (!work.exhausted && work.refill(X.mode == kFetch, next, n, nq)) {
-        X.ray = load_ray(rays, nq);
-        stash[s][threadIdx.x] = RayStash{X.ray.dx, X.ray.dy, X.ray.dz, 0u};
-        stash_q[s][threadIdx.x] = nq;
-        X.best_t = scion::inf();
-        X.best_prim = SCION_MISS_PRIM;
-        X.top = window + (uint32_t)s * (uint32_t)kSlotWindow + threadIdx.x * 4u;
-        X.cur = L::root(T);
-        X.mode = kNode;
-        L::fetch(T, X.cur, X.rec);
-      }
-    }
-  };
-  auto prims = [&](auto SI, bool nothing_else) {
-    constexpr int s = decltype(SI)::value;
-    Slot& X = S[s];
-    const unsigned pmask = __ballot_sync(kFullMask, X.mode == kPrim);
-    if (pmask && (__popc(pmask) >= kPrimMin || nothing_else)) {
-      const bool own = X.mode == kPrim;
-      uint2 range = make_uint2(0u, 0u);
-      if (own) range = stash_leaf[s][threadIdx.x];
-      uint32_t prim_i = range.x;
-      coop_triangles2<L>(T, own, X.ray.ox, X.ray.oy, X.ray.oz, X.ray.tmax, stash[s] + (threadIdx.x & ~31u), prim_i, range.y, X.best_t, X.best_prim,
-                         coop[threadIdx.x >> 5]);
-      if (own) {
-        pop_or_retire(SI);
-        if (X.mode == kNode) L::fetch(T, X.cur, X.rec);
-      }
-    }
-  };
-  using I0 = std::integral_constant<int, 0>;
-  using I1 = std::integral_constant<int, 1>;
-
-  for (;;) {
-#pragma unroll 1
-    for (int k = 0; k < kInner; k++) {
-      if (S[0].mode == kNode) step(I0{});
-      if (S[1].mode == kNode) step(I1{});
-    }
-#if SCION_DUAL_MERGED  // thresholds on the two slots of the warp together (a slot's own events are half as frequent)
-    const bool many_idle = __popc(__ballot_sync(kFullMask, S[0].mode == kFetch)) + __popc(__ballot_sync(kFullMask, S[1].mode == kFetch)) >= kRefillMin;
-#else
-    const bool many_idle = false;
-#endif
-    refill(I0{}, many_idle);
-    refill(I1{}, many_idle);
-    if (work.exhausted && __ballot_sync(kFullMask, S[0].mode != kFetch || S[1].mode != kFetch) == 0u) break;
-    bool nothing_else = __ballot_sync(kFullMask, S[0].mode == kNode || S[1].mode == kNode) == 0u;
-#if SCION_DUAL_MERGED
-    nothing_else = nothing_else || __popc(__ballot_sync(kFullMask, S[0].mode == kPrim)) + __popc(__ballot_sync(kFullMask, S[1].mode == kPrim)) >= kPrimMin;
-#endif
-    prims(I0{}, nothing_else);
-    prims(I1{}, nothing_else);
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// closest_hit, binary family, PAIR step (kernel v10) — for layouts whose reference is a plain
-// integer and whose node has no cold segment.
-//
-// chrt2_kernel visits one node per step: one dependent memory round trip per node visit, and the
-// warp waits for its slowest lane every time (profiles/r1_ncu_v8_c5_q16.txt: two out of three
-// node loads of a warp include a DRAM access).  The closest-point kernel showed what that costs:
-// peeking both children in one step (two loads in flight) is 1.41x faster than one decode per
-// step.  Here a step EXPANDS an interior node: it fetches the records of BOTH children together,
-// tests both boxes, continues with the left child at once and pushes the right child together
-// with the outcome of its (pure) box test:
-//     entry = (a, b, key)   interior: a/b = left/right reference, key = t_near
-//                           leaf:     a/b = primitive range,    key = t_near | sign bit
-//                           box missed / empty leaf: key = +inf ("dead": never passes the cull)
-// The reference tests the right child when it is visited — `intersects(ray, box)` (pure) and, for
-// interiors, `distmin(ray, box) < best[0]` with the `best` of that moment: the pure part is
-// evaluated at push time, the cull `t_near < best` is applied at pop time with the then-current
-// `best`, so every decision is the reference's (same argument as the 8-wide deferred cull, SURVEY
-// Appendix A).  Dead entries are pushed too, so the stack occupancy — and with it the overflow status
-// and the max_stack counter — is the reference's at every moment.  A popped entry needs no memory
-// access at all: dependent round trips per ray drop from (visits) to (visits / 2).
-//
-// MEASURED AND REJECTED (kept behind SCION_PAIR_STEP=1, bit-exact incl. counters and overflow status on
-// the whole GPU suite): C5 probe pbrt-q16 1293 Mrays/s against 2190 for the one-node step; pbrt 1320 vs
-// 2144, sg-eq 629 vs 963.  A 12-byte entry leaves 8 (12 KB window) stack entries in shared memory where
-// incoherent rays average 13, so pushes and pops go to local memory; 16 / 20 KB windows: 1368 / 1463
-// (7 CTAs), 24 KB: 1128 (L1 starved).  In the one-node kernel the left child is the next record
-// (same sector half of the time) and the right child was L2-prefetched when it was pushed — the
-// round trips that matter were already short.
-// ------------------------------------------------------------------------------------------
-#ifndef SCION_PAIR_STEP
-#define SCION_PAIR_STEP 0
-#endif
-#ifndef SCION_MINB2X
-#define SCION_MINB2X 8
-#endif
-#ifndef SCION_INNERX
-#define SCION_INNERX 2
-#endif
-#ifndef SCION_PRIM_MINX
-#define SCION_PRIM_MINX 6
-#endif
-template <class Ref>
-struct PairEntry {
-  Ref a, b;
-  float key;
-};
-template <class L>
-constexpr bool pair_step_ok() {
-  return SCION_PAIR_STEP != 0 && L::kFamily == SCION_FAMILY_BVH2 && !L::kHasCold && std::is_integral<typename L::Ref>::value;
-}
-
-#if SCION_PAIR_STEP
-template <class L, bool COUNT>
-__global__ void __launch_bounds__(kBlockThreads, SCION_MINB2X) chrt2x_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
-                                                               scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
-                                                               scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
-  using Ref = typename L::Ref;
-  using Entry = PairEntry<Ref>;
-  using LS = LaneStack<Entry>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ CoopScratch2 coop[kBlockThreads / 32];
-  __shared__ RayStash stash[kBlockThreads];
-  __shared__ unsigned long long stash_q[kBlockThreads];
-  __shared__ uint2 stash_leaf[kBlockThreads];
-  Entry deep[LS::kDeep];
-  uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
-  asm volatile("" : "+r"(window));
-  uint32_t top = window + threadIdx.x * 4u;
-  uint32_t my_leaf = (uint32_t)__cvta_generic_to_shared(&stash_leaf[threadIdx.x]);
-  asm volatile("" : "+r"(my_leaf));
-  WorkFetcher work;
-  (void)tune;
-  Tally<COUNT> tally;
-  int mode = kFetch;
-  RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
-  float best_t = 0;
-  uint32_t best_prim = 0;
-  Ref ea = L::root(T), eb = ea;  // children of the node this lane expands next (mode == kNode)
-  constexpr uint32_t kLeafBit = 0x80000000u;
-
-  auto retire = [&](uint32_t st) {
-    const uint64_t qq = opaque(stash_q[threadIdx.x]);
-    store_hit(hits + qq, best_t, best_prim);
-    if (status) status[qq] = st;
-    tally.store(counters, qq);
-    mode = kFetch;
-  };
-  auto park = [&](uint32_t b, uint32_t e) {
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(my_leaf), "r"(b), "r"(e));
-    mode = kPrim;
-  };
-  // next pending entry that passes its deferred test, or retire the query
-  auto pop_next = [&]() {
-    for (;;) {
-      const uint32_t rel = top - window;
-      Entry e;
-      if (rel - LS::kSlot < LS::kSmemBytes) {
-        top -= LS::kSlot;
-        LS::load(top, e);
-      } else if (rel < LS::kSlot) {
-        retire(SCION_Q_OK);
-        return;
-      } else {
-        top -= LS::kSlot;
-        e = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
-      }
-      const uint32_t kb = f2u(e.key);
-      if (kb & kLeafBit) {  // a leaf whose box the ray intersects: no distance cull (chrt.scion:10)
-        park((uint32_t)e.a, (uint32_t)e.b);
-        return;
-      }
-      if (e.key < best_t) {  // interior: `distmin(ray, box) < best[0]` with the best of THIS moment; dead entries are +inf
-        ea = e.a;
-        eb = e.b;
-        mode = kNode;
-        return;
-      }
-    }
-  };
-  // outcome of visiting one node whose box test is (hit, t_near): what to do with it now / what to remember
-  auto classify = [&](const typename L::Node& nd, bool hit, float t_near, Ref& a, Ref& b, float& key) {
-    const bool leaf = nd.variant == L::kLeaf;
-    if (leaf) {
-      a = (Ref)nd.data.begin;
-      b = (Ref)nd.data.end;
-      key = (hit && (uint32_t)nd.data.begin < (uint32_t)nd.data.end) ? u2f(f2u(t_near) | kLeafBit) : scion::inf();
-    } else {
-      a = nd.left;
-      b = nd.right;
-      key = hit ? t_near : scion::inf();
-    }
-  };
-
-  auto step = [&]() {
-    typename L::Node nl, nr;
-    L::decode(T, ea, nl);
-    L::decode(T, eb, nr);
-    if (COUNT) { tally.visit(); tally.visit(); }
-    float tl, tr;
-    const bool hl = node_test<L>(T, ray, ea, nl, tl, tally);
-    const bool hr = node_test<L>(T, ray, eb, nr, tr, tally);
-    Ref la, lb, ra, rb;
-    float lkey, rkey;
-    classify(nl, hl, tl, la, lb, lkey);
-    classify(nr, hr, tr, ra, rb, rkey);
-    // push the right child (always: reference discipline = pop self, push right, push left)
-    const uint32_t rel = top - window;
-    if (COUNT) tally.stack(rel / LS::kSlot + 2u);
-    if (rel < LS::kSmemBytes) {
-      LS::store(top, Entry{ra, rb, rkey});
-    } else {
-      const uint32_t depth = rel / LS::kSlot;
-      if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
-        retire(SCION_Q_STACK_OVERFLOW);
-        return;
-      }
-      deep[depth - (uint32_t)LS::kSmem] = Entry{ra, rb, rkey};
-    }
-    top += LS::kSlot;
-    // visit the left child now
-    const uint32_t lk = f2u(lkey);
-    if (lk & kLeafBit) {
-      park((uint32_t)la, (uint32_t)lb);
-    } else if (lkey < best_t) {
-      ea = la;
-      eb = lb;
-    } else {
-      pop_next();
-    }
-  };
-
-  for (;;) {
-#pragma unroll 1
-    for (int k = 0; k < SCION_INNERX; k++) {
-      if (mode == kNode) step();
-    }
-    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
-    if (idle && (__popc(idle) >= kRefillMin || work.exhausted)) {
-      uint64_t nq;
-      if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
-        ray = load_ray(rays, nq);
-        stash[threadIdx.x] = RayStash{ray.dx, ray.dy, ray.dz, 0u};
-        stash_q[threadIdx.x] = nq;
-        best_t = scion::inf();
-        best_prim = SCION_MISS_PRIM;
-        tally.reset();
-        top = window + threadIdx.x * 4u;
-        // the root is visited here (one node, not a pair)
-        const Ref root = L::root(T);
-        typename L::Node nd;
-        L::decode(T, root, nd);
-        tally.visit();
-        float t0;
-        const bool h0 = node_test<L>(T, ray, root, nd, t0, tally);
-        Ref a, b;
-        float key;
-        classify(nd, h0, t0, a, b, key);
-        if (f2u(key) & kLeafBit) {
-          park((uint32_t)a, (uint32_t)b);
-        } else if (key < best_t) {
-          ea = a;
-          eb = b;
-          mode = kNode;
-        } else {
-          retire(SCION_Q_OK);
-        }
-      }
-      if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
-    }
-    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
-    if (pmask && (__popc(pmask) >= SCION_PRIM_MINX || __ballot_sync(kFullMask, mode == kNode) == 0u)) {
-      const bool own = mode == kPrim;
-      uint2 range = make_uint2(0u, 0u);
-      if (own) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(range.x), "=r"(range.y) : "r"(my_leaf));
-      uint32_t prim_i = range.x;
-      const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, range.y, best_t,
-                                               best_prim, coop[threadIdx.x >> 5]);
-      if (COUNT) tally.prim_tests += done;
-      if (own) pop_next();
-    }
-  }
-}
-
-#endif  // SCION_PAIR_STEP
 
 // ------------------------------------------------------------------------------------------
 // closest_hit, 8-wide family.  Stack entries are (child reference, t_near); the cull
@@ -1534,3 +1163,5 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
 }
 
 }  // namespace scion
+
+#include "traverse_experiments.cuh"

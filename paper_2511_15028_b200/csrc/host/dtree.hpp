@@ -115,6 +115,7 @@ struct scion_dtree {
   bool owns_image = true;
   scion::ImageHeader header{};
   scion::TreeView view{};
+  uint8_t* treelet = nullptr;  // side treelet of the top levels (device/treelet.cuh), built once in finish_dtree; a cache, not part of the image
   scion::CounterPool counters;  // one work-fetch counter per launch in flight
   // staging for the host entry points
   static constexpr int kSlots = 4;  // staging slots of the host entry points: H2D(k+1) || kernel(k) || D2H(k-1)

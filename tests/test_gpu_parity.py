@@ -236,21 +236,46 @@ def test_stack_overflow_is_a_query_error(built, oracle, torch_cuda, layout):
         dt.free()
 
 
-def test_staged_prefix_variant_is_identical(built, torch_cuda, world):
-    """experimental kernel variant 2 (TMA bulk copy of the node array's first records into shared memory,
-    served by decode<true>) must return exactly the default kernel's records"""
+def test_treelet_variant_is_identical(built, torch_cuda, world):
+    """kernel variant 2 (north_star: the top levels of the tree staged in shared memory by one TMA bulk copy per CTA — a
+    side treelet in heap order built once per tree, device/treelet.cuh — and served by LDS) must return exactly the
+    default kernel's records and per-query status, for every layout that supports it, on host- and device-encoded trees"""
     sb, torch = built, torch_cuda
     n = world["rays"].shape[0]
     d_rays = dev_bytes(torch, world["rays"])
-    for layout in ("pbrt", "pbrt-q16"):
-        dt = world["lt"].encode(layout).upload(0)
-        a = torch.zeros(n * 8, dtype=torch.uint8, device="cuda:0")
-        b = torch.zeros(n * 8, dtype=torch.uint8, device="cuda:0")
-        dt.closest_hit(d_rays.data_ptr(), n, a.data_ptr())
-        dt.closest_hit(d_rays.data_ptr(), n, b.data_ptr(), variant=2)
-        torch.cuda.synchronize()
-        assert torch.equal(a, b), layout
-        dt.free()
+    for layout in ("pbrt", "pbrt-align16", "pbrt-q16", "sg-eq-align16"):
+        for dt in (world["lt"].encode(layout).upload(0), world["lt"].encode_device(layout, 0)):
+            a = torch.zeros(n * 8, dtype=torch.uint8, device="cuda:0")
+            b = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+            sa = torch.full((n,), 7, dtype=torch.int32, device="cuda:0")
+            sb_ = torch.full((n,), 9, dtype=torch.int32, device="cuda:0")
+            dt.closest_hit(d_rays.data_ptr(), n, a.data_ptr(), sa.data_ptr())
+            dt.closest_hit(d_rays.data_ptr(), n, b.data_ptr(), sb_.data_ptr(), variant=2)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b), layout
+            assert torch.equal(sa, sb_), layout
+            dt.free()
+
+
+def test_treelet_variant_on_a_tiny_tree(built, torch_cuda):
+    """trees shallower than the staged levels (empty treelet slots) and a single-leaf tree"""
+    sb, torch = built, torch_cuda
+    for grid in (1, 2, 5):
+        scene = sb.Scene.terrain(grid, 3)
+        lt = scene.build_sah(32, 4)
+        lo, hi = scene.bounds()
+        cam = sb.default_camera(lo, hi, True, 32, 32)
+        rays = sb.gen_primary_host(cam, 0, 1024)
+        d_rays = dev_bytes(torch, rays)
+        for layout in ("pbrt", "pbrt-q16"):
+            dt = lt.encode(layout).upload(0)
+            a = torch.zeros(1024 * 8, dtype=torch.uint8, device="cuda:0")
+            b = torch.full((1024 * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+            dt.closest_hit(d_rays.data_ptr(), 1024, a.data_ptr())
+            dt.closest_hit(d_rays.data_ptr(), 1024, b.data_ptr(), variant=2)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b), (grid, layout)
+            dt.free()
 
 
 def test_two_rays_per_lane_variant_is_identical(built, torch_cuda, world):

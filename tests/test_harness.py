@@ -47,7 +47,7 @@ def test_verify_matrix(built):
                 if alg == "chrt":
                     assert rep["mismatches_vs_identity_oracle"] == 0, rep
                 total += 1
-    assert total == 2 * (16 + 11)
+    assert total == 2 * (24 + 14)  # 24 layouts (15 corpus + 9 authored), 14 of them binary (closest_point)
     # fault injection: one corrupted c_o byte must be reported
     rep = verify_cli.verify("pbrt", "chrt", "terrain:24", 4096, corrupt=(1, 24, 1))
     assert rep["mismatches_vs_identity_oracle"] >= 1 and len(rep["first_offenders"]) <= 10

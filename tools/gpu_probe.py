@@ -157,7 +157,7 @@ if __name__ == "__main__":
                 print(f"  {layout:10s} {kind:9s} {nr / ms / 1e3:8.1f} Mrays/s  visits/ray {nv:.1f} tris/ray {npt:.1f} maxstack {ctr['max_stack'].max()} mean stack {ctr['max_stack'].mean():.1f} -> {nr * nv / ms / 1e6:.1f} Gvisits/s", flush=True)
             dt.free()
         sys.exit(0)
-    if "--stage" in sys.argv:  # TMA-staged prefix (variant 2) vs default: identical results? timing?
+    if "--stage" in sys.argv:  # TMA-staged top-levels treelet (variant 2) vs default: identical results? timing?
         for G in (708, 2236):
             scene = sb.Scene.terrain(G, seed=1)
             lt = scene.build_sah(32, 4)

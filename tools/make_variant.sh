@@ -10,7 +10,7 @@ mkdir -p build/var_$NAME ../bin
 OBJS=$(ls build/*.o)
 for id in $IDENTS; do
   STAGE=""
-  if [ "$id" = pbrt_q16 ] || [ "$id" = pbrt ]; then STAGE="-DSCION_STAGE_NODES=512 -DSCION_DUAL=2"; fi
+  if [ "$id" = pbrt_q16 ] || [ "$id" = pbrt ]; then STAGE="-DSCION_DUAL=2"; fi
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++20 -ccbin /usr/bin/g++ \
     -fmad=false -prec-div=true -prec-sqrt=true -ftz=false -diag-suppress 20281,1886,549 \
     -Xcompiler -fPIC,-fopenmp,-ffp-contract=off -I../../include -I. $STAGE $FLAGS -c build/inst_$id.cu -o build/var_$NAME/inst_$id.o &
@@ -18,5 +18,5 @@ for id in $IDENTS; do
   OBJS="$OBJS build/var_$NAME/inst_$id.o"
 done
 wait
-/usr/local/cuda/bin/nvcc -shared -o ../bin/libscion_$NAME.so $OBJS -Xcompiler -fopenmp -lgomp -cudart shared 2>/dev/null
+/usr/local/cuda/bin/nvcc -shared -o ../bin/libscion_$NAME.so $OBJS -Xcompiler -fopenmp -lgomp -ldl -cudart shared 2>/dev/null
 echo "built bin/libscion_$NAME.so"
