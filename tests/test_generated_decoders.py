@@ -16,7 +16,7 @@ SHIM = os.path.join(ROOT, "tests", "_host_decode_shim.so")
 
 class TreeView(C.Structure):  # mirror of scion::TreeView (device/scion_rt.cuh)
     _fields_ = [("buf", C.c_void_p * 6), ("seg_base", (C.c_uint64 * 4) * 6), ("count", C.c_uint64 * 6), ("glob", (C.c_uint32 * 4) * 12),
-                ("root0", C.c_uint64), ("root_carried", C.c_float * 6)]
+                ("root0", C.c_uint64), ("root_carried", C.c_float * 6), ("treelet", C.c_void_p), ("treelet_slots", C.c_uint32)]
 
 
 @pytest.fixture(scope="module")
