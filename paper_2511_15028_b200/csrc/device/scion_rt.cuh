@@ -315,8 +315,10 @@ template <class T, int N, class I> SCION_HOSTDEV T get_lane(const vec<T, N>& v, 
 template <int NW>
 struct Words {
   uint32_t w[NW];
+  static constexpr int kWords = NW;
+  template <int I>
+  SCION_HOSTDEV uint32_t word() const { return w[I]; }
 };
-
 SCION_HOSTDEV uint32_t ld32(const uint8_t* p) {
 #if defined(__CUDA_ARCH__)
   return __ldg(reinterpret_cast<const uint32_t*>(p));
@@ -400,6 +402,33 @@ SCION_HOSTDEV void prefetch_to(const void* p) {
 // load_record for the records of the *cold* part of a tree (experiment SCION_HOT_L1, traverse.cuh): same bytes, but the
 // line is not allocated in L1, so that the few thousand records of the top levels stay there.  Only for records that
 // are one 16- or 32-byte vector load.
+// A record staged in shared memory by 16-byte async copies (traverse.cuh chrt8s_kernel): 16-byte chunk c of this lane's
+// record lives at base + c * kChunkPitch (the 32 lanes' copies of one chunk are contiguous, so a warp's LDS.128 of one
+// chunk is conflict free).  Same word<I>() interface as Words: the extraction templates below serve both.
+template <int NW, int PITCH>
+struct StagedRecord {
+#if defined(__CUDA_ARCH__)
+  // shared-space byte address of this lane's chunk 0.  The loads are NON-volatile asm: a pure function of the address for
+  // the compiler, so repeated extractions of one chunk are merged and dead ones removed.  What orders them behind the
+  // asynchronous copies is a data dependence: the kernel passes `addr` through an opaque asm after cp.async.wait_all.
+  uint32_t addr;
+  template <int I>
+  SCION_HOSTDEV uint32_t word() const {
+    uint32_t x, y, z, w;
+    asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr + (uint32_t)((I / 4) * PITCH)));
+    return I % 4 == 0 ? x : (I % 4 == 1 ? y : (I % 4 == 2 ? z : w));
+  }
+#else
+  const uint8_t* base;
+  template <int I>
+  SCION_HOSTDEV uint32_t word() const {
+    uint32_t v;
+    memcpy(&v, base + (I / 4) * PITCH + (I % 4) * 4, 4);
+    return v;
+  }
+#endif
+  static constexpr int kWords = NW;
+};
 template <int BYTES, int ALIGN>
 SCION_HOSTDEV void load_record_na(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
   static_assert((BYTES == 16 && ALIGN % 16 == 0) || (BYTES == 32 && ALIGN % 32 == 0), "single vector load records only");
@@ -508,29 +537,29 @@ SCION_HOSTDEV void load_record_generic(const uint8_t* p, Words<(BYTES + 3) / 4>&
 
 // constant-offset field extraction: the inverse of write_bits_raw
 // (/root/reference/proj/src/bits.cpp:21-36), little-endian, LSB first
-template <int OFF, int W, int NW>
-SCION_HOSTDEV uint32_t ext32(const Words<NW>& r) {
+template <int OFF, int W, class Src>
+SCION_HOSTDEV uint32_t ext32(const Src& r) {
   static_assert(W >= 1 && W <= 32, "ext32 width");
   constexpr int i = OFF / 32, s = OFF % 32;
-  static_assert(i < NW, "field outside record");
+  static_assert(i < Src::kWords, "field outside record");
   if constexpr (s + W <= 32) {
-    if constexpr (W == 32) return r.w[i];
-    else return (r.w[i] >> s) & (uint32_t)((1ull << W) - 1ull);
+    if constexpr (W == 32) return r.template word<i>();
+    else return (r.template word<i>() >> s) & (uint32_t)((1ull << W) - 1ull);
   } else {
-    static_assert(i + 1 < NW, "field outside record");
-    return ((r.w[i] >> s) | (r.w[i + 1] << (32 - s))) & (uint32_t)((1ull << W) - 1ull);
+    static_assert(i + 1 < Src::kWords, "field outside record");
+    return ((r.template word<i>() >> s) | (r.template word<i + 1>() << (32 - s))) & (uint32_t)((1ull << W) - 1ull);
   }
 }
-template <int OFF, int W, int NW>
-SCION_HOSTDEV uint64_t ext64(const Words<NW>& r) {
+template <int OFF, int W, class Src>
+SCION_HOSTDEV uint64_t ext64(const Src& r) {
   static_assert(W > 32 && W <= 64, "ext64 width");
-  uint64_t lo = ext32<OFF, 32, NW>(r);
-  uint64_t hi = ext32<OFF + 32, W - 32, NW>(r);
+  uint64_t lo = ext32<OFF, 32>(r);
+  uint64_t hi = ext32<OFF + 32, W - 32>(r);
   return lo | (hi << 32);
 }
-template <int OFF, int NW>
-SCION_HOSTDEV float extf(const Words<NW>& r) {
-  return u2f(ext32<OFF, 32, NW>(r));
+template <int OFF, class Src>
+SCION_HOSTDEV float extf(const Src& r) {
+  return u2f(ext32<OFF, 32>(r));
 }
 
 template <class T> SCION_HOSTDEV T glob(const TreeView& T_, int i);

@@ -849,6 +849,210 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8) chrt8_kernel(const
 }
 
 // ------------------------------------------------------------------------------------------
+// closest_hit, 8-wide family, STAGED RECORD (kernel v16) — for layouts whose interior record starts on a 16-byte
+// boundary (L::kCanSlot: the paper's `-align16` files and the 256-byte f32 record).
+//
+// chrt8_kernel decodes a whole 104-256-byte record into registers: 124-128 registers, 4 CTAs/SM, 16 warps/SM, issue
+// slots 55 % busy with nothing else saturated (profiles/r1_ncu_v11_c5_q8ci.txt: `wait` + `long_scoreboard` stalls of a
+// kernel that has 4 warps per scheduler to hide them).  Here a lane copies its record into shared memory with 16-byte
+// asynchronous copies (cp.async = SASS LDGSTS: global -> shared without passing through registers; chunk c of the 32
+// lanes of a warp is contiguous, so reading a chunk back is a conflict-free LDS.128) and then decodes ONE child slot at a
+// time from there with the emitted decode_slot<K>() (same expressions as decode(), dead slots removed by the compiler).
+// Slots are visited 7 -> 0 and a passing child is pushed at once, so the entries pop in slot order (chrt8.scion:7) and no
+// per-slot arrays stay live; the lowest passing slot is continued with in registers.  Same visit order, same deferred
+// `t_near < best` cull at pop, same counters and overflow rule as chrt8_kernel (tests compare the two bit for bit).
+// ------------------------------------------------------------------------------------------
+#ifndef SCION_MINB8S
+#define SCION_MINB8S 6
+#endif
+#ifndef SCION_STACK_SMEM8S
+#define SCION_STACK_SMEM8S (16 * 1024)
+#endif
+#ifndef SCION_CPASYNC_CG  /* 1: cp.async.cg (L2 only) instead of .ca (allocate in L1) */
+#define SCION_CPASYNC_CG 0
+#endif
+constexpr int kStackSmemBytesPerBlock8S = SCION_STACK_SMEM8S;
+template <class L>
+constexpr size_t staged_record_bytes() {  // shared memory of one CTA for the lanes' record copies
+  if constexpr (L::kCanSlot) return (size_t)((L::kSlotUsedBytes + 15u) / 16u) * 16u * (size_t)kBlockThreads;
+  else return 0;
+}
+template <class L, bool COUNT>
+__global__ void __launch_bounds__(kBlockThreads, SCION_MINB8S) chrt8s_kernel(const TreeView T, const scion_ray* __restrict__ rays, uint64_t n,
+                                                                scion_hit* __restrict__ hits, uint32_t* __restrict__ status,
+                                                                scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
+  static_assert(L::kCanSlot && L::kVariantInRef, "staged-record kernel: 16-byte aligned interior records, leaf variant in the reference");
+  using Ref = typename L::Ref;
+  using Entry = WideEntry<Ref>;
+  using LS = LaneStack<Entry, kStackSmemBytesPerBlock8S>;
+  constexpr int kChunks = (int)((L::kSlotUsedBytes + 15u) / 16u);
+  constexpr int kPitch = 16 * kBlockThreads;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ CoopScratch2 coop[kBlockThreads / 32];
+  __shared__ RayStash stash[kBlockThreads];
+  __shared__ unsigned long long stash_q[kBlockThreads];
+  Entry deep[LS::kDeep];
+  uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  asm volatile("" : "+r"(window));
+  uint32_t top = window + threadIdx.x * 4u;
+  uint32_t rec_addr = (uint32_t)__cvta_generic_to_shared(smem_raw + kStackSmemBytesPerBlock8S + threadIdx.x * 16u);  // this lane's chunk 0
+  WorkFetcher work;
+  (void)tune;
+  Tally<COUNT> tally;
+  int mode = kFetch;
+  RayCtx ray = make_ray(0, 0, 0, 0, 1, 1, 1);
+  float best_t = 0;
+  uint32_t best_prim = 0, prim_i = 0, prim_end = 0;
+  Ref cur = L::root(T);
+
+  auto retire = [&](uint32_t st) {
+    const uint64_t qq = opaque(stash_q[threadIdx.x]);
+    store_hit(hits + qq, best_t, best_prim);
+    if (status) status[qq] = st;
+    tally.store(counters, qq);
+    mode = kFetch;
+  };
+  auto enter = [&]() {  // `cur` was just chosen: park it if the reference itself says it is a leaf
+    mode = kNode;
+    if (L::ref_variant(cur) == L::kLeaf) {
+      typename L::Node leaf;
+      L::decode(T, cur, leaf);  // reference-only arm: no memory access
+      prim_i = (uint32_t)leaf.data.begin;
+      prim_end = (uint32_t)leaf.data.end;
+      mode = prim_i < prim_end ? kPrim : -1;  // -1: empty leaf, take the next entry
+    }
+  };
+  auto pop_next = [&]() {  // next pending entry whose deferred cull `t_near < best` still passes, or retire
+    for (;;) {
+      const uint32_t rel = top - window;
+      Entry e;
+      if (rel - LS::kSlot < LS::kSmemBytes) {
+        top -= LS::kSlot;
+        LS::load(top, e);
+      } else if (rel < LS::kSlot) {
+        retire(SCION_Q_OK);
+        return;
+      } else {
+        top -= LS::kSlot;
+        e = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
+      }
+      if (e.t_near < best_t) {
+        cur = e.ref;
+        enter();
+        if (mode >= 0) return;
+      }
+    }
+  };
+  auto step = [&]() {
+    {  // stage the record: kChunks 16-byte asynchronous copies, global -> shared
+      const uint8_t* p = L::slot_record(T, cur);
+#pragma unroll
+      for (int c = 0; c < kChunks; c++) {
+#if SCION_CPASYNC_CG
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(rec_addr + (uint32_t)(c * kPitch)), "l"(p + 16 * c) : "memory");
+#else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(rec_addr + (uint32_t)(c * kPitch)), "l"(p + 16 * c) : "memory");
+#endif
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      asm volatile("" : "+r"(rec_addr)::"memory");  // the record loads below depend on THIS value of the address: they cannot move above the wait
+    }
+    const StagedRecord<kChunks * 4, kPitch> rec{rec_addr};
+    tally.visit();
+    const uint32_t rel0 = top - window;
+    uint32_t m = 0;
+    Ref pend = cur;
+    float pend_t = 0.0f;
+    // FAST: all (at most 7) pushes of this step land in the shared-memory window: predicated stores, no branch
+    auto run_slots = [&](auto FAST) {
+      constexpr bool kFast = decltype(FAST)::value;
+      auto slot = [&](auto KC) {
+        constexpr int K = decltype(KC)::value;
+        f32x3 lo, hi;
+        Ref ch;
+        L::template decode_slot<K>(T, cur, rec, lo, hi, ch);
+        float tn, t_far;
+        const bool some = ray_aabb(ray, lo, hi, tn, t_far);
+        if (interval_intersects(ray, some, tn, t_far) && tn < best_t) {
+          if (m) {  // a slot with a larger index passed before: it pops after this one
+            if constexpr (kFast) {
+              LS::store(top, Entry{pend, pend_t});
+            } else {  // entries beyond the reference capacity are dropped: the query retires with an overflow status below
+              const uint32_t rel = top - window;
+              if (rel < LS::kSmemBytes) {
+                LS::store(top, Entry{pend, pend_t});
+              } else {
+                const uint32_t pos = rel / LS::kSlot - (uint32_t)LS::kSmem;
+                if (pos < (uint32_t)LS::kDeep) deep[pos] = Entry{pend, pend_t};
+              }
+            }
+            top += LS::kSlot;
+          }
+          pend = ch;
+          pend_t = tn;
+          m++;
+        }
+      };
+      slot(std::integral_constant<int, 7>{});
+      slot(std::integral_constant<int, 6>{});
+      slot(std::integral_constant<int, 5>{});
+      slot(std::integral_constant<int, 4>{});
+      slot(std::integral_constant<int, 3>{});
+      slot(std::integral_constant<int, 2>{});
+      slot(std::integral_constant<int, 1>{});
+      slot(std::integral_constant<int, 0>{});
+    };
+    if (rel0 + 7u * LS::kSlot <= LS::kSmemBytes) run_slots(std::true_type{});
+    else run_slots(std::false_type{});
+    if (m == 0u) {
+      pop_next();
+      return;
+    }
+    const uint32_t depth0 = rel0 / LS::kSlot;
+    if (COUNT) tally.stack(depth0 + m);
+    if (depth0 + m > (uint32_t)SCION_STACK_DEPTH) {  // the reference would hold all m passing children at once
+      retire(SCION_Q_STACK_OVERFLOW);
+      return;
+    }
+    cur = pend;  // the lowest passing slot is visited next
+    enter();
+    if (mode < 0) pop_next();
+  };
+
+  for (;;) {
+#pragma unroll 1
+    for (int k = 0; k < SCION_INNER8; k++) {
+      if (mode == kNode) step();
+    }
+    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
+    if (idle && (__popc(idle) >= SCION_REFILL_MIN8 || work.exhausted)) {
+      uint64_t nq;
+      if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
+        ray = load_ray(rays, nq);
+        stash[threadIdx.x] = RayStash{ray.dx, ray.dy, ray.dz, 0u};
+        stash_q[threadIdx.x] = nq;
+        best_t = scion::inf();
+        best_prim = SCION_MISS_PRIM;
+        tally.reset();
+        top = window + threadIdx.x * 4u;
+        cur = L::root(T);
+        enter();
+        if (mode < 0) retire(SCION_Q_OK);  // the root is an empty leaf
+      }
+      if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
+    }
+    const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
+    if (pmask && (__popc(pmask) >= SCION_PRIM_MIN8 || __ballot_sync(kFullMask, mode == kNode) == 0u)) {
+      const bool own = mode == kPrim;
+      const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, prim_end, best_t,
+                                               best_prim, coop[threadIdx.x >> 5]);
+      if (COUNT) tally.prim_tests += done;
+      if (own) pop_next();
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // closest_point, binary + DOP-14 families
 // ------------------------------------------------------------------------------------------
 template <class L, class TallyT>

@@ -693,6 +693,55 @@ struct Emitter {
       if (can_fetch) emit_decode("decode_fetched", Mode::All);
       out << "  SCION_HOSTDEV static void decode_cold(const scion::TreeView&, const Ref&, Node&) {}\n";
     }
+    // Per-slot form of an 8-wide interior decode: decode_slot<K>() computes child slot K only, from ANY word source
+    // (registers, or a lane's copy of the record staged in shared memory by 16-byte async copies — the extraction
+    // templates of scion_rt.cuh are generic over the source).  It is the member list of the indirect group, emitted once
+    // more; everything that does not feed slot K is dead code for the C++ compiler.  Emitted for records that start on a
+    // 16-byte boundary (the `-align16` files and the 256-byte f32 record): that is what a 16-byte cp.async needs.
+    {
+      const MemberNode* from_split = nullptr;
+      const Arm* from_arm = nullptr;
+      if (plan.family == Family::Bvh8)
+        for (auto& m : primary->members)
+          if (m->kind == MemberNode::Split)
+            for (auto& a : m->arms)
+              if (a.is_from && !from_arm) { from_split = m.get(); from_arm = &a; }
+      const GroupInfo* gi = nullptr;
+      if (from_arm) {
+        auto it = indirect_groups.find(from_arm->from_group);
+        if (it != indirect_groups.end() && it->second.buf && it->second.buf->segments.size() == 1 && !it->second.buf->is_arena) gi = &it->second;
+      }
+      const bool can_slot = gi && gi->buf->segments[0].stride_bytes % 16 == 0;
+      out << "  static constexpr bool kCanSlot = " << (can_slot ? "true" : "false") << ";  // decode_slot<K>() over a staged record\n";
+      if (can_slot) {
+        const Buffer& b = *gi->buf;
+        const uint64_t bytes = b.segments[0].stride_bytes;
+        const Variant* v = find_variant(from_arm->variant);
+        std::string t2 = ident_of(from_arm->from_group) + "_";
+        out << "  static constexpr uint32_t kSlotRecordBytes = " << bytes << "u;  // stride of the interior record\n";
+        out << "  static constexpr uint32_t kSlotUsedBytes = " << (b.segments[0].stride_bits + 7) / 8 << "u;  // bytes the fields occupy (the rest is alignment padding)\n";
+        out << "  SCION_HOSTDEV static const uint8_t* slot_record(const scion::TreeView& tree__, const Ref& ref__) {  // address of the interior record `ref__` designates\n";
+        out << "    return tree__.buf[" << b.id << "] + (uint64_t)(" << ex(from_arm->from_key, true) << ") * " << bytes << "ull;\n  }\n";
+        out << "  template <int K, class Src>\n";
+        out << "  SCION_HOSTDEV static void decode_slot(const scion::TreeView& tree__, const Ref& ref__, const Src& w_" << t2 << "0, scion::vec<float, 3>& lo__, scion::vec<float, 3>& hi__, Ref& child__) {\n";
+        out << "    (void)tree__; (void)ref__;\n";
+        out << "    Node node__;\n";
+        std::set<std::string> ids;
+        std::function<void(const std::vector<MemberP>&)> scan = [&](const std::vector<MemberP>& ms) {
+          for (auto& m : ms) {
+            collect_idents(m->value, ids);
+            scan(m->members);
+          }
+        };
+        scan(gi->node->members);
+        for (size_t g = 0; g < plan.globals.size(); g++)
+          if (ids.count(plan.globals[g].name) && !plan.globals[g].inferred)
+            out << "    const " << ctype(plan.globals[g].type) << " " << plan.globals[g].name << " = scion::glob<" << ctype(plan.globals[g].type) << ">(tree__, " << g << ");\n";
+        emit_members(gi->node->members, gi->buf, t2, 2, Mode::All, {}, {}, v, true);
+        out << "    lo__ = node__.lo[K];\n    hi__ = node__.hi[K];\n    child__ = node__.children[K];\n  }\n";
+        (void)from_split;
+      }
+    }
     // prefetch(): pull the record a reference designates into L2 ahead of its visit (issued by the
     // traversal when the reference is pushed on the stack)
     out << "  template <int LEVEL = 2>  // 2: into L2 (a reference that was pushed); 1: into L1 (a record about to be visited)\n";

@@ -278,6 +278,35 @@ def test_treelet_variant_on_a_tiny_tree(built, torch_cuda):
             dt.free()
 
 
+STAGED8 = ["bvh8", "bvh8-align16", "bvh8-q8-align16", "bvh8-q8-ci-align16", "bvh8-q16-align16", "bvh8-q16-ci-align16"]
+
+
+@pytest.mark.parametrize("layout", STAGED8)
+def test_staged_record_8wide_kernel_is_identical(built, torch_cuda, world, layout):
+    """chrt8s_kernel (interior record staged in shared memory by 16-byte cp.async copies, one child slot decoded at a time
+    by the emitted decode_slot<K>()) against chrt8_kernel (whole record in registers): hit records, per-query status and
+    the interpreter counters (node visits, primitive tests, peak stack) must be equal bit for bit — variants 4 and 1
+    select the two kernels explicitly, whichever is the default"""
+    sb, torch = built, torch_cuda
+    n = world["rays"].shape[0]
+    d_rays = dev_bytes(torch, world["rays"])
+    dt = world["lt"].encode(layout).upload(0)
+    out = {}
+    for v in (1, 4):
+        h = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+        st = torch.full((n,), 7, dtype=torch.int32, device="cuda:0")
+        c = torch.zeros(n * 16, dtype=torch.uint8, device="cuda:0")
+        dt.closest_hit(d_rays.data_ptr(), n, h.data_ptr(), st.data_ptr(), c.data_ptr(), variant=v)
+        h2 = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+        dt.closest_hit(d_rays.data_ptr(), n, h2.data_ptr(), variant=v)  # the counter-free build
+        torch.cuda.synchronize()
+        assert torch.equal(h, h2), (layout, v)
+        out[v] = (h, st, c)
+    for a, b in zip(out[1], out[4]):
+        assert torch.equal(a, b), layout
+    dt.free()
+
+
 def test_two_rays_per_lane_variant_is_identical(built, torch_cuda, world):
     """experimental kernel variant 3 (two rays per lane, the next record's load of one ray in flight while the other
     ray's step executes; emitted fetch() / decode_fetched()) must return exactly the default kernel's records and

@@ -157,6 +157,30 @@ if __name__ == "__main__":
                 print(f"  {layout:10s} {kind:9s} {nr / ms / 1e3:8.1f} Mrays/s  visits/ray {nv:.1f} tris/ray {npt:.1f} maxstack {ctr['max_stack'].max()} mean stack {ctr['max_stack'].mean():.1f} -> {nr * nv / ms / 1e6:.1f} Gvisits/s", flush=True)
             dt.free()
         sys.exit(0)
+    if "--wide8" in sys.argv:  # 8-wide kernels: register-record (variant 1) vs staged-record (variant 4), C5-like mix
+        i = sys.argv.index("--wide8")
+        layouts = sys.argv[i + 1].split(",") if len(sys.argv) > i + 1 else ["bvh8", "bvh8-align16", "bvh8-q8-align16", "bvh8-q8-ci-align16", "bvh8-q16-align16", "bvh8-q16-ci-align16"]
+        scene = sb.Scene.terrain(2236, seed=1)
+        lt = scene.build_sah(32, 4).collapse8()
+        lo, hi = scene.bounds()
+        nr = 1 << 25
+        d_rays = dbuf(nr * 32); outs = {1: dbuf(nr * 8), 4: dbuf(nr * 8)}
+        cam = sb.default_camera(lo, hi, True, 4096, 4096)
+        for layout in layouts:
+            dt = lt.encode(layout).upload(0)
+            sb.gen_primary(cam, 0, 1 << 24, d_rays.data_ptr()); dt.gen_secondary(77, 0, 1 << 24, d_rays.data_ptr() + (32 << 24))
+            res = {}
+            for v in (1, 4):
+                for _ in range(2): dt.closest_hit(d_rays.data_ptr(), nr, outs[v].data_ptr(), variant=v)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(4): dt.closest_hit(d_rays.data_ptr(), nr, outs[v].data_ptr(), variant=v)
+                e1.record(); torch.cuda.synchronize()
+                res[v] = nr / (e0.elapsed_time(e1) / 4) / 1e3
+            print(f"  {layout:22s} registers {res[1]:8.1f}  staged {res[4]:8.1f} Mrays/s  ({res[4] / res[1]:.3f}x)  identical={bool(torch.equal(outs[1], outs[4]))}", flush=True)
+            dt.free()
+        sys.exit(0)
     if "--stage" in sys.argv:  # TMA-staged top-levels treelet (variant 2) vs default: identical results? timing?
         for G in (708, 2236):
             scene = sb.Scene.terrain(G, seed=1)
