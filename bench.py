@@ -42,13 +42,15 @@ def parse_args():
     ap.add_argument("--workload", default="c5")
     ap.add_argument("--layout", default="pbrt-q16", help="headline layout (the paper's Pareto-optimal layout)")
     ap.add_argument("--sweep", default="all", help="extra layouts reported in `layouts` (at every N): comma list, '' disables, 'all' = every corpus layout "
-                    "except shared-slab (one slab per node: ~2600 node visits per ray on a terrain, minutes per step at this size; "
-                    "it is measured in profiles/r1_all_layouts_*.csv at 1 M triangles)")
+                    "(shared-slab — one slab per node, ~2600 node visits per ray on a terrain — on a stated 2^20-query sample)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink query counts (debug)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     return ap.parse_args()
+
+
+SLAB_SAMPLE = 1 << 20  # shared-slab is measured on this many queries (see the sweep loop)
 
 
 def measured_peak():
@@ -326,11 +328,13 @@ def main():
     d_r = torch.empty(count * r_bytes, dtype=torch.uint8, device=dev)
     d_st = torch.empty(count, dtype=torch.int32, device=dev)
 
+    cur = {"count": count, "total": wl.total}  # queries of this rank / of the whole job in the current measurement
+
     def run_step(dt):
         if wl.algorithm == "chrt":
-            dt.closest_hit(d_q.data_ptr(), count, d_r.data_ptr())
+            dt.closest_hit(d_q.data_ptr(), cur["count"], d_r.data_ptr())
         else:
-            dt.closest_point(d_q.data_ptr(), count, d_r.data_ptr())
+            dt.closest_point(d_q.data_ptr(), cur["count"], d_r.data_ptr())
 
     def timed(dt, steps, warmup, sampler=None):
         for _ in range(warmup):
@@ -359,17 +363,18 @@ def main():
 
     def measure_bytes(dt, layout):
         """exact algorithmic bytes of this rank's slice from the counter-instrumented kernel"""
-        d_ctr = torch.empty(count * 4, dtype=torch.int32, device=dev)
+        cnt = cur["count"]
+        d_ctr = torch.empty(cnt * 4, dtype=torch.int32, device=dev)
         if wl.algorithm == "chrt":
-            dt.closest_hit(d_q.data_ptr(), count, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+            dt.closest_hit(d_q.data_ptr(), cnt, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
         else:
-            dt.closest_point(d_q.data_ptr(), count, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
+            dt.closest_point(d_q.data_ptr(), cnt, d_r.data_ptr(), d_st.data_ptr(), d_ctr.data_ptr())
         torch.cuda.synchronize()
         sums = d_ctr.view(-1, 4).sum(dim=0, dtype=torch.int64)
-        errors = int((d_st != 0).sum().item())
+        errors = int((d_st[:cnt] != 0).sum().item())
         if world > 1 or force_dist:
             dist.all_reduce(sums)
-        s = sums.cpu().numpy().astype(np.float64) / wl.total
+        s = sums.cpu().numpy().astype(np.float64) / cur["total"]
         mean = np.zeros(1, sb.COUNTERS_DTYPE)
         plan = sb.layout_plan(layout)
         nb = [x for x in plan["buffers"] if x["name"] == plan["node_group"]][0]
@@ -382,7 +387,7 @@ def main():
     peak, peak_src = measured_peak()
     results = {}
     # the sweep runs at every N: BASELINE's metric is Mrays/s *per layout* at 1/2/4/8 GPUs (same code path as the headline)
-    sweep = [l["name"] for l in sb.layouts() if l["name"] != "shared-slab"] if args.sweep == "all" else args.sweep.split(",")
+    sweep = [l["name"] for l in sb.layouts()] if args.sweep == "all" else args.sweep.split(",")
     layouts = [args.layout] + [l for l in sweep if l and l != args.layout]
     if wl.algorithm != "chrt":  # closest point is defined for the binary families only (cpq.scion, cpq_dop14.scion)
         cpq_ok = {l["name"] for l in sb.layouts() if l["has_cpq"]}
@@ -390,21 +395,37 @@ def main():
     headline = None
     for li, layout in enumerate(layouts):
         dt, img, pt, bcast_s = replicate(layout)
-        W.generate_device(wl, dt, lo, hi, first, count, d_q.data_ptr())
-        torch.cuda.synchronize()
         is_head = li == 0
+        sample_note = None
+        if layout == "shared-slab" and not is_head and wl.total > SLAB_SAMPLE:
+            # one slab per node: ~2600 node visits per ray on a terrain (its boxes barely cull) — minutes per step at full size.
+            # Measured on a bounded sample with the workload's own mix (equal prefixes of every segment), stated in the entry.
+            ranges = W.sample_indices(wl, SLAB_SAMPLE)
+            mine, off = ranges[rank::world], 0
+            for f0, c0 in mine:
+                W.generate_device(wl, dt, lo, hi, f0, c0, d_q.data_ptr() + off * q_bytes)
+                off += c0
+            cur["count"], cur["total"] = off, sum(c for _, c in ranges)
+            sample_note = f"{cur['total']} of {wl.total} queries: equal prefixes of the workload's {len(ranges)} segments"
+        else:
+            cur["count"], cur["total"] = count, wl.total
+            W.generate_device(wl, dt, lo, hi, first, count, d_q.data_ptr())
+        torch.cuda.synchronize()
         sampler = ClockSampler(local_rank) if (is_head and rank == 0) else None
         ms, launches, clocks = timed(dt, args.steps if is_head else max(2, min(3, args.steps)), args.warmup if is_head else 3, sampler)
         bpq, ctr, errors = measure_bytes(dt, layout)
-        value = wl.total / ms / 1e3
-        gbs = bpq * wl.total / (ms * 1e-3) / 1e9
+        value = cur["total"] / ms / 1e3
+        gbs = bpq * cur["total"] / (ms * 1e-3) / 1e9
         info = {"mrays": value, "ms_per_step": ms, "bytes_per_query": bpq, "achieved_gbs": gbs, "frac_of_measured_hbm": gbs / peak, "frac_of_nominal_8tbs": gbs / 8000.0,
                 "node_visits": ctr["node_visits"], "prim_tests": ctr["prim_tests"], "query_errors": errors}
         if rank == 0:
             info["bvh_bytes_per_prim"] = pt.node_bytes / ltree.nprims
             info["total_bytes_per_prim"] = pt.total_bytes / ltree.nprims
             info["replicate_s"] = bcast_s
+        if sample_note:
+            info["sample"] = sample_note
         results[layout] = info
+        cur["count"], cur["total"] = count, wl.total
         if is_head:
             headline = dict(ms=ms, launches=launches, clocks=clocks, value=value, bpq=bpq, gbs=gbs, dt=dt, img=img, pt=pt)
         else:

@@ -149,6 +149,11 @@ int scion_layout_find(const char* name, scion_layout_info* out);
 int scion_layout_plan_json(const char* name, char** out_json);
 /* emit_cuda: the CUDA sibling of emit_c — deterministic text. */
 int scion_layout_emit_cuda(const char* name, char** out_text);
+/* emit_c, record half ("packed record declarations matching MemoryPlan strides bit-for-bit ... a
+ * static assertion on node size"): a C11 header with the typed packed node records, their assertions and the slot table. */
+int scion_layout_emit_c(const char* name, char** out_text);
+/* op-count report of the layout's decode, per variant (the CLI's --dump-stats): JSON. */
+int scion_layout_stats_json(const char* name, char** out_json);
 /* Compile a layout spec from source text (layout-language subset of the
  * reference grammar, src/parser.cpp:790-955) and return plan JSON / CUDA text. */
 int scion_compile_layout_text(const char* scion_source, char** out_plan_json, char** out_cuda);

@@ -95,6 +95,8 @@ def lib() -> C.CDLL:
         "scion_layout_find": (i32, [cp, P(LayoutInfo)]),
         "scion_layout_plan_json": (i32, [cp, P(vp)]),
         "scion_layout_emit_cuda": (i32, [cp, P(vp)]),
+        "scion_layout_emit_c": (i32, [cp, P(vp)]),
+        "scion_layout_stats_json": (i32, [cp, P(vp)]),
         "scion_compile_layout_text": (i32, [cp, P(vp), P(vp)]),
         "scion_scene_terrain": (i32, [u32, u64, P(vp)]),
         "scion_scene_sphere": (i32, [u32, u64, P(vp)]),
@@ -251,6 +253,20 @@ def emit_cuda(name: str) -> str:
     p = C.c_void_p()
     _check(lib().scion_layout_emit_cuda(name.encode(), C.byref(p)))
     return _take_string(p)
+
+
+def emit_c(name: str) -> str:
+    """C11 header with the typed packed node records of the layout, their static assertions and the slot table."""
+    p = C.c_void_p()
+    _check(lib().scion_layout_emit_c(name.encode(), C.byref(p)))
+    return _take_string(p)
+
+
+def layout_stats(name: str) -> dict:
+    """op counts of the layout's decode per variant (loads, arithmetic, casts, ...): the --dump-stats report"""
+    p = C.c_void_p()
+    _check(lib().scion_layout_stats_json(name.encode(), C.byref(p)))
+    return json.loads(_take_string(p))
 
 
 def compile_layout_text(source: str):

@@ -211,6 +211,12 @@ int scion_layout_plan_json(const char* name, char** out_json) {
 int scion_layout_emit_cuda(const char* name, char** out_text) {
   SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e || !out_text) return fail(SCION_ERR_ARG, "unknown layout"); *out_text = dup_string(scion::lc::emit_cuda(*e->plan)); return SCION_OK;)
 }
+int scion_layout_emit_c(const char* name, char** out_text) {
+  SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e || !out_text) return fail(SCION_ERR_ARG, "unknown layout"); *out_text = dup_string(scion::lc::emit_c_records(*e->plan)); return SCION_OK;)
+}
+int scion_layout_stats_json(const char* name, char** out_json) {
+  SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e || !out_json) return fail(SCION_ERR_ARG, "unknown layout"); *out_json = dup_string(scion::lc::decode_stats_json(*e->plan)); return SCION_OK;)
+}
 int scion_compile_layout_text(const char* src, char** out_plan_json, char** out_cuda) {
   if (!src) return fail(SCION_ERR_ARG, "null source");
   SCION_TRY(scion::lc::Program prog = scion::lc::parse_program({std::string(src)}); scion::lc::Plan plan = scion::lc::plan_layout(prog, "user-layout");

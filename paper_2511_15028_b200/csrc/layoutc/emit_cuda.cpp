@@ -526,11 +526,12 @@ struct Emitter {
           << ", count '" << b.count_name << "', align " << b.align << "\n";
       out << "  static constexpr int kBuf_" << ident_of(b.name) << " = " << b.id << ";\n";
       out << "  static constexpr uint32_t kStride_" << ident_of(b.name) << " = " << b.node_stride() << "u;\n";
-      for (size_t s = 0; s < b.segments.size(); s++) {
-        std::string rn = "Record_" + ident_of(b.name) + "_s" + std::to_string(s);
-        out << "  struct " << rn << " { uint8_t bytes[" << b.segments[s].stride_bytes << "]; };  // " << b.segments[s].stride_bits << " bits used\n";
-        out << "  static_assert(sizeof(" << rn << ") == " << b.segments[s].stride_bytes << ", \"node record must match the planned stride\");\n";
-      }
+    }
+    // the device node record(s): typed, packed, one struct per segment (emit_records.cpp)
+    {
+      std::istringstream rec(emit_records(plan, "Record_", false));
+      std::string line;
+      while (std::getline(rec, line)) out << "  " << line << "\n";
     }
     for (auto& s : plan.slots)
       out << "  static constexpr uint32_t kOff_" << s.name << " = " << s.offset << "u, kWidth_" << s.name << " = " << s.width << "u, kSeg_" << s.name << " = " << s.segment << "u;  // "

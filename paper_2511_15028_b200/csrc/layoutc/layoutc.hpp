@@ -215,6 +215,12 @@ Plan plan_layout(const Program& program, const std::string& registry_name);
 
 // emit_cuda: deterministic CUDA header text for the planned layout.
 std::string emit_cuda(const Plan& plan);
+// typed packed record declarations (one struct per node-buffer segment) + static assertions; shared by emit_cuda and emit-c
+std::string emit_records(const Plan& plan, const std::string& prefix, bool c11);
+// `scionc emit-c`: C11 header with the packed records, their assertions and the slot table (record half)
+std::string emit_c_records(const Plan& plan);
+// op-count report of the layout's decode, per variant (`scionc stats`; SPEC.md:360 --dump-stats)
+std::string decode_stats_json(const Plan& plan);
 // C-identifier form of a registry name ("pbrt-q16" -> "pbrt_q16")
 std::string ident_of(const std::string& registry_name);
 

@@ -64,7 +64,10 @@ def cmd_footprint(a):
 
 
 def cmd_emit(a):
-    text = sb.emit_cuda(a.layout)
+    if getattr(a, "dump_stats", False):  # the reference CLI's --dump-stats: op-count JSON of the decode
+        print(json.dumps(sb.layout_stats(a.layout), indent=1))
+        return 0
+    text = sb.emit_c(a.layout) if a.cmd == "emit-c" else sb.emit_cuda(a.layout)
     if a.output:
         open(a.output, "w").write(text)
     else:
@@ -280,9 +283,11 @@ def main(argv=None):
     p.add_argument("--layout", required=True)
     p.add_argument("--scene", default="terrain:64")
     p.add_argument("--max-leaf", type=int, default=4)
-    p = sub.add_parser("emit-cuda")
-    p.add_argument("--layout", required=True)
-    p.add_argument("-o", "--output")
+    for name in ("emit-cuda", "emit-c"):  # emit-c: the record half of the reference's emit_c (typed packed records + assertions)
+        p = sub.add_parser(name)
+        p.add_argument("--layout", required=True)
+        p.add_argument("-o", "--output")
+        p.add_argument("--dump-stats", action="store_true")
     p = sub.add_parser("compile")
     p.add_argument("file")
     p.add_argument("--plan")
@@ -320,7 +325,7 @@ def main(argv=None):
         ap.print_usage(sys.stderr)
         return 2
     try:
-        return {"check": cmd_check, "footprint": cmd_footprint, "emit-cuda": cmd_emit, "bench": cmd_bench, "compile": cmd_compile,
+        return {"check": cmd_check, "footprint": cmd_footprint, "emit-cuda": cmd_emit, "emit-c": cmd_emit, "bench": cmd_bench, "compile": cmd_compile,
                 "build-tree": cmd_build_tree, "build": cmd_build, "run": cmd_run}[a.cmd](a)
     except sb.ScionError as e:
         print(f"error: {e}", file=sys.stderr)
