@@ -201,6 +201,12 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2, kDone = 4 };  // lane modes (3 = 
 #ifndef SCION_PREFETCH
 #define SCION_PREFETCH 1
 #endif
+#ifndef SCION_CPQ_GUIDED  /* 1: closest_point uses the guided (128 -> 32 query) work-fetch chunks of the closest-hit kernels */
+#define SCION_CPQ_GUIDED 0
+#endif
+#ifndef SCION_TOS  /* 1: the newest stack entry of the binary closest-hit kernel lives in a register (see chrt2_kernel) */
+#define SCION_TOS 0
+#endif
 #ifndef SCION_PF_NEXT
 #define SCION_PF_NEXT 0
 #endif
@@ -456,6 +462,32 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
     mode = kFetch;
   };
 
+#if SCION_TOS
+  // SCION_TOS (north_star: "a short traversal stack in registers that spills to shared memory"): the newest pending
+  // reference lives in the register `tos`; memory (shared window, then local) holds the entries below it, i.e. slots
+  // [0, depth - 1).  A pop hands over `tos` at once and refills it with a load nobody waits for; a push spills the old
+  // `tos`.  `top` keeps its meaning (address of slot `depth`).
+  Ref tos = L::root(T);
+  auto mem_store = [&](uint32_t idx, const Ref& r) {  // slot idx of the memory part
+    if (idx < (uint32_t)LS::kSmem) LS::store(window + threadIdx.x * 4u + idx * LS::kSlot, r);
+    else deep[idx - (uint32_t)LS::kSmem] = r;
+  };
+  auto mem_load = [&](uint32_t idx, Ref& r) {
+    if (idx < (uint32_t)LS::kSmem) LS::load(window + threadIdx.x * 4u + idx * LS::kSlot, r);
+    else r = deep[idx - (uint32_t)LS::kSmem];
+  };
+  auto pop_or_retire = [&]() {
+    const uint32_t depth = (top - window) / LS::kSlot;
+    if (depth == 0u) {
+      retire(SCION_Q_OK);
+      return;
+    }
+    cur = tos;
+    top -= LS::kSlot;
+    if (depth >= 2u) mem_load(depth - 2u, tos);
+    mode = kNode;
+  };
+#else
   // next pending reference, or retire the query when the stack is empty (used after a leaf phase
   // and on the rare paths of step())
   auto pop_or_retire = [&]() {
@@ -476,6 +508,7 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       mode = kNode;
     }
   };
+#endif
 
   constexpr bool kHot = SCION_HOT_L1 > 0 && TL == 0 && L::kCanFetch && !L::kHasCold && std::is_same<Ref, uint32_t>::value;
   const Ref root = [&]() -> Ref {
@@ -541,7 +574,13 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
     // the common push (depth < kSmem) and pop (1 <= depth <= kSmem) are straight-line predicated
     // code; everything else (empty stack = retire, entries beyond the shared-memory window,
     // overflow) is one rarely taken branch
+#if SCION_TOS
+    // memory holds slots [0, depth - 1): a push spills `tos` into slot depth - 1, a pop refills it from slot depth - 2 — both
+    // inside the shared window as long as depth <= kSmem
+    const bool fast = p_push ? rel < LS::kSmemBytes + LS::kSlot : rel - LS::kSlot < LS::kSmemBytes + LS::kSlot;
+#else
     const bool fast = p_push ? rel < LS::kSmemBytes : rel - LS::kSlot < LS::kSmemBytes;
+#endif
     if (COUNT && p_push) tally.stack(rel / LS::kSlot + 2u);  // reference discipline: pop self, push right, push left
     if (!(fast || p_prim)) {
       if (p_push) {
@@ -549,7 +588,12 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
         if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
           retire(SCION_Q_STACK_OVERFLOW);
         } else {
+#if SCION_TOS
+          mem_store(depth - 1u, tos);  // depth > kSmem >= 1 here
+          tos = tagged(node.right);
+#else
           deep[depth - (uint32_t)LS::kSmem] = tagged(node.right);
+#endif
           top += LS::kSlot;
           cur = tagged(node.left);
         }
@@ -563,7 +607,12 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       prefetch_triangles<L>(T, (uint32_t)node.data.begin, (uint32_t)node.data.end);
       mode = kPrim;
     } else if (p_push) {
+#if SCION_TOS
+      if (rel >= LS::kSlot) LS::store(top - LS::kSlot, tos);  // spill the previous newest entry (none when the stack was empty)
+      tos = tagged(node.right);
+#else
       LS::store(top, tagged(node.right));
+#endif
       if constexpr (kPrefetch) {
         // L2-prefetch the pushed child, but only when it is far: a right sibling a few records away shares
         // its lines with what this lane just fetched, and every prefetch costs an L1 tag lookup per lane
@@ -578,8 +627,14 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       top += LS::kSlot;
       cur = tagged(node.left);
     } else {
+#if SCION_TOS
+      cur = tos;  // no load between the pop and the next record's address
+      top -= LS::kSlot;
+      if (top - window >= LS::kSlot) LS::load(top - LS::kSlot, tos);  // refill: needed at the next pop / spill only
+#else
       top -= LS::kSlot;
       LS::load(top, cur);
+#endif
     }
   };
 
@@ -1190,7 +1245,11 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
   uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
   asm volatile("" : "+r"(window));
   uint32_t top = window + threadIdx.x * 4u;
+#if SCION_CPQ_GUIDED
+  WorkFetcher work;
+#else
   WorkFetcherFixed work;
+#endif
   (void)tune;
   Tally<COUNT> tally;
   int mode = kFetch;

@@ -12,7 +12,7 @@ for id in $IDENTS; do
   STAGE=""
   if [ "$id" = pbrt_q16 ] || [ "$id" = pbrt ]; then STAGE="-DSCION_DUAL=2"; fi
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++20 -ccbin /usr/bin/g++ \
-    -fmad=false -prec-div=true -prec-sqrt=true -ftz=false -diag-suppress 20281,1886,549 \
+    -fmad=false -prec-div=true -prec-sqrt=true -ftz=false -diag-suppress 20281,1886,549,186 \
     -Xcompiler -fPIC,-fopenmp,-ffp-contract=off -I../../include -I. $STAGE $FLAGS -c build/inst_$id.cu -o build/var_$NAME/inst_$id.o &
   OBJS=$(echo "$OBJS" | grep -v "build/inst_$id.o")
   OBJS="$OBJS build/var_$NAME/inst_$id.o"
