@@ -535,11 +535,92 @@ SCION_HOSTDEV void load_record_generic(const uint8_t* p, Words<(BYTES + 3) / 4>&
   }
 }
 
+// Per-child view of an 8-wide interior record, for lane-cooperative traversal (traverse_coop8.cuh: lane k of a group of 8
+// lanes decodes and tests child slot k only).  The view presents the record AS IF child slot `k` were slot 0: a bit range
+// that lies in a field shared by all children (kLaneFieldElem == 0: mlo, mex) is read where it is, a bit range of an
+// 8-element per-child field (child_bounds, children, lo, hi) is read k elements further on.  The emitted
+// decode_slot<0>() evaluated over this view therefore yields the bounds and the reference of child k — the emitted
+// expressions are the same for every slot (tests/test_generated_decoders.py checks all 8 slots of every 8-wide layout
+// against decode()).  Loads go straight to global memory through the read-only path with the width of the field
+// (LDG.U8 / .U16 / .32; shared fields by 8-byte pairs): the 8 lanes of a group touch one record, i.e. 1-3 lines per
+// request instead of the 32 lines of a one-ray-per-lane gather.  The asm is not volatile: a pure function of the
+// address for the compiler, so repeated reads are merged and the reads of the 7 other slots are removed as dead code.
+template <class L>
+struct LaneRecord {
+  const uint8_t* p;  // address of the record
+  uint32_t k;        // child slot this lane looks at
+  static constexpr bool kDynamic = true;
+  static constexpr int kWords = (int)((L::kSlotUsedBytes + 3u) / 4u);
+  SCION_HOSTDEV static constexpr int field_of(uint32_t off) {
+    for (int f = 0; f < L::kLaneFields; f++)
+      if (off >= L::kLaneFieldOff[f] && off < L::kLaneFieldEnd[f]) return f;
+    return -1;
+  }
+  template <int BYTES>
+  SCION_HOSTDEV static uint32_t ld(const uint8_t* a) {  // BYTES in {1, 2, 4}, a is BYTES-aligned
+#if defined(__CUDA_ARCH__)
+    uint32_t v;
+    if constexpr (BYTES == 1) asm("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(a));
+    else if constexpr (BYTES == 2) asm("ld.global.nc.u16 %0, [%1];" : "=r"(v) : "l"(a));
+    else asm("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(a));
+    return v;
+#else
+    uint32_t v = 0;
+    memcpy(&v, a, BYTES);
+    return v;
+#endif
+  }
+  SCION_HOSTDEV static uint32_t ld_pair(const uint8_t* a, int half) {  // one 32-bit half of an 8-byte aligned pair
+#if defined(__CUDA_ARCH__)
+    uint32_t x, y;
+    asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "l"(a));
+    return half ? y : x;
+#else
+    uint32_t v;
+    memcpy(&v, a + 4 * half, 4);
+    return v;
+#endif
+  }
+  // bits [OFF, OFF + W) of the view
+  template <int OFF, int W>
+  SCION_HOSTDEV uint32_t field() const {
+    constexpr int f = field_of((uint32_t)OFF);
+    static_assert(f >= 0, "bit range outside the stored fields");
+    constexpr uint32_t E = L::kLaneFieldElem[f];
+    constexpr uint32_t mask = (uint32_t)((1ull << W) - 1ull);
+    if constexpr (E == 0) {  // shared by all children: static address
+      if constexpr (OFF % 32 == 0 && W == 32) {
+        if constexpr (L::kLaneAlign % 8 == 0) return ld_pair(p + (OFF / 64) * 8, (OFF / 32) % 2);
+        else return ld<4>(p + OFF / 8);
+      } else {
+        static_assert(OFF % 8 == 0 && (W == 8 || W == 16) && (OFF / 8) % (W / 8) == 0, "shared field: unsupported bit range");
+        return ld<W / 8>(p + OFF / 8);
+      }
+    } else {
+      static_assert(E % 8 == 0 && OFF % 8 == 0, "per-child elements are whole bytes");
+      const uint8_t* a = p + OFF / 8 + k * (E / 8);
+      if constexpr (W == 32 && (OFF / 8) % 4 == 0 && (E / 8) % 4 == 0) return ld<4>(a);
+      else if constexpr (W == 16 && (OFF / 8) % 2 == 0 && (E / 8) % 2 == 0) return ld<2>(a);
+      else if constexpr (W == 8) return ld<1>(a);
+      else {  // any other byte-aligned range: assembled from bytes
+        uint32_t v = 0;
+#pragma unroll
+        for (int i = 0; i < (W + 7) / 8; i++) v |= ld<1>(a + i) << (8 * i);
+        return v & mask;
+      }
+    }
+  }
+};
+template <class S, class = void> struct is_dynamic_src { static constexpr bool value = false; };
+template <class S> struct is_dynamic_src<S, decltype((void)S::kDynamic)> { static constexpr bool value = true; };
+
 // constant-offset field extraction: the inverse of write_bits_raw
 // (/root/reference/proj/src/bits.cpp:21-36), little-endian, LSB first
 template <int OFF, int W, class Src>
 SCION_HOSTDEV uint32_t ext32(const Src& r) {
   static_assert(W >= 1 && W <= 32, "ext32 width");
+  if constexpr (is_dynamic_src<Src>::value) return r.template field<OFF, W>();
+  else {
   constexpr int i = OFF / 32, s = OFF % 32;
   static_assert(i < Src::kWords, "field outside record");
   if constexpr (s + W <= 32) {
@@ -548,6 +629,7 @@ SCION_HOSTDEV uint32_t ext32(const Src& r) {
   } else {
     static_assert(i + 1 < Src::kWords, "field outside record");
     return ((r.template word<i>() >> s) | (r.template word<i + 1>() << (32 - s))) & (uint32_t)((1ull << W) - 1ull);
+  }
   }
 }
 template <int OFF, int W, class Src>

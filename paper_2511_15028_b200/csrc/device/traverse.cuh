@@ -1428,3 +1428,4 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
 }  // namespace scion
 
 #include "traverse_experiments.cuh"
+#include "traverse_coop8.cuh"

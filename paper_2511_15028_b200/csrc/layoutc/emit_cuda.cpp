@@ -713,14 +713,45 @@ struct Emitter {
         if (it != indirect_groups.end() && it->second.buf && it->second.buf->segments.size() == 1 && !it->second.buf->is_arena) gi = &it->second;
       }
       const bool can_slot = gi && gi->buf->segments[0].stride_bytes % 16 == 0;
-      out << "  static constexpr bool kCanSlot = " << (can_slot ? "true" : "false") << ";  // decode_slot<K>() over a staged record\n";
-      if (can_slot) {
+      out << "  static constexpr bool kCanSlot = " << (can_slot ? "true" : "false") << ";  // 16-byte aligned interior record: may be staged by 16-byte async copies\n";
+      // Per-child view of the record (scion::LaneRecord, lane-cooperative traversal: lane k of a group of 8 decodes child slot k
+      // only): every stored field is either shared by all children (mlo, mex) or an 8-element array with one whole-byte element
+      // per child (child_bounds, children, lo, hi).  The table gives [begin, end) bit offsets and the element width of each.
+      struct LaneField { uint64_t off, end; uint64_t elem; };
+      std::vector<LaneField> lane_fields;
+      bool can_lane = gi != nullptr;
+      if (gi) {
+        for (auto& sl : plan.slots) {
+          if (sl.buffer != gi->buf->id || sl.segment != 0) continue;
+          uint64_t elem = 0;
+          if (sl.type && (sl.type->kind == Type::Vec || sl.type->kind == Type::Array) && sl.type->lanes == 8 && sl.type->len_field.empty()) {
+            elem = sl.width / 8;
+            if (sl.width % 8 != 0 || elem % 8 != 0 || sl.offset % 8 != 0) can_lane = false;
+          }
+          lane_fields.push_back(LaneField{sl.offset, sl.offset + sl.width, elem});
+        }
+        if (lane_fields.empty()) can_lane = false;
+      }
+      out << "  static constexpr bool kCanLane = " << (can_lane ? "true" : "false") << ";  // per-child view of the interior record (scion::LaneRecord)\n";
+      if (gi) {
         const Buffer& b = *gi->buf;
         const uint64_t bytes = b.segments[0].stride_bytes;
         const Variant* v = find_variant(from_arm->variant);
         std::string t2 = ident_of(from_arm->from_group) + "_";
         out << "  static constexpr uint32_t kSlotRecordBytes = " << bytes << "u;  // stride of the interior record\n";
         out << "  static constexpr uint32_t kSlotUsedBytes = " << (b.segments[0].stride_bits + 7) / 8 << "u;  // bytes the fields occupy (the rest is alignment padding)\n";
+        if (can_lane) {
+          out << "  static constexpr uint32_t kLaneAlign = " << gcd_align(b, 0) << "u;  // alignment every record address is known to have\n";
+          out << "  static constexpr int kLaneFields = " << lane_fields.size() << ";\n";
+          auto table = [&](const char* name, auto get, const char* what) {
+            out << "  static constexpr uint32_t " << name << "[" << lane_fields.size() << "] = {";
+            for (size_t i = 0; i < lane_fields.size(); i++) out << (i ? ", " : "") << get(lane_fields[i]) << "u";
+            out << "};  // " << what << "\n";
+          };
+          table("kLaneFieldOff", [](const LaneField& f) { return f.off; }, "first bit of each stored field");
+          table("kLaneFieldEnd", [](const LaneField& f) { return f.end; }, "one past its last bit");
+          table("kLaneFieldElem", [](const LaneField& f) { return f.elem; }, "bits of one per-child element (0: the field is shared by all 8 children)");
+        }
         out << "  SCION_HOSTDEV static const uint8_t* slot_record(const scion::TreeView& tree__, const Ref& ref__) {  // address of the interior record `ref__` designates\n";
         out << "    return tree__.buf[" << b.id << "] + (uint64_t)(" << ex(from_arm->from_key, true) << ") * " << bytes << "ull;\n  }\n";
         out << "  template <int K, class Src>\n";

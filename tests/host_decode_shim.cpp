@@ -86,6 +86,44 @@ template <class L> int dec8(const TreeView* T, uint64_t ref, float* f, uint64_t*
   return 0;
 }
 
+// the per-child record view of the lane-cooperative kernel (scion::LaneRecord): decode_slot<0>() over the view of slot k
+// must give child k of decode(), for every k
+template <class L> int dec8_lane(const TreeView* T, uint64_t ref, float* f, uint64_t* u) {
+  std::memset(f, 0, 48 * sizeof(float));
+  std::memset(u, 0, 11 * sizeof(uint64_t));
+  const typename L::Ref r = (typename L::Ref)ref;
+  u[0] = L::ref_variant(r) == L::kLeaf;
+  if (u[0]) {
+    typename L::Node n{};
+    L::decode(*T, r, n);
+    u[1] = n.data.begin; u[2] = n.nprims;
+    return 0;
+  }
+  // a padded private copy: the host compiler may keep the (dead) reads of the other slots, which reach past the record
+  unsigned char copy[3 * 256] = {0};
+  static_assert(L::kSlotRecordBytes <= 256, "interior record");
+  std::memcpy(copy, L::slot_record(*T, r), L::kSlotUsedBytes);
+  for (uint32_t k = 0; k < 8; k++) {
+    scion::f32x3 lo, hi;
+    typename L::Ref ch;
+    const scion::LaneRecord<L> rec{copy, k};
+    L::template decode_slot<0>(*T, r, rec, lo, hi, ch);
+    u[3 + k] = (uint64_t)ch;
+    float v[6] = {lo.x, lo.y, lo.z, hi.x, hi.y, hi.z};
+    std::memcpy(f + 6 * k, v, sizeof(v));
+  }
+  return 0;
+}
+extern "C" int host_decode8_lane(const char* layout, const TreeView* T, uint64_t ref, float* f, uint64_t* u) {
+  std::string n = layout;
+#define L8(NAME, T_) if (n == NAME) return dec8_lane<g::T_>(T, ref, f, u);
+  L8("bvh8", L_bvh8) L8("bvh8-q8", L_bvh8_q8) L8("bvh8-q8-ci", L_bvh8_q8_ci) L8("bvh8-q16", L_bvh8_q16) L8("bvh8-q16-ci", L_bvh8_q16_ci)
+  L8("bvh8-align16", L_bvh8_align16) L8("bvh8-q8-align16", L_bvh8_q8_align16) L8("bvh8-q8-ci-align16", L_bvh8_q8_ci_align16) L8("bvh8-q16-align16", L_bvh8_q16_align16)
+  L8("bvh8-q16-ci-align16", L_bvh8_q16_ci_align16)
+#undef L8
+  return -1;
+}
+
 extern "C" int host_decode2(const char* layout, const TreeView* T, uint64_t ref, const float* carried, float* f, uint64_t* u) {
   std::string n = layout;
 #define L2(NAME, T_) if (n == NAME) return dec2<g::T_>(T, ref, carried, f, u);

@@ -54,6 +54,7 @@ def test_generated_decoders_match_oracle(built, oracle, shim):
     oracle.lib.oracle_decode8.argtypes = [C.POINTER(TreeBytes), C.c_uint64, C.c_void_p, C.c_void_p]
     shim.host_decode2.argtypes = [C.c_char_p, C.POINTER(TreeView), C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
     shim.host_decode8.argtypes = [C.c_char_p, C.POINTER(TreeView), C.c_uint64, C.c_void_p, C.c_void_p]
+    shim.host_decode8_lane.argtypes = [C.c_char_p, C.POINTER(TreeView), C.c_uint64, C.c_void_p, C.c_void_p]
     scene = built.Scene.terrain(14, 21)
     lt = scene.build_sah(32, 4).collapse8()
     for l in built.layouts():
@@ -92,6 +93,12 @@ def test_generated_decoders_match_oracle(built, oracle, shim):
                 assert np.array_equal(u1, u2), (name, ref, u1, u2)
                 if not u1[0]:  # leaves are encoded in the reference itself: no boxes
                     assert np.array_equal(f1.view(np.uint32), f2.view(np.uint32)), (name, ref)
+                # the per-child record view of the lane-cooperative kernel: slot k through decode_slot<0>(LaneRecord{record, k})
+                f3, u3 = np.zeros(48, np.float32), np.zeros(11, np.uint64)
+                assert shim.host_decode8_lane(name.encode(), C.byref(tv), ref, f3.ctypes.data, u3.ctypes.data) == 0, name
+                assert np.array_equal(u1, u3), (name, ref, u1, u3)
+                if not u1[0]:
+                    assert np.array_equal(f1.view(np.uint32), f3.view(np.uint32)), (name, ref)
                 visited += 1
                 if not u1[0]:
                     wn = lt.wnodes()[int(ref) >> 2]

@@ -307,6 +307,40 @@ def test_staged_record_8wide_kernel_is_identical(built, torch_cuda, world, layou
     dt.free()
 
 
+COOP8 = ["bvh8", "bvh8-align16", "bvh8-q8", "bvh8-q8-align16", "bvh8-q8-ci", "bvh8-q8-ci-align16", "bvh8-q16", "bvh8-q16-align16", "bvh8-q16-ci",
+         "bvh8-q16-ci-align16"]
+
+
+@pytest.mark.parametrize("layout", COOP8)
+def test_lane_cooperative_8wide_kernel_is_identical(built, torch_cuda, world, oracle, layout):
+    """chrt8c_kernel (kernel variant 5: a group of 8 lanes owns one ray, lane k decodes and tests child slot k through the
+    per-child record view scion::LaneRecord, the group's 8 lanes test 8 triangles of a leaf at a time) against chrt8_kernel
+    (variant 1, one ray per lane) AND against the oracle: hit records, per-query status and the interpreter counters
+    (node visits, primitive tests, peak stack) must be equal bit for bit, with and without the counter instrumentation"""
+    sb, torch = built, torch_cuda
+    n = world["rays"].shape[0]
+    d_rays = dev_bytes(torch, world["rays"])
+    pt = world["lt"].encode(layout)
+    dt = pt.upload(0)
+    out = {}
+    for v in (1, 5):
+        h = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+        st = torch.full((n,), 7, dtype=torch.int32, device="cuda:0")
+        c = torch.zeros(n * 16, dtype=torch.uint8, device="cuda:0")
+        dt.closest_hit(d_rays.data_ptr(), n, h.data_ptr(), st.data_ptr(), c.data_ptr(), variant=v)
+        h2 = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+        dt.closest_hit(d_rays.data_ptr(), n, h2.data_ptr(), variant=v)  # the counter-free build
+        torch.cuda.synchronize()
+        assert torch.equal(h, h2), (layout, v)
+        out[v] = (h, st, c)
+    for a, b in zip(out[1], out[5]):
+        assert torch.equal(a, b), layout
+    got = out[5][0].cpu().numpy().view(sb.HIT_DTYPE)
+    want, _ = oracle.closest_hit(oracle.tree_bytes(pt), world["rays"])
+    assert np.array_equal(got["prim"], want["prim"]) and np.array_equal(got["t"].view(np.uint32), want["t"].view(np.uint32))
+    dt.free()
+
+
 def test_two_rays_per_lane_variant_is_identical(built, torch_cuda, world):
     """experimental kernel variant 3 (two rays per lane, the next record's load of one ray in flight while the other
     ray's step executes; emitted fetch() / decode_fetched()) must return exactly the default kernel's records and
