@@ -437,29 +437,59 @@ def main():
     dt = headline["dt"]
     if not args.no_e2e:
         try:
-            h_q = torch.empty(count * q_bytes, dtype=torch.uint8).pin_memory()
+            # closest_hit: host rays in the reference's own packed Ray record (7 x f32 = 28 B, geometry.scion:4) through
+            # scion_closest_hit_host_packed; closest_point: xyz points.  The padded 32-byte scion_ray form of the call is
+            # timed next to it (e2e.padded32) for comparison.
+            chrt = wl.algorithm == "chrt"
             h_r = torch.empty(count * r_bytes, dtype=torch.uint8).pin_memory()
             W.generate_device(wl, dt, lo, hi, first, count, d_q.data_ptr())
-            h_q.copy_(d_q)
+            if chrt:
+                d7 = d_q.view(torch.float32).view(-1, 8)[:, [0, 1, 2, 4, 5, 6, 3]].contiguous()
+                h_q = torch.empty(count * 28, dtype=torch.uint8).pin_memory()
+                h_q.copy_(d7.view(torch.uint8).view(-1))
+                del d7
+                in_bytes = 28
+            else:
+                h_q = torch.empty(count * q_bytes, dtype=torch.uint8).pin_memory()
+                h_q.copy_(d_q)
+                in_bytes = q_bytes
             run_step(dt)  # device-path result of the headline layout, for the equality check below
             torch.cuda.synchronize()
-            hq = h_q.numpy().view(sb.RAY_DTYPE if wl.algorithm == "chrt" else np.float32)
-            hr = h_r.numpy().view(sb.HIT_DTYPE if wl.algorithm == "chrt" else sb.CP_DTYPE)
-            call = (lambda: dt.closest_hit_host(hq, hr)) if wl.algorithm == "chrt" else (lambda: dt.closest_point_host(hq, hr))
-            call()
-            if world > 1:
-                dist.barrier()
-            esteps = max(1, min(3, args.steps))
-            t0 = time.perf_counter()
-            for _ in range(esteps):
-                call()
-            t_e = torch.tensor([(time.perf_counter() - t0) / esteps], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+            hq = h_q.numpy().view(np.float32).reshape(-1, 7) if chrt else h_q.numpy().view(np.float32)
+            hr = h_r.numpy().view(sb.HIT_DTYPE if chrt else sb.CP_DTYPE)
+            call = (lambda: dt.closest_hit_host_packed(hq, hr)) if chrt else (lambda: dt.closest_point_host(hq, hr))
+
+            def time_calls(fn):
+                fn()
+                if world > 1:
+                    dist.barrier()
+                esteps = max(1, min(3, args.steps))
+                t0 = time.perf_counter()
+                for _ in range(esteps):
+                    fn()
+                t = torch.tensor([(time.perf_counter() - t0) / esteps], dtype=torch.float64, device=dev)
+                if world > 1:
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                return float(t.item())
+
+            t_e = time_calls(call)
             # the device result must equal the e2e result
             same = bool(torch.equal(h_r.to(dev), d_r))
-            e2e = {"value": wl.total / float(t_e.item()) / 1e6, "unit": unit, "h2d_bytes_per_step": count * q_bytes, "d2h_bytes_per_step": count * r_bytes,
-                   "ms_per_step": float(t_e.item()) * 1e3, "matches_device_path": same}
+            e2e = {"value": wl.total / t_e / 1e6, "unit": unit, "h2d_bytes_per_step": count * in_bytes, "d2h_bytes_per_step": count * r_bytes,
+                   "ms_per_step": t_e * 1e3, "matches_device_path": same,
+                   "call": "scion_closest_hit_host_packed (host rays = the reference's packed 28-byte Ray record)" if chrt else "scion_closest_point_host"}
+            if chrt:
+                try:  # the padded 32-byte scion_ray form of the same call
+                    del h_q
+                    h_q = torch.empty(count * q_bytes, dtype=torch.uint8).pin_memory()
+                    h_q.copy_(d_q)
+                    hq32 = h_q.numpy().view(sb.RAY_DTYPE)
+                    h_r.zero_()
+                    t32 = time_calls(lambda: dt.closest_hit_host(hq32, hr))
+                    e2e["padded32"] = {"value": wl.total / t32 / 1e6, "ms_per_step": t32 * 1e3, "h2d_bytes_per_step": count * q_bytes,
+                                       "matches_device_path": bool(torch.equal(h_r.to(dev), d_r)), "call": "scion_closest_hit_host (32-byte scion_ray)"}
+                except Exception as ex:
+                    e2e["padded32"] = {"error": str(ex)[:160]}
             del h_q, h_r
         except Exception as ex:  # e.g. not enough pinnable host memory on the box
             e2e = {"value": None, "unit": unit, "error": str(ex)[:200]}
@@ -524,8 +554,9 @@ def main():
                 "config": {"workload": f"{wl.name}: {wl.description}", "layout": args.layout, "queries": wl.total, "queries_per_gpu": count,
                            "l2_policy": "inputs larger than L2 (rays %.1f GB + tree %.2f GB per GPU vs 126 MB L2); no explicit flush" % (count * q_bytes / 1e9, h["pt"].total_bytes / 1e9),
                            "partition": "contiguous query ranges per rank; tree replicated by one ncclBroadcast of the packed image (scion_dtree_broadcast)", "build_s": build_s,
-                           "e2e_note": "e2e is PCIe-bound: 32 B in + 8 B out per ray over a Gen5 x16 link (measured ~55 GB/s H2D with both directions busy, tools/pcie_probe.py) "
-                                       "puts the floor of this call shape at ~162 ms for 2^28 rays; the 3-stream pipeline runs within a few % of it"},
+                           "e2e_note": "e2e is PCIe-bound: 28 B in (the reference's packed Ray record) + 8 B out per ray over a Gen5 x16 link (measured ~53 GB/s H2D with both "
+                                       "directions busy, tools/pcie_probe.py) puts the floor of this call shape at ~142 ms for 2^28 rays (162 ms with 32-byte padded rays); "
+                                       "the 3-stream pipeline runs within a few % of it"},
                 "roofline": {"bound": "hbm", "achieved": h["gbs"], "peak": peak, "unit": "GB/s", "frac": h["gbs"] / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                              "bytes_per_query": h["bpq"], "frac_of_nominal_8tbs": h["gbs"] / 8000.0},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(h["launches"]), "clocks": h["clocks"], "layouts": results}

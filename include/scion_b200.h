@@ -331,6 +331,13 @@ int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64
                            uint32_t* h_status /* nullable */);
 int scion_closest_point_host(const scion_dtree* t, const float* h_points_xyz, uint64_t n, scion_cp* h_out,
                              uint32_t* h_status);
+/* The same call for rays in the reference's own packed record — Ray(origin, direction, tmax), 7 x f32 = 224 bits
+ * (corpus/lib/geometry.scion:4, packed sum of members: src/sema.cpp:47-87) — i.e. exactly what an array of the DSL's
+ * Ray values is on the host.  28 instead of 32 bytes cross the PCIe link per ray (the call is H2D-bound); the rays are
+ * widened to scion_ray on the device (scion_rays_unpack, also usable on its own for device-resident packed rays). */
+int scion_closest_hit_host_packed(const scion_dtree* t, const float* h_rays7, uint64_t n, scion_hit* h_hits,
+                                  uint32_t* h_status /* nullable */);
+int scion_rays_unpack(const float* d_rays7, uint64_t n, scion_ray* d_rays, void* stream);
 
 /* ------------------------------------------------------------------------- */
 /* Query generators (src/rng.cpp placeholder): every query is

@@ -33,6 +33,17 @@ MISS_PRIM = 0xFFFFFFFF
 FAMILY_BVH2, FAMILY_DOP14, FAMILY_BVH8 = 0, 1, 2
 W_SENTINEL = -(2 ** 31)
 
+def pack_rays(rays: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """scion_ray records -> the reference's packed Ray record, float32 [n, 7] = origin, direction, tmax (geometry.scion:4)"""
+    v = rays.view(np.float32).reshape(-1, 8)
+    if out is None:
+        out = np.empty((v.shape[0], 7), np.float32)
+    out[:, 0:3] = v[:, 0:3]
+    out[:, 3:6] = v[:, 4:7]
+    out[:, 6] = v[:, 3]
+    return out
+
+
 RAY_DTYPE = np.dtype([("ox", "f4"), ("oy", "f4"), ("oz", "f4"), ("tmax", "f4"), ("dx", "f4"), ("dy", "f4"), ("dz", "f4"), ("pad", "f4")])
 HIT_DTYPE = np.dtype([("t", "f4"), ("prim", "u4")])
 CP_DTYPE = np.dtype([("d2", "f4"), ("x", "f4"), ("y", "f4"), ("z", "f4"), ("prim", "u4")])
@@ -156,6 +167,8 @@ def lib() -> C.CDLL:
         "scion_collision_detection": (i32, [vp, vp, vp, u64, P(u64), P(CdStats), u64, vp]),
         "scion_collision_detection_host": (i32, [vp, vp, vp, u64, P(u64), P(CdStats)]),
         "scion_closest_hit_host": (i32, [vp, vp, u64, vp, vp]),
+        "scion_closest_hit_host_packed": (i32, [vp, vp, u64, vp, vp]),
+        "scion_rays_unpack": (i32, [vp, u64, vp, vp]),
         "scion_closest_point_host": (i32, [vp, vp, u64, vp, vp]),
         "scion_camera_default": (None, [P(C.c_float * 3), P(C.c_float * 3), i32, u32, u32, P(Camera)]),
         "scion_gen_primary": (i32, [P(Camera), u64, u64, vp, vp]),
@@ -588,6 +601,15 @@ class DeviceTree:
         if hits is None:
             hits = np.empty(n, HIT_DTYPE)
         _check(lib().scion_closest_hit_host(self._h, rays.ctypes.data, n, hits.ctypes.data, status.ctypes.data if status is not None else None))
+        return hits
+
+    def closest_hit_host_packed(self, rays7: np.ndarray, hits: Optional[np.ndarray] = None, status: Optional[np.ndarray] = None):
+        """rays as the reference's packed Ray record: float32 [n, 7] = origin, direction, tmax (geometry.scion:4)"""
+        assert rays7.dtype == np.float32 and rays7.flags.c_contiguous and rays7.ndim == 2 and rays7.shape[1] == 7
+        n = rays7.shape[0]
+        if hits is None:
+            hits = np.empty(n, HIT_DTYPE)
+        _check(lib().scion_closest_hit_host_packed(self._h, rays7.ctypes.data, n, hits.ctypes.data, status.ctypes.data if status is not None else None))
         return hits
 
     def closest_point_host(self, points: np.ndarray, out: Optional[np.ndarray] = None, status: Optional[np.ndarray] = None):

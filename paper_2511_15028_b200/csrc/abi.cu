@@ -708,6 +708,7 @@ void scion_dtree_free(scion_dtree* t) {
     if (t->ev_out[i]) cudaEventDestroy(t->ev_out[i]);
     if (t->h2d[i]) cudaFree(t->h2d[i]);
     if (t->d2h[i]) cudaFree(t->d2h[i]);
+    if (t->pk[i]) cudaFree(t->pk[i]);
     if (t->d_status[i]) cudaFree(t->d_status[i]);
   }
   t->counters.destroy();
@@ -830,12 +831,24 @@ int scion_collision_detection_host(const scion_dtree* a, const scion_dtree* b, s
 //   download(c) waits for kernel(c)
 // so the H2D copy engine never idles behind a kernel or a D2H copy of its own slot: the call runs at
 // the speed of the slowest of the three (on a PCIe Gen5 x16 B200 the 32-byte rays: ~55 GB/s).
-static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uint64_t n, void* h_out, uint32_t* h_status) {
+namespace scion {
+// the reference's packed Ray record (corpus/lib/geometry.scion:4: origin, direction, tmax — 7 x f32, 28 bytes) -> scion_ray
+__global__ void unpack_rays_kernel(const float* __restrict__ packed, uint64_t n, scion_ray* __restrict__ rays) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* p = packed + 7 * i;
+  const float ox = __ldcs(p), oy = __ldcs(p + 1), oz = __ldcs(p + 2), dx = __ldcs(p + 3), dy = __ldcs(p + 4), dz = __ldcs(p + 5), tmax = __ldcs(p + 6);
+  float4* o = reinterpret_cast<float4*>(rays + i);
+  o[0] = make_float4(ox, oy, oz, tmax);
+  o[1] = make_float4(dx, dy, dz, 0.0f);
+}
+}  // namespace scion
+static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uint64_t n, void* h_out, uint32_t* h_status, bool packed_rays = false) {
   if (!ct || (!h_in && n) || (!h_out && n)) return fail(SCION_ERR_ARG, "null argument");
   scion_dtree* t = const_cast<scion_dtree*>(ct);
   std::lock_guard<std::mutex> lock(t->host_mutex);
   CUDA_OK(cudaSetDevice(t->device));
-  const uint64_t in_sz = hit ? sizeof(scion_ray) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
+  const uint64_t in_sz = hit ? (packed_rays ? 28 : sizeof(scion_ray)) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
   // chunk size: an eighth of the call, between 2^19 and 2^23 queries (every chunk kernel pays ~0.5 ms of
   // ramp-up and ragged tail, so small chunks are kernel-bound: 2^28 rays run in 225 / 224 / 185 / 183 ms
   // with 2^20 / 2^21 / 2^22 / 2^23-query chunks); SCION_HOST_CHUNK_LOG2 overrides
@@ -862,6 +875,14 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
     }
     t->chunk = kChunk;
   }
+  if (packed_rays && t->pk_chunk < t->chunk) {  // 28-byte staging of the packed entry point, first use only
+    t->pk_chunk = 0;
+    for (int i = 0; i < S; i++) {
+      if (t->pk[i]) { cudaFree(t->pk[i]); t->pk[i] = nullptr; }
+      CUDA_OK(cudaMalloc(&t->pk[i], t->chunk * 28));
+    }
+    t->pk_chunk = t->chunk;
+  }
   // kernels alternate between two streams: the ragged tail of chunk c (a persistent grid drains at the
   // pace of its longest queries) overlaps the head of chunk c + 1
   cudaStream_t s_in = t->streams[0], s_out = t->streams[3];
@@ -874,10 +895,15 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
       cudaStream_t s_run = t->streams[1 + (c & 1)];
       const uint64_t m = std::min(kChunk, n - off);
       if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_in, t->ev_run[k], 0));
-      CUDA_OK(cudaMemcpyAsync(t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
+      CUDA_OK(cudaMemcpyAsync(packed_rays ? t->pk[k] : t->h2d[k], (const uint8_t*)h_in + off * in_sz, m * in_sz, cudaMemcpyHostToDevice, s_in));
       CUDA_OK(cudaEventRecord(t->ev_in[k], s_in));
       CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_in[k], 0));
       if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_out[k], 0));
+      if (packed_rays) {  // 28 -> 32 bytes on the device: ~0.1 ms per 2^23-ray chunk, behind the upload of the next chunk
+        scion::unpack_rays_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s_run>>>((const float*)t->pk[k], m, (scion_ray*)t->h2d[k]);
+        CUDA_OK(cudaGetLastError());
+        g_launches.fetch_add(1);
+      }
       int rc = run_query(t, hit, t->h2d[k], m, t->d2h[k], h_status ? t->d_status[k] : nullptr, nullptr, 0, s_run);
       if (rc) return rc;
       CUDA_OK(cudaEventRecord(t->ev_run[k], s_run));
@@ -901,6 +927,17 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
 }
 int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64_t n, scion_hit* h_hits, uint32_t* h_status) {
   return run_query_host(t, true, h_rays, n, h_hits, h_status);
+}
+int scion_closest_hit_host_packed(const scion_dtree* t, const float* h_rays7, uint64_t n, scion_hit* h_hits, uint32_t* h_status) {
+  return run_query_host(t, true, h_rays7, n, h_hits, h_status, true);
+}
+int scion_rays_unpack(const float* d_rays7, uint64_t n, scion_ray* d_rays, void* stream) {
+  if ((!d_rays7 || !d_rays) && n) return fail(SCION_ERR_ARG, "null argument");
+  if (n == 0) return SCION_OK;
+  scion::unpack_rays_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_rays7, n, d_rays);
+  CUDA_OK(cudaGetLastError());
+  g_launches.fetch_add(1);
+  return SCION_OK;
 }
 int scion_closest_point_host(const scion_dtree* t, const float* h_points, uint64_t n, scion_cp* h_out, uint32_t* h_status) {
   return run_query_host(t, false, h_points, n, h_out, h_status);

@@ -121,6 +121,8 @@ struct scion_dtree {
   static constexpr int kSlots = 4;  // staging slots of the host entry points: H2D(k+1) || kernel(k) || D2H(k-1)
   void* h2d[kSlots] = {};
   void* d2h[kSlots] = {};
+  void* pk[kSlots] = {};  // packed-ray staging (scion_closest_hit_host_packed), allocated on first use
+  uint64_t pk_chunk = 0;
   uint32_t* d_status[kSlots] = {};
   cudaStream_t streams[kSlots] = {};  // [0] uploads, [1] and [2] kernels (alternating), [3] downloads
   cudaEvent_t ev_in[kSlots] = {}, ev_run[kSlots] = {}, ev_out[kSlots] = {};

@@ -362,6 +362,33 @@ def test_two_rays_per_lane_variant_is_identical(built, torch_cuda, world):
         dt.free()
 
 
+def test_packed_ray_host_entry_is_identical(built, torch_cuda, world):
+    """scion_closest_hit_host_packed (host rays in the reference's packed 28-byte Ray record: origin, direction, tmax —
+    geometry.scion:4) must return exactly what scion_closest_hit_host returns for the same rays as 32-byte scion_ray
+    records, records and per-query status, over several staging chunks and for an empty call; scion_rays_unpack on its own
+    must reproduce the scion_ray array (pad = 0)"""
+    sb, torch = built, torch_cuda
+    rays = np.concatenate([world["rays"]] * 3)  # a few thousand rays; the chunking is exercised through SCION_HOST_CHUNK_LOG2 in the fullsize tests
+    rays["pad"] = 0.0
+    packed = sb.pack_rays(rays)
+    assert packed.shape == (rays.shape[0], 7) and packed.dtype == np.float32
+    for layout in ("pbrt-q16", "bvh8-q8-ci", "dop14"):
+        dt = world["lt"].encode(layout).upload(0)
+        sa, sb_ = np.full(rays.shape[0], 7, np.uint32), np.full(rays.shape[0], 9, np.uint32)
+        a = dt.closest_hit_host(rays, status=sa)
+        b = dt.closest_hit_host_packed(packed, status=sb_)
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), layout
+        assert np.array_equal(sa, sb_), layout
+        assert dt.closest_hit_host_packed(packed[:0]).shape[0] == 0
+        dt.free()
+    d_p = torch.from_numpy(packed.reshape(-1)).to("cuda:0")
+    d_r = torch.full((rays.shape[0] * 8,), 5.0, dtype=torch.float32, device="cuda:0")
+    from paper_2511_15028_b200 import lib, _check
+    _check(lib().scion_rays_unpack(d_p.data_ptr(), rays.shape[0], d_r.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(d_r.cpu().numpy().view(np.uint32), rays.view(np.uint32).reshape(-1))
+
+
 def test_fault_injection_changes_results(built, oracle, torch_cuda, world):
     """corrupting one c_o byte must surface as >= 1 mismatch against the oracle of the intact tree"""
     sb = built
