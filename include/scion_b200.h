@@ -204,6 +204,13 @@ void scion_ltree_free(scion_ltree* t);
 /* build_physical: LogicalTree -> byte buffers + globals + root ref */
 /* ------------------------------------------------------------------------- */
 int scion_encode(const scion_ltree* t, const char* layout, scion_ptree** out);
+/* The same through the layout's own `build` block (constructor specialisation):
+ * the layout compiler turns the block into per-variant constructors (gen/<layout>.cuh build_<Variant>()) that run a
+ * count pass + a recursive emit pass on the host.  scion_encode is the fast path (hand-restated per family, OpenMP or
+ * device-side); the two must produce byte-identical trees (tests/test_generated_build.py).  SCION_ERR_BUILD when the
+ * layout file carries no build block (scion_layout_has_build) or on a build fault (count / emit disagreement). */
+int scion_encode_generated(const scion_ltree* t, const char* layout, scion_ptree** out);
+int scion_layout_has_build(const char* layout);
 const char* scion_ptree_layout(const scion_ptree* p);
 int scion_ptree_nbuffers(const scion_ptree* p);
 int scion_ptree_buffer(const scion_ptree* p, int i, const char** name, const uint8_t** data,

@@ -51,6 +51,16 @@ static bool dump_one(const std::string& label, const std::vector<std::string>& f
     std::cerr << label << ": check_layout diagnostics: " << diags.size() << "\n";
     return false;
   }
+  // the reference's own check_build (src/sema_build.cpp) over the file's build block, when it carries one
+  if (const BuildSpec* cb = program.find_build(layout->name)) {
+    auto bd = check_build(*adt, *layout, const_cast<BuildSpec&>(*cb), program);
+    if (!bd.empty()) {
+      std::cerr << label << ": check_build diagnostics: " << bd.size() << "\n";
+      for (auto& d : bd) std::cerr << "  " << d.message << "\n";
+      return false;
+    }
+    std::cerr << label << ": check_build ok\n";
+  }
   MemoryPlan plan = plan_layout(*adt, *layout, program);
   os << "  \"" << esc(label) << "\": {\n";
   os << "    \"adt\": \"" << esc(plan.adt_name) << "\",\n    \"ref\": [";

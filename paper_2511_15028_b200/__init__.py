@@ -136,6 +136,8 @@ def lib() -> C.CDLL:
         "scion_ltree_wroot": (C.c_int32, [vp]),
         "scion_ltree_free": (None, [vp]),
         "scion_encode": (i32, [vp, cp, P(vp)]),
+        "scion_encode_generated": (i32, [vp, cp, P(vp)]),
+        "scion_layout_has_build": (i32, [cp]),
         "scion_ptree_layout": (cp, [vp]),
         "scion_ptree_nbuffers": (i32, [vp]),
         "scion_ptree_buffer": (i32, [vp, i32, P(cp), P(vp), P(u64), P(u64)]),
@@ -403,6 +405,13 @@ class LogicalTree:
     def encode(self, layout: str) -> "PhysicalTree":
         h = C.c_void_p()
         _check(lib().scion_encode(self._h, layout.encode(), C.byref(h)))
+        return PhysicalTree(h)
+
+    def encode_generated(self, layout: str) -> "PhysicalTree":
+        """build_physical through the layout's own `build` block, compiled by the layout compiler (constructor
+        specialisation); must be byte-identical to encode(layout)."""
+        h = C.c_void_p()
+        _check(lib().scion_encode_generated(self._h, layout.encode(), C.byref(h)))
         return PhysicalTree(h)
 
     def encode_device(self, layout: str, device: int = 0) -> "DeviceTree":

@@ -15,6 +15,7 @@
 
 #include "device/geometry.cuh"
 #include "device/launch.cuh"
+#include "host/build_ctx.hpp"
 #include "host/dtree.hpp"
 #include "host/encode_node.hpp"
 #include "host/physical.hpp"
@@ -282,6 +283,16 @@ int scion_encode(const scion_ltree* t, const char* layout, scion_ptree** out) {
   SCION_TRY(const scion::LayoutEntry* e = scion::find_layout(layout); if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + layout + "'");
             if (e->plan->family == scion::lc::Family::Bvh8 && !t->has_wide) return fail(SCION_ERR_BUILD, "8-wide layouts need scion_ltree_collapse8 first");
             auto* p = new scion_ptree(); try { scion::encode_tree(*t, *e, *p); } catch (...) { delete p; throw; } *out = p; return SCION_OK;)
+}
+int scion_encode_generated(const scion_ltree* t, const char* layout, scion_ptree** out) {
+  if (!t || !layout || !out) return fail(SCION_ERR_ARG, "null argument");
+  SCION_TRY(const scion::LayoutEntry* e = scion::find_layout(layout); if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + layout + "'");
+            if (e->plan->family == scion::lc::Family::Bvh8 && !t->has_wide) return fail(SCION_ERR_BUILD, "8-wide layouts need scion_ltree_collapse8 first");
+            auto* p = new scion_ptree(); try { scion::encode_tree_generated(*t, *e, *p); } catch (...) { delete p; throw; } *out = p; return SCION_OK;)
+}
+int scion_layout_has_build(const char* layout) {
+  const scion::BuilderEntry* b = layout ? scion::find_builder(layout) : nullptr;
+  return b && b->build_root ? 1 : 0;
 }
 const char* scion_ptree_layout(const scion_ptree* p) { return p->layout.c_str(); }
 int scion_ptree_nbuffers(const scion_ptree* p) { return (int)p->buffers.size(); }

@@ -11,6 +11,7 @@
 // *generated decoders* can be unit-tested on a machine without a GPU (tests only; nothing in the
 // product calls the host mode).
 #pragma once
+#include <stddef.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -642,6 +643,24 @@ SCION_HOSTDEV uint64_t ext64(const Src& r) {
 template <int OFF, class Src>
 SCION_HOSTDEV float extf(const Src& r) {
   return u2f(ext32<OFF, 32>(r));
+}
+
+// constant-offset field store into a zero-initialised record image: write_bits_raw (/root/reference/proj/src/bits.cpp:21-36)
+// specialised to constant offsets — used by the emitted constructors (build_<Variant>, the compiled `build` block)
+template <int OFF, int W>
+SCION_HOSTDEV void dep32(uint32_t* w, uint32_t v) {
+  static_assert(W >= 1 && W <= 32, "dep32 width");
+  constexpr int i = OFF / 32, s = OFF % 32;
+  const uint32_t m = (uint32_t)((1ull << W) - 1ull);
+  v &= m;
+  w[i] = (w[i] & ~(m << s)) | (v << s);
+  if constexpr (s + W > 32) w[i + 1] = (w[i + 1] & ~(m >> (32 - s))) | (v >> (32 - s));
+}
+template <int OFF, int W>
+SCION_HOSTDEV void dep64(uint32_t* w, uint64_t v) {
+  static_assert(W > 32 && W <= 64, "dep64 width");
+  dep32<OFF, 32>(w, (uint32_t)v);
+  dep32<OFF + 32, W - 32>(w, (uint32_t)(v >> 32));
 }
 
 template <class T> SCION_HOSTDEV T glob(const TreeView& T_, int i);

@@ -16,6 +16,7 @@
 #include <limits>
 #include <stdexcept>
 
+#include "build_ctx.hpp"
 #include "encode_node.hpp"
 #include "physical.hpp"
 
@@ -293,6 +294,56 @@ void encode_tree(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& o
   const int64_t n = (int64_t)job.count;
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; i++) enc::encode_one(job, (uint64_t)i);
+}
+
+// build_physical through the layout's own `build` block, compiled by emit_cuda into gen/<layout>.cuh build_node()
+// (SPEC.md:276-284, :387-395).  (a) count pass: every buffer is sized from the LogicalTree and the plan's variant_home
+// (which buffer a variant materialises in) and allocated exactly once; (b) recursive emit pass in the order the build
+// block prescribes; (c) count / emit agreement is checked — a mismatch is a hard fault.
+void encode_tree_generated(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& out) {
+  const BuilderEntry* be = find_builder(layout.name.c_str());
+  if (!be || !be->build_root) throw std::runtime_error("layout '" + layout.name + "' carries no build block");
+  encode_tree_with(t, layout, be->build_root, out);
+}
+void encode_tree_with(const scion_ltree& t, const LayoutEntry& layout, build_root_fn build_root, scion_ptree& out) {
+  const lc::Plan& plan = *layout.plan;
+  init_ptree(t, layout, out);
+  const bool wide = plan.family == lc::Family::Bvh8;
+  if (wide) require(t.has_wide, "8-wide layouts need a collapsed tree (scion_ltree_collapse8)");
+  // logical nodes per variant (variant 0 = Interior, 1 = Leaf in every ADT of the corpus)
+  uint64_t per_variant[2] = {0, 0};
+  if (wide) {
+    per_variant[0] = t.wnodes.size();
+    per_variant[1] = t.wleaves.size();
+    for (auto& l : t.wleaves) require(l.nprims >= 1 && l.nprims <= plan.max_leaf, "8-wide leaf exceeds the nprims capacity of layout " + plan.layout_name);
+  } else {
+    for (auto& n : t.nodes) per_variant[n.left < 0 ? 1 : 0]++;
+  }
+  Writer w(out, plan, false);
+  for (auto& b : plan.buffers) {
+    uint64_t count = 0;
+    if (b.is_global_array) {
+      count = t.tris.size() / 9;
+    } else {
+      for (size_t v = 0; v < plan.adt->variants.size() && v < 2; v++) {
+        auto it = plan.variant_home.find(plan.adt->variants[v].name);
+        if (it != plan.variant_home.end() && it->second == b.id) count += per_variant[v];
+      }
+    }
+    const uint64_t arena = b.is_arena ? (count ? (count - 1) * arena_stride(b) + b.segments[0].stride_bytes : 0) + 8 : 0;
+    w.alloc(b.name, count, arena);
+    for (size_t g = 0; g < plan.globals.size(); g++)
+      if (plan.globals[g].name == b.count_name) w.global_u(b.count_name, count);
+  }
+  BuildCtx ctx(t, plan, out);
+  ctx.root_id = wide ? (int64_t)t.wroot : 0;
+  if (wide ? t.wroot == SCION_W_SENTINEL : t.nodes.empty()) throw std::runtime_error("build fault: empty tree");
+  out.root0 = build_root(ctx);
+  for (auto& b : plan.buffers) {
+    const uint64_t used = ctx.cursor[(size_t)b.id];
+    const uint64_t want = b.is_arena ? (out.counts[(size_t)b.id] ? out.counts[(size_t)b.id] * arena_stride(b) : 0) : out.counts[(size_t)b.id];
+    require(used == want, "count pass and emit pass disagree on buffer '" + b.name + "' (" + std::to_string(used) + " vs " + std::to_string(want) + ")");
+  }
 }
 
 void encode_shell(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& out, enc::EncodeJob& job, std::vector<uint32_t>& post) {

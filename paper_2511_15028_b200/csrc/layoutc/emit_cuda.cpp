@@ -77,14 +77,21 @@ struct Emitter {
         return e->has_u ? s + "u" : s;
       }
       case Expr::FloatLit: return float_lit(e->text);
+      case Expr::BuildChild:  // constructor context: build the child, the value is its reference
+        return "(uint64_t)b__.template child<Self__>(n__." + e->text + ")";
       case Expr::Ident:
         if (e->text == "inf") return "scion::inf()";
+        if (in_build && e->text == "this") return "this__";
         if (in_layout && ref_names.count(e->text)) return ref_is_struct ? "ref__." + e->text : "ref__";
         return e->text;
       case Expr::Binary: return "(" + ex(e->args[0], in_layout) + " " + e->text + " " + ex(e->args[1], in_layout) + ")";
       case Expr::Unary: return "(" + e->text + ex(e->args[0], in_layout) + ")";
       case Expr::Call: {
         std::string fn;
+        if (in_build && e->text == "append") {  // append(data, n): copy the leaf's primitives behind the cursor, the value is the start
+          if (e->args.size() != 2) throw LayoutError("append takes (data, count)");
+          return "b__.append(n__." + ex(e->args[0], in_layout) + ", (uint64_t)(" + ex(e->args[1], in_layout) + "))";
+        }
         if (is_intrinsic(e->text)) {
           fn = e->text == "cross_" ? "cross" : e->text == "floorf" ? "floorf_" : e->text == "ceilf" ? "ceilf_" : e->text;
           fn = "scion::" + fn;
@@ -221,6 +228,7 @@ struct Emitter {
     }
   }
   std::string cur_ret;
+  bool in_build = false;  // emitting a constructor of the build block: `this`, `append`, `build child` are legal
 
   // ------------------------------------------------------------------ field extraction
   std::string extract(const TypeP& t, uint64_t off, const std::string& words) const {
@@ -254,6 +262,214 @@ struct Emitter {
       case Type::Tuple: break;
     }
     throw LayoutError("cannot load a value of type " + t->str());
+  }
+
+  // typed store of `val` at bit offset `off` of the staged record image `words` (the inverse of extract)
+  void deposit(const TypeP& t, uint64_t off, const std::string& words, const std::string& val, const std::string& pad) {
+    auto o = std::to_string(off);
+    switch (t->kind) {
+      case Type::Float: out << pad << "scion::dep32<" << o << ", 32>(" << words << ", scion::f2u(" << val << "));\n"; return;
+      case Type::Bool: out << pad << "scion::dep32<" << o << ", 1>(" << words << ", (" << val << ") ? 1u : 0u);\n"; return;
+      case Type::Ptr: out << pad << "scion::dep64<" << o << ", 64>(" << words << ", (uint64_t)(" << val << "));\n"; return;
+      case Type::Int:
+        if (t->width > 32) out << pad << "scion::dep64<" << o << ", " << t->width << ">(" << words << ", (uint64_t)(" << val << "));\n";
+        else out << pad << "scion::dep32<" << o << ", " << t->width << ">(" << words << ", (uint32_t)(" << val << "));\n";
+        return;
+      case Type::Vec: case Type::Array: {
+        if (!t->len_field.empty()) break;
+        uint64_t ew = plan.type_bits(t->elem);
+        for (uint32_t i = 0; i < t->lanes; i++) deposit(t->elem, off + i * ew, words, val + "[" + std::to_string(i) + "]", pad);
+        return;
+      }
+      case Type::Named: {
+        const TypeDecl* d = prog.find_type(t->name);
+        if (!d || d->is_adt()) break;
+        uint64_t o2 = off;
+        for (auto& f : d->fields) {
+          deposit(f.type, o2, words, val + "." + f.name, pad);
+          o2 += plan.type_bits(f.type);
+        }
+        return;
+      }
+      case Type::Tuple: break;
+    }
+    throw LayoutError("cannot store a value of type " + t->str());
+  }
+
+  // ------------------------------------------------------------------ constructor emission (build blocks)
+  // SPEC.md:276-284 specialize_constructors / PAPER.md:1495-1569: per variant one function that reserves this node's
+  // storage (before the children for order=pre, after them for order=post), evaluates the build statements — typed stores
+  // into a staged image of the record, `append` cursors, recursive child builds through the build context B
+  // (host/build_ctx.hpp) — and returns the node's reference.
+  bool is_child_type(const TypeP& t) const {
+    const Type* u = t.get();
+    if ((u->kind == Type::Array || u->kind == Type::Vec) && u->len_field.empty()) u = u->elem.get();
+    if (u->kind != Type::Named) return false;
+    const TypeDecl* d = prog.find_type(u->name);
+    return d && d->is_adt();
+  }
+  bool stmt_builds_child(const StmtP& st, const BuildCtor& c) const {
+    std::function<bool(const ExprP&)> has = [&](const ExprP& e) -> bool {
+      if (!e) return false;
+      if (e->kind == Expr::BuildChild) return true;
+      for (auto& a : e->args)
+        if (has(a)) return true;
+      return false;
+    };
+    if (has(st->value) || has(st->lhs) || has(st->cond)) return true;
+    if (st->kind == Stmt::Build && !st->value)
+      for (auto& pa : c.params)
+        if (pa.name == st->name && is_child_type(pa.type)) return true;
+    return false;
+  }
+  void emit_build() {
+    const BuildDecl* bd = nullptr;
+    for (auto& b : prog.builds)
+      if (b.adt == plan.adt->name) bd = &b;
+    out << "  static constexpr bool kHasBuild = " << (bd ? "true" : "false") << ";  // build_node(): the layout's `build` block, compiled\n";
+    if (!bd) return;
+    const bool post = bd->order == "post";
+    out << "  static constexpr bool kBuildPost = " << (post ? "true" : "false") << ";\n";
+    const std::string self = "L_" + ident_of(plan.layout_name);
+    const std::string this_t = ctype(plan.ref[0].type);
+    in_build = true;
+    for (auto& c : bd->ctors) {
+      const Variant* v = find_variant(c.variant);
+      if (!v) throw LayoutError("build block names unknown variant " + c.variant);
+      auto hit = plan.variant_home.find(c.variant);
+      const int home = hit == plan.variant_home.end() ? -1 : hit->second;
+      const Buffer* hb = home >= 0 ? &plan.buffers[(size_t)home] : nullptr;
+      // helper funcs the constructor reaches are emitted with the decode helpers (reach() in run())
+      out << "  template <class B>\n  static uint64_t build_" << c.variant << "(B& b__, const typename B::Node& n__) {\n";
+      out << "    using Self__ = " << self << ";\n";
+      if (hb)
+        for (size_t sg = 0; sg < hb->segments.size(); sg++)
+          out << "    uint32_t rec" << sg << "__[" << (hb->segments[sg].stride_bytes + 3) / 4 + 1 << "] = {0};\n";
+      for (auto& pa : c.params) {
+        if (is_child_type(pa.type)) continue;                                   // children are built, not read
+        if (pa.type->kind == Type::Array && !pa.type->len_field.empty()) continue;  // data: only `append` touches it
+        out << "    const " << ctype(pa.type) << " " << pa.name << " = (" << ctype(pa.type) << ")n__." << pa.name << ";\n";
+      }
+      auto reserve = [&]() {
+        if (!hb) { out << "    const " << this_t << " this__ = 0;\n"; return; }
+        uint64_t bytes = hb->segments[0].stride_bytes;
+        if (hb->is_arena) bytes = (bytes + hb->align - 1) / hb->align * hb->align;
+        out << "    const " << this_t << " this__ = (" << this_t << ")b__.reserve(" << hb->id << ", " << bytes << "ull);\n";
+      };
+      size_t last_child = 0;
+      bool any_child = false;
+      for (size_t i = 0; i < c.body.size(); i++)
+        if (stmt_builds_child(c.body[i], c)) { last_child = i; any_child = true; }
+      if (!post || !any_child) reserve();
+      // globals the statements outside the root block read
+      std::set<std::string> ids;
+      std::function<void(const std::vector<StmtP>&)> scan = [&](const std::vector<StmtP>& b) {
+        for (auto& st : b) {
+          if (st->kind == Stmt::BuildRoot) continue;
+          collect_idents(st->value, ids);
+          collect_idents(st->cond, ids);
+          scan(st->then_body);
+          scan(st->else_body);
+        }
+      };
+      scan(c.body);
+      std::set<std::string> param_names;
+      for (auto& pa : c.params) param_names.insert(pa.name);
+      auto read_globals = [&]() {
+        for (size_t g = 0; g < plan.globals.size(); g++)
+          if (ids.count(plan.globals[g].name) && !plan.globals[g].inferred && !param_names.count(plan.globals[g].name))
+            out << "    const " << ctype(plan.globals[g].type) << " " << plan.globals[g].name << " = b__.template glob<" << ctype(plan.globals[g].type) << ">(" << g << ");\n";
+      };
+      bool has_root_block = false;
+      for (auto& st : c.body)
+        if (st->kind == Stmt::BuildRoot) has_root_block = true;
+      if (!has_root_block) read_globals();
+      std::function<void(const StmtP&, const std::string&, bool)> emit_build_stmt = [&](const StmtP& st, const std::string& pad, bool in_root) {
+        const std::string& n = st->name;
+        // the value: the expression, or the same-named constructor parameter
+        bool child_param = false;
+        TypeP ptype;
+        for (auto& pa : c.params)
+          if (pa.name == n) { ptype = pa.type; child_param = is_child_type(pa.type); }
+        const Slot* slot = nullptr;
+        if (hb)
+          for (auto& sl : plan.slots)
+            if (sl.name == n && sl.buffer == hb->id) slot = &sl;
+        if (!st->value && child_param) {  // `build left;` / `build children;`
+          const bool many = ptype->kind == Type::Array || ptype->kind == Type::Vec;
+          if (many) {
+            out << pad << "scion::vec<uint64_t, " << ptype->lanes << "> " << n << "__refs;\n";
+            out << pad << "for (int k__ = 0; k__ < " << ptype->lanes << "; k__++) " << n << "__refs[k__] = (uint64_t)b__.template child<Self__>(n__." << n << "[k__]);\n";
+            if (slot) deposit(slot->type, slot->offset, "rec" + std::to_string(slot->segment) + "__", n + "__refs", pad);
+          } else {
+            out << pad << "const uint64_t " << n << "__ref = (uint64_t)b__.template child<Self__>(n__." << n << ");\n";
+            if (slot) deposit(slot->type, slot->offset, "rec" + std::to_string(slot->segment) + "__", n + "__ref", pad);
+            else out << pad << "(void)" << n << "__ref;\n";
+          }
+          return;
+        }
+        const std::string val = st->value ? ex(st->value, false) : n;
+        if (slot) {
+          out << pad << "{ const " << ctype(slot->type) << " v__ = (" << ctype(slot->type) << ")(" << val << ");\n";
+          deposit(slot->type, slot->offset, "rec" + std::to_string(slot->segment) + "__", "v__", pad + "  ");
+          out << pad << "}\n";
+          return;
+        }
+        for (size_t g = 0; g < plan.globals.size(); g++)
+          if (plan.globals[g].name == n) {
+            if (!in_root) throw LayoutError("build of global '" + n + "' outside a root block");
+            out << pad << "const " << ctype(plan.globals[g].type) << " " << n << " = (" << ctype(plan.globals[g].type) << ")(" << val << ");\n";
+            out << pad << "b__.set_global(" << g << ", " << n << ");\n";
+            return;
+          }
+        for (size_t r = 1; r < plan.ref.size(); r++)
+          if (plan.ref[r].name == n) {  // tree-carried component of the root reference (shared-slab: plo, phi)
+            if (!in_root) throw LayoutError("build of reference component '" + n + "' outside a root block");
+            out << pad << "const " << ctype(plan.ref[r].type) << " " << n << " = (" << ctype(plan.ref[r].type) << ")(" << val << ");\n";
+            out << pad << "b__.set_root_component(" << r << ", " << n << ");\n";
+            for (size_t g = 0; g < plan.globals.size(); g++)
+              if (plan.globals[g].name == "__ref_" + n) out << pad << "b__.set_global(" << g << ", " << n << ");\n";
+            return;
+          }
+        throw LayoutError("layout " + plan.layout_name + ": `build " + n + "` names neither a stored field of variant " + c.variant + "'s record, a global, a reference component nor a child");
+      };
+      bool returned = false;
+      for (size_t i = 0; i < c.body.size(); i++) {
+        const StmtP& st = c.body[i];
+        switch (st->kind) {
+          case Stmt::BuildRoot:
+            out << "    if (b__.is_root(n__)) {  // root block: runs once, before anything else of the build (SPEC.md:282)\n";
+            for (auto& rs : st->then_body) {
+              if (rs->kind == Stmt::Build) emit_build_stmt(rs, "      ", true);
+              else emit_stmts({rs}, 3);
+            }
+            out << "    }\n";
+            read_globals();
+            break;
+          case Stmt::Build: emit_build_stmt(st, "    ", false); break;
+          case Stmt::Return: {
+            if (!st->value) throw LayoutError("a constructor must return the node's reference");
+            out << "    const uint64_t ret__ = (uint64_t)(" << ex(st->value, false) << ");\n";
+            if (hb)
+              for (size_t sg = 0; sg < hb->segments.size(); sg++)
+                out << "    b__.commit(" << hb->id << ", " << sg << ", (uint64_t)this__, rec" << sg << "__, " << hb->segments[sg].stride_bytes << "ull);\n";
+            out << "    return ret__;\n";
+            returned = true;
+            break;
+          }
+          default: emit_stmts({st}, 2); break;
+        }
+        if (post && any_child && i == last_child) reserve();
+      }
+      if (!returned) throw LayoutError("constructor of " + c.variant + " does not return");
+      out << "  }\n";
+    }
+    out << "  template <class B>\n  static uint64_t build_node(B& b__, const typename B::Node& n__) {\n";
+    for (size_t i = 0; i < bd->ctors.size(); i++) {
+      out << "    " << (i ? "else " : "") << "if (n__.variant == " << variant_index(bd->ctors[i].variant) << ") return build_" << bd->ctors[i].variant << "(b__, n__);\n";
+    }
+    out << "    return 0;\n  }\n";
+    in_build = false;
   }
 
   // ------------------------------------------------------------------ decode emission
@@ -505,6 +721,14 @@ struct Emitter {
     find_groups(plan.layout->members);
     if (!primary) throw LayoutError("layout has no direct group indexed by a reference component");
     reach_members(plan.layout->members);
+    for (auto& b : prog.builds)
+      if (b.adt == plan.adt->name)
+        for (auto& c : b.ctors) {
+          std::vector<std::string> calls;
+          collect_calls(c.body, calls);
+          for (auto& f : calls)
+            if (f != "append") reach(f);
+        }
     if (primary_buf && primary_buf->segments.size() > 1) compute_cold(primary->members);
     bool has_cold = !cold_names.empty();
 
@@ -774,6 +998,7 @@ struct Emitter {
         (void)from_split;
       }
     }
+    emit_build();
     // prefetch(): pull the record a reference designates into L2 ahead of its visit (issued by the
     // traversal when the reference is pushed on the stack)
     out << "  template <int LEVEL = 2>  // 2: into L2 (a reference that was pushed); 1: into L1 (a record about to be visited)\n";

@@ -1,8 +1,8 @@
 // scionc — the layout compiler of the B200 backend.
 //
 // Reads the *layout language* of Scion (the `type`, `func` and `layout` declarations of a
-// .scion file; `build` blocks are recognised and skipped — the encoders restate them in
-// host/encode.cpp), plans the physical memory (bit-exact with the reference planner,
+// .scion file, and its `build` blocks: emit_cuda turns them into the generated constructors,
+// host/encode.cpp holds the hand-written per-family encoders they are checked against), plans the physical memory (bit-exact with the reference planner,
 // /root/reference/proj/src/plan.cpp:75-140, :174-241, :307-347) and emits, per layout, a
 // CUDA header with the device node record, slot constants and the decode routine
 // (emit_cuda — the sibling of the reference's emit_c slot).
@@ -44,7 +44,7 @@ struct Type {
 struct Expr;
 using ExprP = std::shared_ptr<Expr>;
 struct Expr {
-  enum Kind { IntLit, FloatLit, Ident, Binary, Unary, Call, Member, Index, Range, Cast, Construct, Brace, Tuple } kind = IntLit;
+  enum Kind { IntLit, FloatLit, Ident, Binary, Unary, Call, Member, Index, Range, Cast, Construct, Brace, Tuple, BuildChild } kind = IntLit;  // BuildChild: `build left` in expression position (text = the child parameter)
   uint64_t ival = 0;
   bool has_u = false;       // integer literal carried a 'u' suffix
   std::string text;         // FloatLit spelling, Ident / Call / Member name, operator
@@ -57,8 +57,10 @@ struct Expr {
 struct Stmt;
 using StmtP = std::shared_ptr<Stmt>;
 struct Stmt {
-  enum Kind { Let, Assign, If, Return, ExprS } kind = Let;
-  std::string name;  // Let
+  // Build / BuildRoot only occur in the constructors of a `build` block: `build X;`, `build X = e;` (name = X, value = e or
+  // null) and `build root { ... }` (then_body; runs once, for the root node, before anything else: SPEC.md:282)
+  enum Kind { Let, Assign, If, Return, ExprS, Build, BuildRoot } kind = Let;
+  std::string name;  // Let, Build
   TypeP type;        // Let
   bool is_mut = false;
   ExprP lhs, value, cond;
@@ -116,6 +118,19 @@ struct MemberNode {
   std::vector<Arm> arms;
 };
 
+// `build ADT[order=pre|post] { build Variant(params) { statements }; ... }` — the constructors of a layout
+// (SPEC.md:276-284 specialize_constructors)
+struct BuildCtor {
+  std::string variant;
+  std::vector<Param> params;  // the logical fields of the variant, by name
+  std::vector<StmtP> body;
+};
+struct BuildDecl {
+  std::string adt;
+  std::string order = "pre";
+  std::vector<BuildCtor> ctors;
+};
+
 struct Layout {
   std::string name;  // the ADT it realises
   std::vector<Param> ref;
@@ -126,7 +141,8 @@ struct Program {
   std::vector<TypeDecl> types;
   std::vector<Func> funcs;
   std::vector<Layout> layouts;
-  std::vector<std::string> build_orders;  // "pre"/"post" of each skipped build block
+  std::vector<std::string> build_orders;  // "pre"/"post" of each build block
+  std::vector<BuildDecl> builds;
   const TypeDecl* find_type(const std::string& n) const {
     for (auto& t : types)
       if (t.name == n) return &t;

@@ -364,6 +364,12 @@ struct Parser {
       expect("}");
       return b;
     }
+    if (in_build && is_kw("build")) {  // `let R: u32 = build right;`
+      p++;
+      auto e = mk(Expr::BuildChild);
+      e->text = ident("child name");
+      return e;
+    }
     if (t.kind == T::Ident) {
       std::string id = toks[p++].text;
       if (is_punct("{") && ident_is_type(id)) {  // T { a, b, c }
@@ -403,8 +409,24 @@ struct Parser {
     expect("}");
     return out;
   }
+  bool in_build = false;  // inside a constructor of a `build` block: `build ...` statements and expressions are legal
   StmtP parse_stmt() {
     auto s = std::make_shared<Stmt>();
+    if (in_build && is_kw("build")) {
+      p++;
+      if (is_kw("root") && look().kind == T::Punct && look().text == "{") {
+        p++;
+        s->kind = Stmt::BuildRoot;
+        s->then_body = parse_block();
+        accept(";");
+        return s;
+      }
+      s->kind = Stmt::Build;
+      s->name = ident("field or child name");
+      if (accept("=")) s->value = parse_expr();
+      expect(";");
+      return s;
+    }
     if (is_kw("let")) {
       p++;
       s->kind = Stmt::Let;
@@ -639,7 +661,7 @@ struct Parser {
   }
   void parse_build_decl() {
     p++;  // build
-    ident("build name");
+    const std::string adt = ident("build name");
     std::string order = "pre";
     if (accept("[")) {
       if (is_kw("order")) {
@@ -651,8 +673,33 @@ struct Parser {
       expect("]");
     }
     prog.build_orders.push_back(order);
-    if (!is_punct("{")) fail("expected '{'");
-    skip_balanced_block();
+    BuildDecl bd;
+    bd.adt = adt;
+    bd.order = order;
+    expect("{");
+    while (!is_punct("}")) {
+      if (!is_kw("build")) fail("expected 'build Variant(...)'");
+      p++;
+      BuildCtor c;
+      c.variant = ident("variant name");
+      expect("(");
+      if (!is_punct(")")) do {
+        Param pa;
+        pa.name = ident("parameter name");
+        expect(":");
+        pa.type = parse_type();
+        c.params.push_back(pa);
+      } while (accept(","));
+      expect(")");
+      in_build = true;
+      c.body = parse_block();
+      in_build = false;
+      accept(";");
+      bd.ctors.push_back(std::move(c));
+    }
+    expect("}");
+    accept(";");
+    prog.builds.push_back(std::move(bd));
   }
   void run() {
     while (cur().kind != T::End) {
