@@ -157,6 +157,16 @@ int scion_layout_stats_json(const char* name, char** out_json);
 /* Compile a layout spec from source text (layout-language subset of the
  * reference grammar, src/parser.cpp:790-955) and return plan JSON / CUDA text. */
 int scion_compile_layout_text(const char* scion_source, char** out_plan_json, char** out_cuda);
+/* Open-world layouts (constructor + destructor specialisation at run time): compile a layout the
+ * library was not built with and register it under `name`.  The text goes through the front end (SCION_ERR_LAYOUT with
+ * the reference's diagnostic classes when it is ill-formed), emit_cuda produces its header (decode, typed records, the
+ * constructors of its build block), nvcc instantiates every traversal kernel for it with the library's own flags, and
+ * the plugin is loaded into the process.  Afterwards scion_encode (through the layout's build block), scion_dtree_upload,
+ * scion_ptree_from_buffers, scion_closest_hit / _point, scion_collision_detection accept the name like a built-in's.
+ * Needs nvcc (SCION_NVCC, default /usr/local/cuda/bin/nvcc) and the library's device sources (SCION_B200_SRC, default
+ * csrc/ next to the library) at run time; takes about a minute.  work_dir: where the sources and the plugin are kept
+ * (null: a fresh directory under $TMPDIR).  *out_log (nullable, scion_free_string) receives the build log. */
+int scion_layout_register(const char* name, const char* scion_text, const char* work_dir, char** out_log);
 void scion_free(void* p);
 
 /* ------------------------------------------------------------------------- */

@@ -137,6 +137,7 @@ def lib() -> C.CDLL:
         "scion_ltree_free": (None, [vp]),
         "scion_encode": (i32, [vp, cp, P(vp)]),
         "scion_encode_generated": (i32, [vp, cp, P(vp)]),
+        "scion_layout_register": (i32, [cp, cp, cp, P(vp)]),
         "scion_layout_has_build": (i32, [cp]),
         "scion_ptree_layout": (cp, [vp]),
         "scion_ptree_nbuffers": (i32, [vp]),
@@ -289,6 +290,17 @@ def compile_layout_text(source: str):
     pj, pc = C.c_void_p(), C.c_void_p()
     _check(lib().scion_compile_layout_text(source.encode(), C.byref(pj), C.byref(pc)))
     return json.loads(_take_string(pj)), _take_string(pc)
+
+
+def register_layout(name: str, source: str, work_dir: Optional[str] = None) -> str:
+    """Open-world layouts: compile `source` (.scion text with a layout and its build block) at run time — front end,
+    emit_cuda, nvcc, g++ — and register it under `name`; returns the build log.  About a minute; needs nvcc."""
+    log = C.c_void_p()
+    rc = lib().scion_layout_register(name.encode(), source.encode(), work_dir.encode() if work_dir else None, C.byref(log))
+    text = _take_string(log) if log.value else ""
+    if rc != 0:
+        _check(rc)
+    return text
 
 
 # --------------------------------------------------------------------------------------- scene tools

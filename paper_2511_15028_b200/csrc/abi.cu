@@ -198,10 +198,12 @@ static void info_of(const scion::LayoutEntry& e, scion_layout_info* out) {
   out->has_cpq = e.has_cpq ? 1 : 0;
 }
 int scion_layout_count(void) {
-  SCION_TRY(return (int)scion::layout_registry().size();)
+  SCION_TRY(return (int)scion::layout_registry().size() + scion::dyn_layout_count();)
 }
 int scion_layout_info_at(int index, scion_layout_info* out) {
-  SCION_TRY(auto& r = scion::layout_registry(); if (index < 0 || index >= (int)r.size() || !out) return fail(SCION_ERR_ARG, "layout index out of range"); info_of(r[(size_t)index], out); return SCION_OK;)
+  SCION_TRY(auto& r = scion::layout_registry(); if (!out || index < 0) return fail(SCION_ERR_ARG, "layout index out of range");
+            if (index < (int)r.size()) { info_of(r[(size_t)index], out); return SCION_OK; }
+            const scion::LayoutEntry* e = scion::dyn_layout_at(index - (int)r.size()); if (!e) return fail(SCION_ERR_ARG, "layout index out of range"); info_of(*e, out); return SCION_OK;)
 }
 int scion_layout_find(const char* name, scion_layout_info* out) {
   SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + (name ? name : "") + "'"); if (out) info_of(*e, out); return SCION_OK;)
@@ -222,6 +224,21 @@ int scion_compile_layout_text(const char* src, char** out_plan_json, char** out_
   if (!src) return fail(SCION_ERR_ARG, "null source");
   SCION_TRY(scion::lc::Program prog = scion::lc::parse_program({std::string(src)}); scion::lc::Plan plan = scion::lc::plan_layout(prog, "user-layout");
             if (out_plan_json) *out_plan_json = dup_string(plan.to_json()); if (out_cuda) *out_cuda = dup_string(scion::lc::emit_cuda(plan)); return SCION_OK;)
+}
+
+int scion_layout_register(const char* name, const char* src, const char* work_dir, char** out_log) {
+  if (!name || !src) return fail(SCION_ERR_ARG, "null argument");
+  std::string log;
+  int rc = SCION_OK;
+  try {
+    scion::register_layout_plugin(name, src, work_dir ? work_dir : "", log);
+  } catch (const scion::lc::LayoutError& e) {
+    rc = fail(SCION_ERR_LAYOUT, e.what());
+  } catch (const std::exception& e) {
+    rc = fail(SCION_ERR_BUILD, e.what());
+  }
+  if (out_log) *out_log = dup_string(log);
+  return rc;
 }
 
 // ------------------------------------------------------------------ scene tools

@@ -46,10 +46,16 @@ const std::vector<LayoutEntry>& layout_registry() {
   }();
   return reg;
 }
+const LayoutEntry* dyn_find_layout(const std::string& name);  // host/plugin.cpp: layouts registered at run time
 const LayoutEntry* find_layout(const std::string& name) {
   for (auto& e : layout_registry())
     if (e.name == name) return &e;
-  return nullptr;
+  return dyn_find_layout(name);
+}
+static bool is_builtin(const LayoutEntry& layout) {
+  for (auto& e : layout_registry())
+    if (&e == &layout) return true;
+  return false;
 }
 
 namespace {
@@ -286,6 +292,10 @@ void init_ptree(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& ou
 }  // namespace
 
 void encode_tree(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& out) {
+  if (!is_builtin(layout)) {  // a layout registered at run time: its own build block is its only encoder
+    encode_tree_generated(t, layout, out);
+    return;
+  }
   init_ptree(t, layout, out);
   Writer w(out, *layout.plan, false);
   EncodeJob job;

@@ -36,6 +36,10 @@ struct LayoutEntry {
 // registry of every layout compiled into the library (parsed + planned lazily, once)
 const std::vector<LayoutEntry>& layout_registry();
 const LayoutEntry* find_layout(const std::string& name);
+// layouts compiled and registered at run time (host/plugin.cpp)
+int dyn_layout_count();
+const LayoutEntry* dyn_layout_at(int i);
+void register_layout_plugin(const std::string& name, const std::string& source, const std::string& work_dir, std::string& log);
 
 // build_physical: throws std::runtime_error (builder hard fault) on capacity violations
 void encode_tree(const scion_ltree& t, const LayoutEntry& layout, scion_ptree& out);
