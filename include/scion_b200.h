@@ -165,8 +165,12 @@ int scion_compile_layout_text(const char* scion_source, char** out_plan_json, ch
  * scion_ptree_from_buffers, scion_closest_hit / _point, scion_collision_detection accept the name like a built-in's.
  * Needs nvcc (SCION_NVCC, default /usr/local/cuda/bin/nvcc) and the library's device sources (SCION_B200_SRC, default
  * csrc/ next to the library) at run time; takes about a minute.  work_dir: where the sources and the plugin are kept
- * (null: a fresh directory under $TMPDIR).  *out_log (nullable, scion_free_string) receives the build log. */
+ * (null: a fresh directory under $TMPDIR).  *out_log (nullable, scion_free) receives the build log. */
 int scion_layout_register(const char* name, const char* scion_text, const char* work_dir, char** out_log);
+/* layouts registered at run time, in registration order (scion_layout_count / _info_at enumerate the built-in registry,
+ * i.e. the corpus of corpus_layouts(); scion_layout_find resolves both) */
+int scion_layout_registered_count(void);
+int scion_layout_registered_at(int index, scion_layout_info* out);
 void scion_free(void* p);
 
 /* ------------------------------------------------------------------------- */

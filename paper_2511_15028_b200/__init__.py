@@ -103,6 +103,8 @@ def lib() -> C.CDLL:
         "scion_kernel_launches": (u64, []),
         "scion_layout_count": (i32, []),
         "scion_layout_info_at": (i32, [i32, P(LayoutInfo)]),
+        "scion_layout_registered_count": (i32, []),
+        "scion_layout_registered_at": (i32, [i32, P(LayoutInfo)]),
         "scion_layout_find": (i32, [cp, P(LayoutInfo)]),
         "scion_layout_plan_json": (i32, [cp, P(vp)]),
         "scion_layout_emit_cuda": (i32, [cp, P(vp)]),
@@ -252,8 +254,19 @@ def layouts():
     return out
 
 
+def registered_layouts():
+    """layouts compiled and registered at run time (register_layout), in registration order"""
+    out = []
+    for i in range(lib().scion_layout_registered_count()):
+        info = LayoutInfo()
+        _check(lib().scion_layout_registered_at(i, C.byref(info)))
+        out.append(dict(name=info.name.decode(), family=info.family, arity=info.arity, node_stride=info.node_stride, node_align=info.node_align,
+                        n_segments=info.n_segments, ref_bits=info.ref_bits, max_leaf=info.max_leaf, has_cpq=bool(info.has_cpq)))
+    return out
+
+
 def layout_info(name: str) -> dict:
-    for l in layouts():
+    for l in layouts() + registered_layouts():
         if l["name"] == name:
             return l
     raise ScionError(ERR_ARG, f"unknown layout '{name}'")

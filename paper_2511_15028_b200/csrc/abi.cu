@@ -198,12 +198,14 @@ static void info_of(const scion::LayoutEntry& e, scion_layout_info* out) {
   out->has_cpq = e.has_cpq ? 1 : 0;
 }
 int scion_layout_count(void) {
-  SCION_TRY(return (int)scion::layout_registry().size() + scion::dyn_layout_count();)
+  SCION_TRY(return (int)scion::layout_registry().size();)
 }
 int scion_layout_info_at(int index, scion_layout_info* out) {
-  SCION_TRY(auto& r = scion::layout_registry(); if (!out || index < 0) return fail(SCION_ERR_ARG, "layout index out of range");
-            if (index < (int)r.size()) { info_of(r[(size_t)index], out); return SCION_OK; }
-            const scion::LayoutEntry* e = scion::dyn_layout_at(index - (int)r.size()); if (!e) return fail(SCION_ERR_ARG, "layout index out of range"); info_of(*e, out); return SCION_OK;)
+  SCION_TRY(auto& r = scion::layout_registry(); if (index < 0 || index >= (int)r.size() || !out) return fail(SCION_ERR_ARG, "layout index out of range"); info_of(r[(size_t)index], out); return SCION_OK;)
+}
+int scion_layout_registered_count(void) { return scion::dyn_layout_count(); }
+int scion_layout_registered_at(int index, scion_layout_info* out) {
+  SCION_TRY(const scion::LayoutEntry* e = scion::dyn_layout_at(index); if (!e || !out) return fail(SCION_ERR_ARG, "layout index out of range"); info_of(*e, out); return SCION_OK;)
 }
 int scion_layout_find(const char* name, scion_layout_info* out) {
   SCION_TRY(const scion::LayoutEntry* e = name ? scion::find_layout(name) : nullptr; if (!e) return fail(SCION_ERR_ARG, std::string("unknown layout '") + (name ? name : "") + "'"); if (out) info_of(*e, out); return SCION_OK;)

@@ -85,16 +85,16 @@ def user_layout(built):
 
 
 def test_register_compiles_and_lists_the_layout(built, user_layout):
-    names = [l["name"] for l in built.layouts()]
-    assert NAME in names and "pbrt-q16" in names
-    info = [l for l in built.layouts() if l["name"] == NAME][0]
+    assert NAME in [l["name"] for l in built.registered_layouts()]
+    assert NAME not in [l["name"] for l in built.layouts()]  # the built-in registry (= the corpus) is unchanged
+    info = built.layout_info(NAME)
     assert info["node_stride"] == 16 and info["family"] == 0
     assert "nvcc" in _state["log"]
     with pytest.raises(Exception):  # a name can be registered once
         built.register_layout(NAME, USER_LAYOUT)
     with pytest.raises(Exception):  # ill-formed layouts are rejected by the front end, nothing is compiled
         built.register_layout("user-broken", USER_LAYOUT.replace("c_offset: u28;", ""))
-    assert "user-broken" not in [l["name"] for l in built.layouts()]
+    assert "user-broken" not in [l["name"] for l in built.registered_layouts()]
 
 
 def test_user_layout_is_encoded_through_its_own_build_block(built, user_layout):
