@@ -9,6 +9,9 @@
 #ifndef SCION_TRI_LDG32
 #define SCION_TRI_LDG32 0
 #endif
+#ifndef SCION_TRI_LDG256  /* 1: a triangle is fetched by two 256-bit loads (its two 32-byte sectors) instead of three 128-bit ones */
+#define SCION_TRI_LDG256 0
+#endif
 
 namespace scion {
 
@@ -210,6 +213,33 @@ SCION_DEV void load_triangle36(const uint8_t* prims, uint64_t index, float (&v)[
   const uint32_t* q = reinterpret_cast<const uint32_t*>(prims + index * 36ull);
 #pragma unroll
   for (int j = 0; j < 9; j++) v[j] = u2f(__ldg(q + j));
+#elif defined(__CUDA_ARCH__) && SCION_TRI_LDG256
+  // 36 bytes at a 4-byte aligned address never span more than two 32-byte sectors: two 256-bit loads (one L1 wavefront
+  // per lane each) instead of three 128-bit ones, word re-alignment by a three-level select
+  const uint64_t addr = (uint64_t)prims + index * 36ull;
+  const uint8_t* q = reinterpret_cast<const uint8_t*>(addr & ~31ull);
+  const uint32_t s = (uint32_t)(addr >> 2) & 7u;
+  uint32_t w[16];
+#if SCION_CACHE_HINTS >= 3
+  const uint64_t pol = l2_policy_stream();
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "l"(q), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]) : "l"(q + 32), "l"(pol));
+#else
+  ld256(q, w);
+  ld256(q + 32, w + 8);
+#endif
+  const bool s1 = (s & 1u) != 0u, s2 = (s & 2u) != 0u, s4 = (s & 4u) != 0u;
+  uint32_t x[12];  // words s4 ? [4, 16) : [0, 12)
+#pragma unroll
+  for (int j = 0; j < 12; j++) x[j] = s4 ? w[j + 4] : w[j];
+#pragma unroll
+  for (int j = 0; j < 9; j++) {
+    const uint32_t lo = s1 ? x[j + 1] : x[j];
+    const uint32_t hi = s1 ? x[j + 3] : x[j + 2];
+    v[j] = u2f(s2 ? hi : lo);
+  }
 #elif defined(__CUDA_ARCH__)
   const uint64_t addr = (uint64_t)prims + index * 36ull;
   const uint4* q = reinterpret_cast<const uint4*>(addr & ~15ull);

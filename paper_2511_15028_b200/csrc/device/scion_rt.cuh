@@ -36,7 +36,11 @@
 #define SCION_CACHE_HINTS 4
 #endif
 #ifndef SCION_LDG_COVER
-#define SCION_LDG_COVER 1
+// byte-granular strides (identity 41 B, pbrt-post 34 B, shared-slab 29 B): 1 = the covering 16-byte quads (3-4 LDG.128 per
+// record), 2 = the covering 32-byte sectors (2-3 LDG.256: one L1 wavefront per lane each; identity is L1-tag-bound, l1tex
+// 99 % in profiles/r2_ncu_c5_identity.txt).  C5 probe: identity 1225 -> 1273 (+3.9 %), pbrt-post 1436 -> 1448 (+0.8 %);
+// bit-exact (profiles/r2_ldg256_probe.txt).
+#define SCION_LDG_COVER 2
 #endif
 #ifndef SCION_I2F_MAGIC
 #define SCION_I2F_MAGIC 0
@@ -475,6 +479,37 @@ SCION_HOSTDEV void load_record(const uint8_t* p, Words<(BYTES + 3) / 4>& r) {
   } else if constexpr (ALIGN % 4 == 0 && BYTES % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < NW; i++) r.w[i] = ld32(p + 4 * i);
+  } else if constexpr (SCION_LDG_COVER == 2 && BYTES > 16 && BYTES <= 64) {
+    // byte-granular stride, 256-bit variant: the 32-byte aligned sectors that cover the record (2, sometimes 3, loads of
+    // one L1 wavefront per lane each, where the 16-byte quads below take 3-4), word re-alignment by a three-level select,
+    // byte re-alignment by funnel shifts.  The last sector is only read when the record's bytes reach into it, so the read
+    // never goes more than 31 bytes past the record (buffers carry 32 bytes of slack).
+    const uint64_t a = (uint64_t)p;
+    const uint8_t* q = (const uint8_t*)(a & ~31ull);
+    const uint32_t wsh = (uint32_t)(a >> 2) & 7u;
+    const uint32_t bsh = (uint32_t)(a & 3ull) * 8u;
+    constexpr int NR = NW + 1;           // words needed before the funnel shift
+    constexpr int K = (NR + 7 + 7) / 8;  // sectors covering words [wsh, wsh + NR)
+    uint32_t w[8 * K + 8];
+#pragma unroll
+    for (int k = 0; k < K - 1; k++) ld256(q + 32 * k, w + 8 * k);
+#pragma unroll
+    for (int i = 8 * (K - 1); i < 8 * K + 8; i++) w[i] = 0u;
+    // the last sector is only read when the record's bytes (not the extra funnel word) reach into it
+    if ((uint32_t)(a & 31ull) + (uint32_t)BYTES > 32u * (uint32_t)(K - 1)) ld256(q + 32 * (K - 1), w + 8 * (K - 1));
+    const bool s1 = (wsh & 1u) != 0u, s2 = (wsh & 2u) != 0u, s4 = (wsh & 4u) != 0u;
+    uint32_t x[NR + 3];
+#pragma unroll
+    for (int i = 0; i < NR + 3; i++) x[i] = s4 ? w[i + 4] : w[i];
+    uint32_t raw[NR];
+#pragma unroll
+    for (int i = 0; i < NR; i++) {
+      const uint32_t lo = s1 ? x[i + 1] : x[i];
+      const uint32_t hi = s1 ? x[i + 3] : x[i + 2];
+      raw[i] = s2 ? hi : lo;
+    }
+#pragma unroll
+    for (int i = 0; i < NW; i++) r.w[i] = funnel_r(raw[i], raw[i + 1], bsh);
   } else if constexpr (SCION_LDG_COVER && BYTES > 16) {
     // byte-granular stride (identity 41 B, pbrt-post 34 B, shared-slab 29 B): the 16-byte-aligned quads that
     // cover the record (4 instead of 12 loads for identity), word re-alignment by a two-level select, byte
