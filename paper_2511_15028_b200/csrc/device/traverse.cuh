@@ -158,17 +158,11 @@ SCION_DEV RayCtx load_ray(const scion_ray* rays, uint64_t q) {
 
 // bounds test of one binary / DOP node against the ray.  Loads the cold segment only when the
 // reference semantics would evaluate it (dop.scion:20-21 `if I {...}`).
-// SCION_COLD_EAGER: fetch the cold segment together with the hot one instead of after the hot test.  The loads are pure
-// (any node index is a valid address in every segment), so only the timing changes: one dependent memory round trip
-// per passing node instead of two.  The counters still count a cold load only where the reference evaluates it.
-#ifndef SCION_COLD_EAGER
-#define SCION_COLD_EAGER 0
-#endif
 template <class L, class TallyT>
 SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L::Ref& ref, typename L::Node& n, float& t_near, TallyT& tally) {
   float t_far;
   // kBoundsCold: the box itself lies (partly) behind `---` (pbrt-soaos-align16), so the cold segment is part of every visit
-  constexpr bool kEager = L::kHasCold && (SCION_COLD_EAGER != 0 || L::kBoundsCold);
+  constexpr bool kEager = L::kHasCold && L::kBoundsCold;
   if constexpr (kEager) L::decode_cold(T, ref, n);
   if constexpr (L::kFamily == SCION_FAMILY_DOP14) {
     bool some = ray_aabb(ray, n.lo1, n.hi1, t_near, t_far);
@@ -191,27 +185,12 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
   }
 }
 
-enum : int { kFetch = 0, kNode = 1, kPrim = 2, kDone = 4 };  // lane modes (3 = kPop of the closest-point kernel)
-// SCION_DEFER_RETIRE: a lane whose stack runs empty only marks itself kDone; the result stores (~23 instructions that ran
-// for ONE lane at a time: 3.4 % of all warp instructions in profiles/r1_ncu_v11_c5_q16.txt) happen at the next refill,
-// for all finished lanes of the warp together.
-#ifndef SCION_DEFER_RETIRE
-#define SCION_DEFER_RETIRE 0
-#endif
+enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes (3 = kPop of the closest-point kernel)
 #ifndef SCION_PREFETCH
 #define SCION_PREFETCH 1
 #endif
 #ifndef SCION_CPQ_GUIDED  /* 1: closest_point uses the guided (128 -> 32 query) work-fetch chunks of the closest-hit kernels */
 #define SCION_CPQ_GUIDED 0
-#endif
-#ifndef SCION_TOS  /* 1: the newest stack entry of the binary closest-hit kernel lives in a register (see chrt2_kernel) */
-#define SCION_TOS 0
-#endif
-#ifndef SCION_PF_NEXT
-#define SCION_PF_NEXT 0
-#endif
-#ifndef SCION_PF_MIN
-#define SCION_PF_MIN 0
 #endif
 #ifndef SCION_INNER
 #define SCION_INNER 4
@@ -221,16 +200,6 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2, kDone = 4 };  // lane modes (3 = 
 #endif
 #ifndef SCION_PF8
 #define SCION_PF8 0
-#endif
-// SCION_HOT_L1 = N > 0 (binary kernel, single-vector-load layouts with a 32-bit index reference): records of subtrees with
-// fewer than N nodes are fetched with L1::no_allocate, so that the top of the tree (a few thousand records) stays in L1
-// instead of being evicted by the cold bottom levels (L1 hit rate 15.8 %).  The "hot" flag travels in bit 31 of the
-// reference (children inherit it from the size of their parent's left subtree, c_offset).
-#ifndef SCION_HOT_L1
-#define SCION_HOT_L1 0
-#endif
-#ifndef SCION_CPQ_PFY
-#define SCION_CPQ_PFY 0
 #endif
 #ifndef SCION_CPQ_BOTH
 #define SCION_CPQ_BOTH -1  // -1: per layout (records fetched by ONE vector load), 0: never, 1: always
@@ -462,32 +431,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
     mode = kFetch;
   };
 
-#if SCION_TOS
-  // SCION_TOS (north_star: "a short traversal stack in registers that spills to shared memory"): the newest pending
-  // reference lives in the register `tos`; memory (shared window, then local) holds the entries below it, i.e. slots
-  // [0, depth - 1).  A pop hands over `tos` at once and refills it with a load nobody waits for; a push spills the old
-  // `tos`.  `top` keeps its meaning (address of slot `depth`).
-  Ref tos = L::root(T);
-  auto mem_store = [&](uint32_t idx, const Ref& r) {  // slot idx of the memory part
-    if (idx < (uint32_t)LS::kSmem) LS::store(window + threadIdx.x * 4u + idx * LS::kSlot, r);
-    else deep[idx - (uint32_t)LS::kSmem] = r;
-  };
-  auto mem_load = [&](uint32_t idx, Ref& r) {
-    if (idx < (uint32_t)LS::kSmem) LS::load(window + threadIdx.x * 4u + idx * LS::kSlot, r);
-    else r = deep[idx - (uint32_t)LS::kSmem];
-  };
-  auto pop_or_retire = [&]() {
-    const uint32_t depth = (top - window) / LS::kSlot;
-    if (depth == 0u) {
-      retire(SCION_Q_OK);
-      return;
-    }
-    cur = tos;
-    top -= LS::kSlot;
-    if (depth >= 2u) mem_load(depth - 2u, tos);
-    mode = kNode;
-  };
-#else
   // next pending reference, or retire the query when the stack is empty (used after a leaf phase
   // and on the rare paths of step())
   auto pop_or_retire = [&]() {
@@ -497,43 +440,21 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       LS::load(top, cur);
       mode = kNode;
     } else if (rel < LS::kSlot) {  // empty: the query is done
-#if SCION_DEFER_RETIRE
-      mode = kDone;
-#else
       retire(SCION_Q_OK);
-#endif
     } else {
       top -= LS::kSlot;
       cur = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
       mode = kNode;
     }
   };
-#endif
 
-  constexpr bool kHot = SCION_HOT_L1 > 0 && TL == 0 && L::kCanFetch && !L::kHasCold && std::is_same<Ref, uint32_t>::value;
   const Ref root = [&]() -> Ref {
     if constexpr (TL > 0) return tl_on ? (Ref)kTreeletBit : L::root(T);  // slot 0 of the treelet is the root
     else return L::root(T);
   }();
-  constexpr uint32_t kHotBit = 0x80000000u;
   auto step = [&]() {
     typename L::Node node;
-    uint32_t child_flag = 0u;
-    auto tagged = [&](const Ref& r) -> Ref {  // the child reference with the hot flag of this node's children
-      if constexpr (kHot) return (Ref)(r | (Ref)child_flag);
-      else return r;
-    };
-    if constexpr (kHot) {
-      const Ref idx = (Ref)((uint32_t)cur & ~kHotBit);
-      typename L::Fetched w;
-      if ((uint32_t)cur & kHotBit) L::template fetch<false>(T, idx, w);
-      else L::template fetch<true>(T, idx, w);
-      L::decode_fetched(T, idx, w, node);
-      if (node.variant != L::kLeaf) {
-        child_flag = (uint32_t)(node.right - idx) >= (uint32_t)SCION_HOT_L1 ? kHotBit : 0u;
-      }
-      cur = idx;
-    } else if constexpr (TL > 0) {
+    if constexpr (TL > 0) {
       typename L::Fetched w;
       const bool in_t = ((uint32_t)cur & kTreeletBit) != 0u;
       const uint32_t slot = (uint32_t)cur & ~kTreeletBit;
@@ -559,11 +480,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
     } else {
       L::decode(T, cur, node);
     }
-#if SCION_PF_NEXT == 1
-    if constexpr (std::is_integral<Ref>::value) L::template prefetch<1>(T, (Ref)(cur + 1));
-#elif SCION_PF_NEXT > 1  // L2 prefetch SCION_PF_NEXT records ahead in the (preorder) array
-    if constexpr (std::is_integral<Ref>::value) L::template prefetch<2>(T, (Ref)(cur + SCION_PF_NEXT));
-#endif
     tally.visit();
     float t_near;
     const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
@@ -574,13 +490,7 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
     // the common push (depth < kSmem) and pop (1 <= depth <= kSmem) are straight-line predicated
     // code; everything else (empty stack = retire, entries beyond the shared-memory window,
     // overflow) is one rarely taken branch
-#if SCION_TOS
-    // memory holds slots [0, depth - 1): a push spills `tos` into slot depth - 1, a pop refills it from slot depth - 2 — both
-    // inside the shared window as long as depth <= kSmem
-    const bool fast = p_push ? rel < LS::kSmemBytes + LS::kSlot : rel - LS::kSlot < LS::kSmemBytes + LS::kSlot;
-#else
     const bool fast = p_push ? rel < LS::kSmemBytes : rel - LS::kSlot < LS::kSmemBytes;
-#endif
     if (COUNT && p_push) tally.stack(rel / LS::kSlot + 2u);  // reference discipline: pop self, push right, push left
     if (!(fast || p_prim)) {
       if (p_push) {
@@ -588,14 +498,9 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
         if (depth + 2u > (uint32_t)SCION_STACK_DEPTH) {
           retire(SCION_Q_STACK_OVERFLOW);
         } else {
-#if SCION_TOS
-          mem_store(depth - 1u, tos);  // depth > kSmem >= 1 here
-          tos = tagged(node.right);
-#else
-          deep[depth - (uint32_t)LS::kSmem] = tagged(node.right);
-#endif
+          deep[depth - (uint32_t)LS::kSmem] = node.right;
           top += LS::kSlot;
-          cur = tagged(node.left);
+          cur = node.left;
         }
       } else {
         pop_or_retire();
@@ -607,34 +512,20 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       prefetch_triangles<L>(T, (uint32_t)node.data.begin, (uint32_t)node.data.end);
       mode = kPrim;
     } else if (p_push) {
-#if SCION_TOS
-      if (rel >= LS::kSlot) LS::store(top - LS::kSlot, tos);  // spill the previous newest entry (none when the stack was empty)
-      tos = tagged(node.right);
-#else
-      LS::store(top, tagged(node.right));
-#endif
+      LS::store(top, node.right);
       if constexpr (kPrefetch) {
-        // L2-prefetch the pushed child, but only when it is far: a right sibling a few records away shares
-        // its lines with what this lane just fetched, and every prefetch costs an L1 tag lookup per lane
+        // L2-prefetch the pushed child (+4 %; gating it by distance loses 3-7 %: even a sibling four records away profits)
         if constexpr (TL > 0) {
           if (((uint32_t)node.right & kTreeletBit) == 0u) L::prefetch(T, node.right);  // staged children need no prefetch
-        } else if constexpr (std::is_integral<Ref>::value && SCION_PF_MIN > 0) {
-          if ((uint64_t)(node.right - cur) > (uint64_t)SCION_PF_MIN) L::prefetch(T, node.right);
         } else {
           L::prefetch(T, node.right);
         }
       }
       top += LS::kSlot;
-      cur = tagged(node.left);
+      cur = node.left;
     } else {
-#if SCION_TOS
-      cur = tos;  // no load between the pop and the next record's address
-      top -= LS::kSlot;
-      if (top - window >= LS::kSlot) LS::load(top - LS::kSlot, tos);  // refill: needed at the next pop / spill only
-#else
       top -= LS::kSlot;
       LS::load(top, cur);
-#endif
     }
   };
 
@@ -645,15 +536,8 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       if (mode == kNode) step();
     }
     // ---- FETCH: refill idle lanes
-#if SCION_DEFER_RETIRE
-    const unsigned idle = __ballot_sync(kFullMask, mode == kFetch || mode == kDone);
-#else
     const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
-#endif
     if (idle && (__popc(idle) >= kRefillMin || work.exhausted)) {
-#if SCION_DEFER_RETIRE
-      if (mode == kDone) retire(SCION_Q_OK);
-#endif
       uint64_t nq;
       if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
         ray = load_ray(rays, nq);
@@ -664,7 +548,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
         tally.reset();
         top = window + threadIdx.x * 4u;
         cur = root;
-        if constexpr (kHot) cur = (Ref)((uint32_t)cur | kHotBit);
         mode = kNode;
       }
       if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
@@ -1190,22 +1073,10 @@ SCION_DEV uint32_t coop_points2(const TreeView& T, bool own, const f32x3& p, uin
 #ifndef SCION_MINBC
 #define SCION_MINBC 6
 #endif
-// SCION_CPQ_STORE_D: a pushed far child carries the distance its parent's peek computed (8-byte stack entries for 32-bit
-// references).  The reference decodes a popped node, computes the same (pure) distance and skips the node unless it is
-// < best[0]; with the distance on the stack that cull needs no record: culled entries cost one LDS.64 instead of a step
-// with a dependent load.  The instrumented build still counts the decode the reference performs.
-#ifndef SCION_CPQ_STORE_D
-#define SCION_CPQ_STORE_D 0
-#endif
 #ifndef SCION_STACK_SMEM_C  /* shared-memory stack window of one closest-point CTA */
 #define SCION_STACK_SMEM_C SCION_STACK_SMEM
 #endif
 constexpr int kStackSmemBytesPerBlockC = SCION_STACK_SMEM_C;
-template <class Ref>
-struct CpqEntryD {
-  Ref ref;
-  float d;
-};
 #ifndef SCION_PRIM_MINC
 #define SCION_PRIM_MINC 6
 #endif
@@ -1229,8 +1100,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
                                                              scion_counters* __restrict__ counters, unsigned long long* __restrict__ next, const int tune) {
   using Ref = typename L::Ref;
   using Node = typename L::Node;
-  constexpr bool kStoreD = SCION_CPQ_STORE_D != 0 && std::is_integral<Ref>::value;
-  using Entry = typename std::conditional<kStoreD, CpqEntryD<Ref>, Ref>::type;
+  using Entry = Ref;
   using LS = LaneStack<Entry, kStackSmemBytesPerBlockC>;
   enum : int { kPop = 3 };  // stepping lanes: kNode (record + distance of `node` are valid) or kPop (take the next pending reference first)
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1238,10 +1108,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
   __shared__ float4 best_pt[kBlockThreads];
   __shared__ unsigned long long stash_q[kBlockThreads];
   Entry deep[LS::kDeep];
-  auto make_entry = [](const Ref& r, float dist) -> Entry {
-    if constexpr (kStoreD) return Entry{r, dist};
-    else return r;
-  };
+  auto make_entry = [](const Ref& r, float) -> Entry { return r; };
   uint32_t window = (uint32_t)__cvta_generic_to_shared(smem_raw);
   asm volatile("" : "+r"(window));
   uint32_t top = window + threadIdx.x * 4u;
@@ -1300,38 +1167,15 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
     }
     const uint32_t rel = top - window;
     if (!go) {  // pop the next pending reference, or retire
-      if constexpr (kStoreD) {
-        for (;;) {
-          const uint32_t r2 = top - window;
-          Entry e;
-          if (r2 - LS::kSlot < LS::kSmemBytes) {
-            top -= LS::kSlot;
-            LS::load(top, e);
-          } else if (r2 < LS::kSlot) {
-            retire(SCION_Q_OK);
-            return;
-          } else {
-            top -= LS::kSlot;
-            e = deep[r2 / LS::kSlot - 1u - (uint32_t)LS::kSmem];
-          }
-          if (e.d < best_d) {
-            rx = e.ref;
-            break;
-          }
-          tally.visit();  // culled without its record: the reference decodes the node, then skips it (cpq.scion:5)
-          if (L::kHasCold) tally.cold();
-        }
+      if (rel - LS::kSlot < LS::kSmemBytes) {
+        top -= LS::kSlot;
+        LS::load(top, rx);
+      } else if (rel < LS::kSlot) {
+        retire(SCION_Q_OK);
+        return;
       } else {
-        if (rel - LS::kSlot < LS::kSmemBytes) {
-          top -= LS::kSlot;
-          LS::load(top, rx);
-        } else if (rel < LS::kSlot) {
-          retire(SCION_Q_OK);
-          return;
-        } else {
-          top -= LS::kSlot;
-          rx = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
-        }
+        top -= LS::kSlot;
+        rx = deep[rel / LS::kSlot - 1u - (uint32_t)LS::kSmem];
       }
     } else {
       const uint32_t depth = rel / LS::kSlot;
@@ -1341,10 +1185,6 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINBC) cpq2_kernel(const 
         return;
       }
     }
-#if SCION_CPQ_PFY > 0  // start the (far) right child's fetch before the left child's record is awaited: the compiler keeps
-    // the Y load inside the `go` branch, behind X's load + decode (profiles/r1_ncu_v11_c4_q16.txt: 24 % of the stall samples)
-    if (go) L::template prefetch<SCION_CPQ_PFY>(T, ry);
-#endif
     // Both decode slots unconditional where the record is ONE vector load (pbrt, pbrt-align16, pbrt-q16, sg-eq-align16):
     // a popping lane decodes its X record twice (same address, no extra sector).  The Y instructions are issued for the
     // warp anyway as soon as one lane descends, and without the `go` branch around them the Y load is in flight together
