@@ -17,6 +17,7 @@ Exit codes as the reference CLI: 0 pass, 1 diagnostics/mismatch, 2 usage.  `veri
 oracle) lives in tests/verify_cli.py because only test infrastructure may touch oracle/.
 """
 import argparse
+import os
 import json
 import sys
 
@@ -277,6 +278,9 @@ def scene_is_terrain(spec):
 
 def main(argv=None):
     ap = argparse.ArgumentParser(prog="paper_2511_15028_b200.harness")
+    ap.add_argument("--layout-file", action="append", default=[], metavar="FILE.scion",
+                    help="compile and register this layout (layout + build block) at run time under the name of the file "
+                         "(my_layout.scion -> my-layout) before the command runs; needs nvcc; repeatable")
     sub = ap.add_subparsers(dest="cmd")
     sub.add_parser("check")
     p = sub.add_parser("footprint")
@@ -325,6 +329,15 @@ def main(argv=None):
         ap.print_usage(sys.stderr)
         return 2
     try:
+        for f in a.layout_file:  # open-world layouts: front end -> emit_cuda -> nvcc -> plugin (scion_layout_register)
+            name = os.path.splitext(os.path.basename(f))[0].replace("_", "-")
+            try:
+                text = open(f).read()
+            except OSError as e:
+                print(f"error: {e}", file=sys.stderr)
+                return 2
+            sb.register_layout(name, text)
+            print(f"registered layout '{name}' from {f}", file=sys.stderr)
         return {"check": cmd_check, "footprint": cmd_footprint, "emit-cuda": cmd_emit, "emit-c": cmd_emit, "bench": cmd_bench, "compile": cmd_compile,
                 "build-tree": cmd_build_tree, "build": cmd_build, "run": cmd_run}[a.cmd](a)
     except sb.ScionError as e:

@@ -143,3 +143,87 @@ def test_user_layout_traverses_like_its_twin(built, user_layout):
         assert torch.equal(a, b)
     got = out[NAME][0].cpu().numpy().view(sb.HIT_DTYPE)
     assert (got["prim"] != sb.MISS_PRIM).mean() > 0.3
+
+
+def test_cli_accepts_a_layout_file(built, tmp_path):
+    """`harness --layout-file my.scion <command>`: the file is compiled and registered in that process, the command then
+    takes the layout by name (here: footprint through the layout's own build block)"""
+    import json
+    import subprocess
+    import sys
+    if not os.path.exists(os.environ.get("SCION_NVCC", "/usr/local/cuda/bin/nvcc")):
+        pytest.skip("run-time layout plugins need nvcc")
+    f = tmp_path / "cli_q16_swapped.scion"
+    f.write_text(USER_LAYOUT)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "paper_2511_15028_b200.harness", "--layout-file", str(f), "footprint", "--layout", "cli-q16-swapped", "--scene", "terrain:16"],
+                       capture_output=True, text=True, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rep = json.loads(r.stdout)
+    assert rep["layout"] == "cli-q16-swapped" and rep["node_stride"] == 16 and rep["primitives"] == 512
+    r = subprocess.run([sys.executable, "-m", "paper_2511_15028_b200.harness", "--layout-file", str(tmp_path / "missing.scion"), "check"], capture_output=True, text=True, cwd=root)
+    assert r.returncode == 2
+
+
+def wide_user_layout():
+    """bvh8-q8-ci with the child references in FRONT of the quantisation frame and the code boxes (every stored field at
+    another offset): derived from the shipped file's text so that the arithmetic is the twin's by construction"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_2511_15028_b200", "layouts", "bvh8_q8_ci.scion")).read()
+    a = "    mlo: f32x3;\n    mex: f32x3;\n    child_bounds: qbox3x8;\n    children: u32x8;\n"
+    assert a in src
+    return src.replace(a, "    children: u32x8;\n    mlo: f32x3;\n    mex: f32x3;\n    child_bounds: qbox3x8;\n")
+
+
+WIDE_NAME = "user-wide-q8"
+
+
+@pytest.fixture(scope="session")
+def wide_layout(built):
+    if not os.path.exists(os.environ.get("SCION_NVCC", "/usr/local/cuda/bin/nvcc")):
+        pytest.skip("run-time layout plugins need nvcc")
+    if "wide" not in _state:
+        _state["wide"] = built.register_layout(WIDE_NAME, wide_user_layout())
+    return WIDE_NAME
+
+
+def test_wide_user_layout_records_are_the_twins_rotated(built, wide_layout):
+    lt = built.Scene.terrain(19, 6).build_sah(32, 4).collapse8()
+    mine, ref = lt.encode(WIDE_NAME), lt.encode("bvh8-q8-ci")
+    a = np.frombuffer(bytes([b for b in mine.buffers() if b["name"] == "Interiors"][0]["data"]), np.uint8).reshape(-1, 104)
+    b = np.frombuffer(bytes([b for b in ref.buffers() if b["name"] == "Interiors"][0]["data"]), np.uint8).reshape(-1, 104)
+    assert a.shape == b.shape and a.shape[0] == len(lt.wnodes())
+    assert np.array_equal(a[:, 0:32], b[:, 72:104])   # children
+    assert np.array_equal(a[:, 32:104], b[:, 0:72])   # mlo, mex, child_bounds
+    assert mine.root() == ref.root()
+
+
+@pytest.mark.gpu
+def test_wide_user_layout_traverses_like_its_twin(built, wide_layout):
+    """every 8-wide kernel — register-record (variant 1), lane-cooperative (variant 5; staged: the 104-byte record is not
+    16-byte aligned) — instantiated for the run-time layout by the plugin build"""
+    import torch
+    sb = built
+    scene = sb.Scene.sphere(40, 3)
+    lt = scene.build_sah(32, 4).collapse8()
+    lo, hi = scene.bounds()
+    cam = sb.default_camera(lo, hi, False, 96, 96)
+    rays = np.concatenate([sb.gen_primary_host(cam, 0, 96 * 96), sb.gen_secondary_host(lt.triangles(), 5, 0, 8192)])
+    n = rays.shape[0]
+    d_rays = torch.from_numpy(rays.view(np.uint8).reshape(-1)).to("cuda:0")
+    out = {}
+    for layout in (WIDE_NAME, "bvh8-q8-ci"):
+        dt = lt.encode(layout).upload(0)
+        for v in (1, 5):
+            h = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+            st = torch.full((n,), 7, dtype=torch.int32, device="cuda:0")
+            c = torch.zeros(n * 16, dtype=torch.uint8, device="cuda:0")
+            dt.closest_hit(d_rays.data_ptr(), n, h.data_ptr(), st.data_ptr(), c.data_ptr(), variant=v)
+            torch.cuda.synchronize()
+            out[(layout, v)] = (h, st, c)
+        dt.free()
+    for v in (1, 5):
+        for a, b in zip(out[(WIDE_NAME, v)], out[("bvh8-q8-ci", 1)]):
+            assert torch.equal(a, b), v
+    got = out[(WIDE_NAME, 1)][0].cpu().numpy().view(sb.HIT_DTYPE)
+    assert (got["prim"] != sb.MISS_PRIM).mean() > 0.3
