@@ -2,7 +2,7 @@
 
 Every entry records where its figure comes from, so that bench.py can say in the bench line whether the kernel
 sources changed since the capture:
-  {"bytes": dram__bytes_read.sum + dram__bytes_write.sum of ONE launch, "capture": file, "commit": the commit that
+  {"bytes": dram__bytes_read.sum + dram__bytes_write.sum of ONE launch, "capture": file, "commit": the commit that last wrote the capture,
    added the capture, "kernel_sha": sha1 over csrc/device/* + csrc/gen/*.cuh AT that commit (same rule as
    bench.py kernel_sources_sha()), "kernel": demangled kernel name, "ms": gpu__time_duration of the captured launch}
 Usage: python tools/make_traffic.py [--head FILE ...]   (--head: these captures were taken from the working tree,
@@ -81,8 +81,8 @@ def main():
         if name in heads:
             commit, when = "worktree", 1 << 62
         else:
-            commit = git("log", "--diff-filter=A", "-1", "--format=%h", "--", "profiles/" + name).strip()
-            when = int(git("log", "--diff-filter=A", "-1", "--format=%ct", "--", "profiles/" + name).strip() or 0)
+            commit = git("log", "-1", "--format=%h", "--", "profiles/" + name).strip()
+            when = int(git("log", "-1", "--format=%ct", "--", "profiles/" + name).strip() or 0)
         order.append((when, name, f"c{m.group(1)}:{lay}:1", d, commit))
     cache = {}
     for when, name, key, d, commit in sorted(order):  # the newest capture of a key wins
