@@ -15,11 +15,21 @@
 
 namespace scion {
 
+#ifndef SCION_SEL_MASK
+// 0: near / far plane chosen by FSEL on three predicates re-derived from `neg` in every step (2 LOP3 + 2 ISETP);
+// 1: chosen by a bitwise mux — near = lo ^ ((lo ^ hi) & m), ONE LOP3 per plane, no predicates — on per-axis masks
+//    m = direction[a] < 0 ? ~0 : 0 kept in registers (2 more than `neg`).  Same values bit for bit.
+#define SCION_SEL_MASK 0
+#endif
 struct RayCtx {
   float ox, oy, oz, tmax;
   float dx, dy, dz;
   float rdx, rdy, rdz;  // 1.0 / direction, hoisted (pure, geometry.scion:13)
+#if SCION_SEL_MASK
+  uint32_t mx, my, mz;  // all ones iff direction[a] < 0.0 (-0.0 is not negative)
+#else
   uint32_t neg;         // bit a set iff direction[a] < 0.0 (-0.0 is not negative); one register instead of three flags
+#endif
 };
 
 SCION_DEV RayCtx make_ray(float ox, float oy, float oz, float tmax, float dx, float dy, float dz) {
@@ -27,16 +37,33 @@ SCION_DEV RayCtx make_ray(float ox, float oy, float oz, float tmax, float dx, fl
   r.ox = ox; r.oy = oy; r.oz = oz; r.tmax = tmax;
   r.dx = dx; r.dy = dy; r.dz = dz;
   r.rdx = 1.0f / dx; r.rdy = 1.0f / dy; r.rdz = 1.0f / dz;
+#if SCION_SEL_MASK
+  r.mx = dx < 0.0f ? 0xffffffffu : 0u;
+  r.my = dy < 0.0f ? 0xffffffffu : 0u;
+  r.mz = dz < 0.0f ? 0xffffffffu : 0u;
+#else
   r.neg = (dx < 0.0f ? 1u : 0u) | (dy < 0.0f ? 2u : 0u) | (dz < 0.0f ? 4u : 0u);
+#endif
   return r;
 }
 
 // intersectsp_ray_aabb, geometry.scion:12-22.  Returns `some`; t_near/t_far are the interval.
 SCION_DEV bool ray_aabb(const RayCtx& r, const f32x3& lo, const f32x3& hi, float& t_near, float& t_far) {
+#if SCION_SEL_MASK
+  auto mux = [](float a, float b, uint32_t m) {  // m ? b : a bit by bit: ONE LOP3 (the C++ form becomes three per axis, the common a ^ b first)
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(d) : "r"(f2u(a)), "r"(f2u(b)), "r"(m));
+    return u2f(d);
+  };
+  const float nx = mux(lo.x, hi.x, r.mx), fx = mux(hi.x, lo.x, r.mx);
+  const float ny = mux(lo.y, hi.y, r.my), fy = mux(hi.y, lo.y, r.my);
+  const float nz = mux(lo.z, hi.z, r.mz), fz = mux(hi.z, lo.z, r.mz);
+#else
   const bool sx = (r.neg & 1u) != 0u, sy = (r.neg & 2u) != 0u, sz = (r.neg & 4u) != 0u;
   const float nx = sx ? hi.x : lo.x, fx = sx ? lo.x : hi.x;
   const float ny = sy ? hi.y : lo.y, fy = sy ? lo.y : hi.y;
   const float nz = sz ? hi.z : lo.z, fz = sz ? lo.z : hi.z;
+#endif
   const float t_nx = (nx - r.ox) * r.rdx, t_fx = (fx - r.ox) * r.rdx;
   const float t_ny = (ny - r.oy) * r.rdy, t_fy = (fy - r.oy) * r.rdy;
   const float t_nz = (nz - r.oz) * r.rdz, t_fz = (fz - r.oz) * r.rdz;
