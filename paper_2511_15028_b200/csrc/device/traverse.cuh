@@ -336,6 +336,26 @@ SCION_DEV uint32_t coop_triangles2(const TreeView& T, bool own, float ox, float 
   return tested;
 }
 
+// SCION_LEAF_NOINLINE (experiment): the cooperative leaf phase as an out-of-line function with by-value arguments and
+// results, so that its ~35 live registers (triangle, Moeller-Trumbore temporaries) no longer count towards the register
+// allocation of the node step: the step's state is saved around the CALL only, and the kernel can be bounded to fewer
+// registers / more CTAs per SM (SCION_MINB2) without spilling inside the step.
+#ifndef SCION_LEAF_NOINLINE
+#define SCION_LEAF_NOINLINE 0
+#endif
+struct LeafOut {
+  float best_t;
+  uint32_t best_prim, tested;
+};
+template <class L>
+__device__ __noinline__ LeafOut coop_triangles2_call(const uint8_t* prims, bool own, float ox, float oy, float oz, float tmax, const RayStash* warp_stash, uint32_t prim_i,
+                                                     uint32_t prim_end, float best_t, uint32_t best_prim, CoopScratch2* sc) {
+  TreeView T;
+  T.buf[L::kBuf_primitives] = prims;
+  const uint32_t tested = coop_triangles2<L>(T, own, ox, oy, oz, tmax, warp_stash, prim_i, prim_end, best_t, best_prim, *sc);
+  return LeafOut{best_t, best_prim, tested};
+}
+
 // ------------------------------------------------------------------------------------------
 // closest_hit, binary + DOP-14 families (kernel v6)
 //
@@ -559,8 +579,16 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       uint2 range = make_uint2(0u, 0u);
       if (own) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(range.x), "=r"(range.y) : "r"(my_leaf));
       uint32_t prim_i = range.x;
+#if SCION_LEAF_NOINLINE
+      const LeafOut lo_ = coop_triangles2_call<L>(T.buf[L::kBuf_primitives], own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, range.y, best_t,
+                                                  best_prim, &coop[threadIdx.x >> 5]);
+      best_t = lo_.best_t;
+      best_prim = lo_.best_prim;
+      const uint32_t done = lo_.tested;
+#else
       const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, range.y, best_t,
                                                best_prim, coop[threadIdx.x >> 5]);
+#endif
       if (COUNT) tally.prim_tests += done;
       if (own) pop_or_retire();
     }

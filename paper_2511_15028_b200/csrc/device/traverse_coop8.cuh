@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kBlockThreads, SCION_MINB8C) chrt8c_kernel(con
     const Ref nxt = bcast_ref(ch, gbase + first);
     const uint32_t m = (uint32_t)__popc(mask);
     bool cont = false;
+    __syncwarp();  // the pops of the previous step / leaf phase (reads of the group's stack) are complete before this step's pushes
     if (act) {
       tally.visit();
       if (mask != 0u) {
