@@ -195,6 +195,9 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes (3 = kPop of the
 #ifndef SCION_INNER
 #define SCION_INNER 4
 #endif
+#ifndef SCION_DUMMY_LD
+#define SCION_DUMMY_LD 0
+#endif
 #ifndef SCION_PF_TRI
 #define SCION_PF_TRI 0
 #endif
@@ -500,6 +503,16 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
     } else {
       L::decode(T, cur, node);
     }
+#if SCION_DUMMY_LD  // diagnostic: N extra loads of the record's own first word (an L1 hit on the sector just requested, nobody waits for them)
+    if constexpr (L::kCanStage && std::is_integral<Ref>::value) {
+      const uint8_t* a__ = T.buf[L::kStageBuffer] + (uint64_t)cur * L::kStageStride;
+#pragma unroll
+      for (int i__ = 0; i__ < SCION_DUMMY_LD; i__++) {
+        uint32_t d__;
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(d__) : "l"(a__ + 4 * i__));
+      }
+    }
+#endif
     tally.visit();
     float t_near;
     const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
