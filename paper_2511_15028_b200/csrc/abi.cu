@@ -790,10 +790,20 @@ static int run_query(const scion_dtree* t, bool hit, const void* in, uint64_t n,
     cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, t->device);
     if (maxw > 0 && bytes > (size_t)maxw) bytes = (size_t)maxw;
     attr.accessPolicyWindow.num_bytes = bytes;
-    attr.accessPolicyWindow.hitRatio = 1.0f;
+    // hitRatio: the fraction of the window's lines that may persist; window > carve-out with ratio 1 thrashes the carve-out
+    static const float ratio = [] { const char* e = getenv("SCION_L2_PERSIST_RATIO"); float r = e ? (float)atof(e) : 1.0f; return r > 0.0f && r <= 1.0f ? r : 1.0f; }();
+    attr.accessPolicyWindow.hitRatio = ratio;
     attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cudaStreamSetAttribute(a.stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+    const cudaError_t pe = cudaStreamSetAttribute(a.stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+    static bool told = false;
+    if (!told && getenv("SCION_DEBUG")) {
+      told = true;
+      cudaDeviceProp prop;
+      cudaGetDeviceProperties(&prop, t->device);
+      fprintf(stderr, "[scion] L2 persistence: window %zu B of %zu B, ratio %.2f, carve-out max %d B, max window %d B, rc %d\n", bytes, (size_t)t->header.bytes[1], ratio,
+              prop.persistingL2CacheMaxSize, maxw, (int)pe);
+    }
   }
   {
     const cudaError_t e1 = fn(a);
