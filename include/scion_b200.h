@@ -164,8 +164,9 @@ int scion_compile_layout_text(const char* scion_source, char** out_plan_json, ch
  * the plugin is loaded into the process.  Afterwards scion_encode (through the layout's build block), scion_dtree_upload,
  * scion_ptree_from_buffers, scion_closest_hit / _point, scion_collision_detection accept the name like a built-in's.
  * Needs nvcc (SCION_NVCC, default /usr/local/cuda/bin/nvcc) and the library's device sources (SCION_B200_SRC, default
- * csrc/ next to the library) at run time; takes about a minute.  work_dir: where the sources and the plugin are kept
- * (null: a fresh directory under $TMPDIR).  *out_log (nullable, scion_free) receives the build log. */
+ * csrc/ next to the library) at run time; 10-25 s.  work_dir: where the sources and the plugin are kept (null: a fresh
+ * directory under $TMPDIR); a plugin found there that was compiled from the same text with the same compiler, flags and
+ * library is reused without compiling.  *out_log (nullable, scion_free) receives the build log. */
 int scion_layout_register(const char* name, const char* scion_text, const char* work_dir, char** out_log);
 /* layouts registered at run time, in registration order (scion_layout_count / _info_at enumerate the built-in registry,
  * i.e. the corpus of corpus_layouts(); scion_layout_find resolves both) */

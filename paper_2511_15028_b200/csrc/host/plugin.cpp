@@ -167,13 +167,28 @@ void register_layout_plugin(const std::string& name, const std::string& source, 
                  "; }\nextern \"C\" const void* scion_plugin_kernels() { return &scion::kKernels_" + ident + "; }\nextern \"C\" const void* scion_plugin_builder() { return &scion::kBuilder_" + ident + "; }\n");
   // 3. compile + link: the library's own flags (include paths re-rooted at the work directory and the library's headers)
   const std::string inc = " -I" + work + " -I" + csrc + " -I" + csrc + "/../../include";
-  const std::string so = work + "/libscion_layout_" + ident + ".so";
+  // the plugin is keyed by everything it was compiled from: the emitted header (= layout text + compiler), the two stamped
+  // templates, the flags and the library it links against — a caller that passes the same work_dir again reuses it
+  uint64_t key = 1469598103934665603ull;  // FNV-1a
+  auto mix = [&](const std::string& t) { for (unsigned char c : t) { key ^= c; key *= 1099511628211ull; } };
+  mix(header); mix(read_file(csrc + "/device/inst.cu.in")); mix(read_file(csrc + "/host/build_inst.cpp.in")); mix(kBuildNvccFlags); mix(kBuildCxxFlags); mix(name);
+  {
+    struct stat st;
+    if (::stat(library_path().c_str(), &st) == 0) mix(std::to_string((long long)st.st_size) + ":" + std::to_string((long long)st.st_mtime));
+  }
+  char keyhex[32];
+  snprintf(keyhex, sizeof keyhex, "%016llx", (unsigned long long)key);
+  const std::string so = work + "/libscion_layout_" + ident + "." + keyhex + ".so";
+  if (exists(so)) {
+    log += "reusing " + so + "\n";
+  } else {
   run("cd " + work + "/build && " + nvcc + " " + kBuildNvccFlags + inc + " -c inst_" + ident + ".cu -o inst_" + ident + ".o", log);
   run("cd " + work + "/build && " + nvcc + " " + kBuildNvccFlags + inc + " -x cu -c entry_" + ident + ".cpp -o entry_" + ident + ".o", log);
   run("cd " + work + "/build && /usr/bin/g++ " + kBuildCxxFlags + inc + " -frounding-math -c build_" + ident + ".cpp -o build_" + ident + ".o", log);
   run("cd " + work + "/build && " + nvcc + " -shared -o " + so + " inst_" + ident + ".o entry_" + ident + ".o build_" + ident + ".o " + library_path() +
           " -Xcompiler -fopenmp -lgomp -ldl -cudart shared",
       log);
+  }
   // 4. load + register
   void* h = dlopen(so.c_str(), RTLD_NOW | RTLD_LOCAL);
   if (!h) throw std::runtime_error(std::string("cannot load the layout plugin: ") + dlerror());

@@ -73,6 +73,9 @@ build BVH[order=pre] {
 """
 NAME = "user-q16-swapped"
 _state = {}
+# plugins compiled by the fixtures are kept here between test runs (the library keys them by everything they were compiled
+# from, so a stale one is never picked up)
+CACHE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), ".pytest_cache", "scion_plugins")
 
 
 @pytest.fixture(scope="session")
@@ -80,7 +83,8 @@ def user_layout(built):
     if not os.path.exists(os.environ.get("SCION_NVCC", "/usr/local/cuda/bin/nvcc")):
         pytest.skip("run-time layout plugins need nvcc")
     if "log" not in _state:
-        _state["log"] = built.register_layout(NAME, USER_LAYOUT)
+        os.makedirs(CACHE, exist_ok=True)
+        _state["log"] = built.register_layout(NAME, USER_LAYOUT, CACHE)
     return NAME
 
 
@@ -89,7 +93,7 @@ def test_register_compiles_and_lists_the_layout(built, user_layout):
     assert NAME not in [l["name"] for l in built.layouts()]  # the built-in registry (= the corpus) is unchanged
     info = built.layout_info(NAME)
     assert info["node_stride"] == 16 and info["family"] == 0
-    assert "nvcc" in _state["log"]
+    assert "nvcc" in _state["log"] or "reusing" in _state["log"]
     with pytest.raises(Exception):  # a name can be registered once
         built.register_layout(NAME, USER_LAYOUT)
     with pytest.raises(Exception):  # ill-formed layouts are rejected by the front end, nothing is compiled
@@ -183,7 +187,8 @@ def wide_layout(built):
     if not os.path.exists(os.environ.get("SCION_NVCC", "/usr/local/cuda/bin/nvcc")):
         pytest.skip("run-time layout plugins need nvcc")
     if "wide" not in _state:
-        _state["wide"] = built.register_layout(WIDE_NAME, wide_user_layout())
+        os.makedirs(CACHE, exist_ok=True)
+        _state["wide"] = built.register_layout(WIDE_NAME, wide_user_layout(), CACHE)
     return WIDE_NAME
 
 
@@ -227,3 +232,21 @@ def test_wide_user_layout_traverses_like_its_twin(built, wide_layout):
             assert torch.equal(a, b), v
     got = out[(WIDE_NAME, 1)][0].cpu().numpy().view(sb.HIT_DTYPE)
     assert (got["prim"] != sb.MISS_PRIM).mean() > 0.3
+
+
+def test_plugin_cache_is_reused_by_a_second_process(built, tmp_path):
+    """a caller that passes the same work_dir again gets the plugin it compiled before (keyed by the emitted header, the
+    stamped templates, the flags and the library): registration in a fresh process takes milliseconds"""
+    import subprocess
+    import sys
+    if not os.path.exists(os.environ.get("SCION_NVCC", "/usr/local/cuda/bin/nvcc")):
+        pytest.skip("run-time layout plugins need nvcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, time; sys.path.insert(0, %r); import paper_2511_15028_b200 as sb; from tests.test_open_world import USER_LAYOUT; t0 = time.time(); "
+            "log = sb.register_layout('cached-q16', USER_LAYOUT, %r); lt = sb.Scene.terrain(8, 1).build_sah(32, 4); "
+            "print('REUSED' if 'reusing' in log else 'BUILT', lt.encode('cached-q16').total_bytes)") % (root, str(tmp_path))
+    first = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root)
+    assert first.returncode == 0 and first.stdout.startswith("BUILT"), first.stderr[-1500:]
+    second = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root)
+    assert second.returncode == 0 and second.stdout.startswith("REUSED"), second.stderr[-1500:]
+    assert first.stdout.split()[1] == second.stdout.split()[1]
