@@ -198,9 +198,6 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes (3 = kPop of the
 #ifndef SCION_DUMMY_LD
 #define SCION_DUMMY_LD 0
 #endif
-#ifndef SCION_STASH_RAY
-#define SCION_STASH_RAY 0
-#endif
 #ifndef SCION_PF_TRI
 #define SCION_PF_TRI 0
 #endif
@@ -284,8 +281,7 @@ struct alignas(16) RayStash {
 };
 template <class L>
 SCION_DEV uint32_t coop_triangles2(const TreeView& T, bool own, float ox, float oy, float oz, float tmax, const RayStash* __restrict__ warp_stash,
-                                   uint32_t& prim_i, uint32_t prim_end, float& best_t, uint32_t& best_prim, CoopScratch2& sc,
-                                   const float4* __restrict__ warp_origin = nullptr) {
+                                   uint32_t& prim_i, uint32_t prim_end, float& best_t, uint32_t& best_prim, CoopScratch2& sc) {
   static_assert(L::kStride_primitives == 36, "Triangle stride");
   const unsigned lane = threadIdx.x & 31u;
   uint32_t tested = 0;
@@ -313,15 +309,10 @@ SCION_DEV uint32_t coop_triangles2(const TreeView& T, bool own, float ox, float 
     const unsigned o = sc.owner[first];
     const uint32_t kk = lane - first;
     RayCtx r;
-    if (warp_origin) {  // SCION_STASH_RAY: the owner's origin and tmax come from shared memory, its registers are free during the phase
-      const float4 og = warp_origin[o];
-      r.ox = og.x; r.oy = og.y; r.oz = og.z; r.tmax = og.w;
-    } else {
-      r.ox = __shfl_sync(kFullMask, ox, o);
-      r.oy = __shfl_sync(kFullMask, oy, o);
-      r.oz = __shfl_sync(kFullMask, oz, o);
-      r.tmax = __shfl_sync(kFullMask, tmax, o);
-    }
+    r.ox = __shfl_sync(kFullMask, ox, o);
+    r.oy = __shfl_sync(kFullMask, oy, o);
+    r.oz = __shfl_sync(kFullMask, oz, o);
+    r.tmax = __shfl_sync(kFullMask, tmax, o);
     const uint32_t pi = __shfl_sync(kFullMask, prim_i, o) + kk;
     float t = scion::inf();
     if (work) {
@@ -434,12 +425,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
   }
   __shared__ CoopScratch2 coop[BT / 32];
   __shared__ RayStash stash[BT];          // ray direction: only the leaf phase needs it
-#if SCION_STASH_RAY
-  // SCION_STASH_RAY: origin + tmax and reciprocal direction + sign word also live in shared memory; the leaf phase reads the
-  // owners' origins from there and the step's ray registers are re-loaded after the phase, so they are dead during it
-  __shared__ float4 stash_o[BT];
-  __shared__ float4 stash_rd[BT];
-#endif
   __shared__ unsigned long long stash_q[BT];  // query index: only the retire path needs it
   __shared__ uint2 stash_leaf[BT];        // parked primitive range [begin, end)
   Ref deep[LS::kDeep];
@@ -590,10 +575,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       if (!work.exhausted && work.refill(mode == kFetch, next, n, nq)) {
         ray = load_ray(rays, nq);
         stash[threadIdx.x] = RayStash{ray.dx, ray.dy, ray.dz, 0u};
-#if SCION_STASH_RAY
-        stash_o[threadIdx.x] = make_float4(ray.ox, ray.oy, ray.oz, ray.tmax);
-        stash_rd[threadIdx.x] = make_float4(ray.rdx, ray.rdy, ray.rdz, __uint_as_float(ray.neg));
-#endif
         stash_q[threadIdx.x] = nq;
         best_t = scion::inf();
         best_prim = SCION_MISS_PRIM;
@@ -617,16 +598,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       best_t = lo_.best_t;
       best_prim = lo_.best_prim;
       const uint32_t done = lo_.tested;
-#elif SCION_STASH_RAY
-      const uint32_t done = coop_triangles2<L>(T, own, 0.0f, 0.0f, 0.0f, 0.0f, stash + (threadIdx.x & ~31u), prim_i, range.y, best_t, best_prim, coop[threadIdx.x >> 5],
-                                               stash_o + (threadIdx.x & ~31u));
-      {  // the step's ray registers were dead during the phase: re-load them (volatile asm: the compiler cannot keep the old values instead)
-        uint32_t ao = (uint32_t)__cvta_generic_to_shared(&stash_o[threadIdx.x]), ar = (uint32_t)__cvta_generic_to_shared(&stash_rd[threadIdx.x]);
-        uint32_t ng;
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(ray.ox), "=f"(ray.oy), "=f"(ray.oz), "=f"(ray.tmax) : "r"(ao));
-        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=f"(ray.rdx), "=f"(ray.rdy), "=f"(ray.rdz), "=r"(ng) : "r"(ar));
-        ray.neg = ng;
-      }
 #else
       const uint32_t done = coop_triangles2<L>(T, own, ray.ox, ray.oy, ray.oz, ray.tmax, stash + (threadIdx.x & ~31u), prim_i, range.y, best_t,
                                                best_prim, coop[threadIdx.x >> 5]);
