@@ -185,7 +185,7 @@ SCION_DEV bool node_test(const TreeView& T, const RayCtx& ray, const typename L:
   }
 }
 
-enum : int { kFetch = 0, kNode = 1, kPrim = 2, kPrimSpec = 3 };  // lane modes (cpq2_kernel: 3 = kPop); kPrimSpec: parked with a leaf AND stepping through surely-culled stack entries (SCION_SPEC_POP): bit 0 = steps, bit 1 = owns a parked leaf
+enum : int { kFetch = 0, kNode = 1, kPrim = 2 };  // lane modes (3 = kPop of the closest-point kernel)
 #ifndef SCION_PREFETCH
 #define SCION_PREFETCH 1
 #endif
@@ -197,15 +197,6 @@ enum : int { kFetch = 0, kNode = 1, kPrim = 2, kPrimSpec = 3 };  // lane modes (
 #endif
 #ifndef SCION_DUMMY_LD
 #define SCION_DUMMY_LD 0
-#endif
-// SCION_SPEC_POP: a lane that waits with a parked leaf keeps stepping through the entries of its stack that are culled FOR
-// SURE — a box the ray misses, or an interior whose t_near is not below the lane's CURRENT best (the pending leaf can only
-// lower best, so the reference culls it too) — instead of idling until the cooperative leaf phase runs.  An entry whose test
-// could still go either way (an interior hit with t_near < best, a leaf hit) is left on the stack untouched and the lane stops
-// speculating.  Same decisions as the reference for every node, hence the same results and the same counters; only the
-// moment at which culled nodes are looked at moves.
-#ifndef SCION_SPEC_POP
-#define SCION_SPEC_POP 0
 #endif
 #ifndef SCION_PF_TRI
 #define SCION_PF_TRI 0
@@ -522,24 +513,12 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       }
     }
 #endif
-#if SCION_SPEC_POP
-    const bool spec = mode == kPrimSpec;
-    const Tally<COUNT> tally_before = tally;  // (instrumented build) an entry left on the stack is not a visit yet
-#endif
     tally.visit();
     float t_near;
     const bool hit = node_test<L>(T, ray, cur, node, t_near, tally);
     const bool leaf = node.variant == L::kLeaf;
     const bool p_prim = hit && leaf && (uint32_t)node.data.begin < (uint32_t)node.data.end;
     const bool p_push = hit && !leaf && t_near < best_t;
-#if SCION_SPEC_POP
-    if (spec && (p_prim || p_push)) {  // not culled for sure: back on the stack (its slot was never overwritten), stop speculating
-      top += LS::kSlot;
-      mode = kPrim;
-      if (COUNT) tally = tally_before;
-      return;
-    }
-#endif
     const uint32_t rel = top - window;
     // the common push (depth < kSmem) and pop (1 <= depth <= kSmem) are straight-line predicated
     // code; everything else (empty stack = retire, entries beyond the shared-memory window,
@@ -557,10 +536,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
           cur = node.left;
         }
       } else {
-#if SCION_SPEC_POP
-        if (spec) mode = kPrim;  // nothing left in the shared-memory window to look at: wait for the leaf phase
-        else
-#endif
         pop_or_retire();
       }
       return;
@@ -569,13 +544,6 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(my_leaf), "r"((uint32_t)node.data.begin), "r"((uint32_t)node.data.end));
       prefetch_triangles<L>(T, (uint32_t)node.data.begin, (uint32_t)node.data.end);
       mode = kPrim;
-#if SCION_SPEC_POP
-      if (rel - LS::kSlot < LS::kSmemBytes) {  // a pending entry in the shared-memory window: look at it while waiting
-        top -= LS::kSlot;
-        LS::load(top, cur);
-        mode = kPrimSpec;
-      }
-#endif
     } else if (p_push) {
       LS::store(top, node.right);
       if constexpr (kPrefetch) {
@@ -598,11 +566,7 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
     // ---- NODE: kInner steps per lane without looking at the rest of the warp
 #pragma unroll 1
     for (int k = 0; k < kInner; k++) {
-#if SCION_SPEC_POP
-      if (mode & 1) step();  // kNode and kPrimSpec
-#else
       if (mode == kNode) step();
-#endif
     }
     // ---- FETCH: refill idle lanes
     const unsigned idle = __ballot_sync(kFullMask, mode == kFetch);
@@ -622,18 +586,9 @@ __global__ void __launch_bounds__(BT, MINB) chrt2_kernel(const TreeView T, const
       if (work.exhausted && __ballot_sync(kFullMask, mode != kFetch) == 0u) break;
     }
     // ---- PRIM: all 32 lanes test the parked (owner, triangle) pairs
-#if SCION_SPEC_POP
-    const unsigned pmask = __ballot_sync(kFullMask, (mode & 2) != 0);
-#else
     const unsigned pmask = __ballot_sync(kFullMask, mode == kPrim);
-#endif
     if (pmask && (__popc(pmask) >= kPrimMin || __ballot_sync(kFullMask, mode == kNode) == 0u)) {
-#if SCION_SPEC_POP
-      const bool own = (mode & 2) != 0;
-      if (mode == kPrimSpec) top += LS::kSlot;  // the entry being looked at goes back: pop_or_retire() below takes it again
-#else
       const bool own = mode == kPrim;
-#endif
       uint2 range = make_uint2(0u, 0u);
       if (own) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(range.x), "=r"(range.y) : "r"(my_leaf));
       uint32_t prim_i = range.x;
