@@ -133,9 +133,31 @@ static int bench_multi(int G, scion_dtree* dt0, const scion_layout_info& li, con
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: scion_run layouts | footprint <layout> <scene>:<N> | bench <layout> <scene>:<N> <queries> [primary|secondary|points] [--host-encode]\n");
+    std::fprintf(stderr, "usage: scion_run layouts | footprint <layout> <scene>:<N> | bench <layout> <scene>:<N> <queries> [primary|secondary|points] [--host-encode] [--gpus G] [--layout-file FILE.scion]\n");
     return 2;
   }
+  // --layout-file FILE.scion (anywhere on the command line, repeatable): compile the file at run time and register it
+  // under its stem (my_layout.scion -> my-layout) before the command runs — scion_layout_register, needs nvcc
+  for (int i = 1; i + 1 < argc;) {
+    if (std::strcmp(argv[i], "--layout-file") != 0) { i++; continue; }
+    std::string path = argv[i + 1], name = path;
+    const size_t slash = name.rfind('/');
+    if (slash != std::string::npos) name = name.substr(slash + 1);
+    const size_t dot = name.rfind('.');
+    if (dot != std::string::npos) name = name.substr(0, dot);
+    for (auto& c : name) if (c == '_') c = '-';
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) { std::fprintf(stderr, "scion_run: cannot read %s\n", path.c_str()); return 2; }
+    std::string text;
+    char buf[4096];
+    for (size_t k; (k = std::fread(buf, 1, sizeof buf, f)) > 0;) text.append(buf, k);
+    std::fclose(f);
+    if (scion_layout_register(name.c_str(), text.c_str(), nullptr, nullptr) != SCION_OK) return die(1, "layout registration failed");
+    std::fprintf(stderr, "registered layout '%s' from %s\n", name.c_str(), path.c_str());
+    for (int k = i; k + 2 < argc; k++) argv[k] = argv[k + 2];  // drop the two arguments
+    argc -= 2;
+  }
+  if (argc < 2) return 2;
   const std::string cmd = argv[1];
   if (cmd == "layouts") {
     for (int i = 0; i < scion_layout_count(); i++) {

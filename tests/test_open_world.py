@@ -250,3 +250,19 @@ def test_plugin_cache_is_reused_by_a_second_process(built, tmp_path):
     second = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root)
     assert second.returncode == 0 and second.stdout.startswith("REUSED"), second.stderr[-1500:]
     assert first.stdout.split()[1] == second.stdout.split()[1]
+
+
+def test_native_harness_accepts_a_layout_file(built, tmp_path):
+    """the C++ harness (pure C ABI): `scion_run footprint <name> <scene> --layout-file FILE.scion`"""
+    import json
+    import subprocess
+    if not os.path.exists(os.environ.get("SCION_NVCC", "/usr/local/cuda/bin/nvcc")):
+        pytest.skip("run-time layout plugins need nvcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "paper_2511_15028_b200", "bin", "scion_run")
+    f = tmp_path / "native_q16_swapped.scion"
+    f.write_text(USER_LAYOUT)
+    r = subprocess.run([exe, "footprint", "native-q16-swapped", "terrain:16", "--layout-file", str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-1500:]
+    rep = json.loads(r.stdout)
+    assert rep["layout"] == "native-q16-swapped" and rep["node_stride"] == 16 and rep["primitives"] == 512
