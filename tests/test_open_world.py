@@ -147,6 +147,18 @@ def test_user_layout_traverses_like_its_twin(built, user_layout):
         assert torch.equal(a, b)
     got = out[NAME][0].cpu().numpy().view(sb.HIT_DTYPE)
     assert (got["prim"] != sb.MISS_PRIM).mean() > 0.3
+    # the third algorithm through the plugin's kernels: collision detection, same pair set and the same dual-tree recursion
+    from tests.test_collision import two_meshes
+    sa, sb2 = two_meshes(sb, 24)
+    la, lb = sa.build_median(1), sb2.build_median(1)
+    res = {}
+    for layout in (NAME, "pbrt-q16"):
+        da, db = la.encode(layout).upload(0), lb.encode(layout).upload(0)
+        res[layout] = da.collide_host(db, capacity=1 << 20)
+        da.free()
+        db.free()
+    assert res[NAME][1] == res["pbrt-q16"][1] > 0 and np.array_equal(res[NAME][0], res["pbrt-q16"][0])
+    assert res[NAME][2]["node_pairs"] == res["pbrt-q16"][2]["node_pairs"] and res[NAME][2]["tri_tests"] == res["pbrt-q16"][2]["tri_tests"]
 
 
 def test_cli_accepts_a_layout_file(built, tmp_path):
