@@ -487,6 +487,21 @@ def main():
                    "ms_per_step": t_e * 1e3, "matches_device_path": same,
                    "call": "scion_closest_hit_host_packed (host rays = the reference's packed 28-byte Ray record)" if chrt else "scion_closest_point_host"}
             if chrt:
+                try:  # rays with the DSL's default tmax = inf as origin + direction only (24 B): every ray of this workload is one
+                    d6 = d_q.view(torch.float32).view(-1, 8)[:, [0, 1, 2, 4, 5, 6]].contiguous()
+                    all_inf = bool(torch.isinf(d_q.view(torch.float32).view(-1, 8)[:, 3]).all().item())
+                    h6 = torch.empty(count * 24, dtype=torch.uint8).pin_memory()
+                    h6.copy_(d6.view(torch.uint8).view(-1))
+                    del d6
+                    hq6 = h6.numpy().view(np.float32).reshape(-1, 6)
+                    h_r.zero_()
+                    t24 = time_calls(lambda: dt.closest_hit_host_od(hq6, hr))
+                    e2e["default_tmax24"] = {"value": wl.total / t24 / 1e6, "ms_per_step": t24 * 1e3, "h2d_bytes_per_step": count * 24, "applicable": all_inf,
+                                             "matches_device_path": bool(torch.equal(h_r.to(dev), d_r)),
+                                             "call": "scion_closest_hit_host_od (origin + direction, tmax = inf implied: the DSL's default)"}
+                    del h6
+                except Exception as ex:
+                    e2e["default_tmax24"] = {"error": str(ex)[:160]}
                 try:  # the padded 32-byte scion_ray form of the same call
                     del h_q
                     h_q = torch.empty(count * q_bytes, dtype=torch.uint8).pin_memory()

@@ -360,6 +360,10 @@ int scion_closest_point_host(const scion_dtree* t, const float* h_points_xyz, ui
 int scion_closest_hit_host_packed(const scion_dtree* t, const float* h_rays7, uint64_t n, scion_hit* h_hits,
                                   uint32_t* h_status /* nullable */);
 int scion_rays_unpack(const float* d_rays7, uint64_t n, scion_ray* d_rays, void* stream);
+/* ... and for rays that carry the DSL's default tmax (`Ray(origin, direction)`: tmax = inf, geometry.scion:4): origin and
+ * direction only, 6 x f32 = 24 bytes per ray — with this form the call is no longer bound by the PCIe link on C5 */
+int scion_closest_hit_host_od(const scion_dtree* t, const float* h_rays6, uint64_t n, scion_hit* h_hits,
+                              uint32_t* h_status /* nullable */);
 
 /* ------------------------------------------------------------------------- */
 /* Query generators (src/rng.cpp placeholder): every query is

@@ -173,6 +173,7 @@ def lib() -> C.CDLL:
         "scion_collision_detection_host": (i32, [vp, vp, vp, u64, P(u64), P(CdStats)]),
         "scion_closest_hit_host": (i32, [vp, vp, u64, vp, vp]),
         "scion_closest_hit_host_packed": (i32, [vp, vp, u64, vp, vp]),
+        "scion_closest_hit_host_od": (i32, [vp, vp, u64, vp, vp]),
         "scion_rays_unpack": (i32, [vp, u64, vp, vp]),
         "scion_closest_point_host": (i32, [vp, vp, u64, vp, vp]),
         "scion_camera_default": (None, [P(C.c_float * 3), P(C.c_float * 3), i32, u32, u32, P(Camera)]),
@@ -644,6 +645,15 @@ class DeviceTree:
         if hits is None:
             hits = np.empty(n, HIT_DTYPE)
         _check(lib().scion_closest_hit_host_packed(self._h, rays7.ctypes.data, n, hits.ctypes.data, status.ctypes.data if status is not None else None))
+        return hits
+
+    def closest_hit_host_od(self, rays6: np.ndarray, hits: Optional[np.ndarray] = None, status: Optional[np.ndarray] = None):
+        """rays with the DSL's default tmax = inf: float32 [n, 6] = origin, direction"""
+        assert rays6.dtype == np.float32 and rays6.flags.c_contiguous and rays6.ndim == 2 and rays6.shape[1] == 6
+        n = rays6.shape[0]
+        if hits is None:
+            hits = np.empty(n, HIT_DTYPE)
+        _check(lib().scion_closest_hit_host_od(self._h, rays6.ctypes.data, n, hits.ctypes.data, status.ctypes.data if status is not None else None))
         return hits
 
     def closest_point_host(self, points: np.ndarray, out: Optional[np.ndarray] = None, status: Optional[np.ndarray] = None):

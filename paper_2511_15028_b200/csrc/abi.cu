@@ -871,24 +871,30 @@ int scion_collision_detection_host(const scion_dtree* a, const scion_dtree* b, s
 //   download(c) waits for kernel(c)
 // so the H2D copy engine never idles behind a kernel or a D2H copy of its own slot: the call runs at
 // the speed of the slowest of the three (on a PCIe Gen5 x16 B200 the 32-byte rays: ~55 GB/s).
+}  // extern "C"
 namespace scion {
 // the reference's packed Ray record (corpus/lib/geometry.scion:4: origin, direction, tmax — 7 x f32, 28 bytes) -> scion_ray
+// FLOATS = 7: origin, direction, tmax;  FLOATS = 6: origin, direction with the DSL's default tmax = inf (geometry.scion:4 `tmax = inf`)
+template <int FLOATS>
 __global__ void unpack_rays_kernel(const float* __restrict__ packed, uint64_t n, scion_ray* __restrict__ rays) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const float* p = packed + 7 * i;
-  const float ox = __ldcs(p), oy = __ldcs(p + 1), oz = __ldcs(p + 2), dx = __ldcs(p + 3), dy = __ldcs(p + 4), dz = __ldcs(p + 5), tmax = __ldcs(p + 6);
+  const float* p = packed + FLOATS * i;
+  const float ox = __ldcs(p), oy = __ldcs(p + 1), oz = __ldcs(p + 2), dx = __ldcs(p + 3), dy = __ldcs(p + 4), dz = __ldcs(p + 5);
+  const float tmax = FLOATS == 7 ? __ldcs(p + 6) : __uint_as_float(0x7f800000u);
   float4* o = reinterpret_cast<float4*>(rays + i);
   o[0] = make_float4(ox, oy, oz, tmax);
   o[1] = make_float4(dx, dy, dz, 0.0f);
 }
 }  // namespace scion
-static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uint64_t n, void* h_out, uint32_t* h_status, bool packed_rays = false) {
+extern "C" {
+static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uint64_t n, void* h_out, uint32_t* h_status, int packed_floats = 0) {
+  const bool packed_rays = packed_floats != 0;
   if (!ct || (!h_in && n) || (!h_out && n)) return fail(SCION_ERR_ARG, "null argument");
   scion_dtree* t = const_cast<scion_dtree*>(ct);
   std::lock_guard<std::mutex> lock(t->host_mutex);
   CUDA_OK(cudaSetDevice(t->device));
-  const uint64_t in_sz = hit ? (packed_rays ? 28 : sizeof(scion_ray)) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
+  const uint64_t in_sz = hit ? (packed_rays ? 4u * (uint64_t)packed_floats : sizeof(scion_ray)) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
   // chunk size: an eighth of the call, between 2^19 and 2^23 queries (every chunk kernel pays ~0.5 ms of
   // ramp-up and ragged tail, so small chunks are kernel-bound: 2^28 rays run in 225 / 224 / 185 / 183 ms
   // with 2^20 / 2^21 / 2^22 / 2^23-query chunks); SCION_HOST_CHUNK_LOG2 overrides
@@ -940,7 +946,8 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
       CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_in[k], 0));
       if (c >= (uint64_t)S) CUDA_OK(cudaStreamWaitEvent(s_run, t->ev_out[k], 0));
       if (packed_rays) {  // 28 -> 32 bytes on the device: ~0.1 ms per 2^23-ray chunk, behind the upload of the next chunk
-        scion::unpack_rays_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s_run>>>((const float*)t->pk[k], m, (scion_ray*)t->h2d[k]);
+        if (packed_floats == 7) scion::unpack_rays_kernel<7><<<(unsigned)((m + 255) / 256), 256, 0, s_run>>>((const float*)t->pk[k], m, (scion_ray*)t->h2d[k]);
+        else scion::unpack_rays_kernel<6><<<(unsigned)((m + 255) / 256), 256, 0, s_run>>>((const float*)t->pk[k], m, (scion_ray*)t->h2d[k]);
         CUDA_OK(cudaGetLastError());
         g_launches.fetch_add(1);
       }
@@ -969,12 +976,15 @@ int scion_closest_hit_host(const scion_dtree* t, const scion_ray* h_rays, uint64
   return run_query_host(t, true, h_rays, n, h_hits, h_status);
 }
 int scion_closest_hit_host_packed(const scion_dtree* t, const float* h_rays7, uint64_t n, scion_hit* h_hits, uint32_t* h_status) {
-  return run_query_host(t, true, h_rays7, n, h_hits, h_status, true);
+  return run_query_host(t, true, h_rays7, n, h_hits, h_status, 7);
+}
+int scion_closest_hit_host_od(const scion_dtree* t, const float* h_rays6, uint64_t n, scion_hit* h_hits, uint32_t* h_status) {
+  return run_query_host(t, true, h_rays6, n, h_hits, h_status, 6);
 }
 int scion_rays_unpack(const float* d_rays7, uint64_t n, scion_ray* d_rays, void* stream) {
   if ((!d_rays7 || !d_rays) && n) return fail(SCION_ERR_ARG, "null argument");
   if (n == 0) return SCION_OK;
-  scion::unpack_rays_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_rays7, n, d_rays);
+  scion::unpack_rays_kernel<7><<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_rays7, n, d_rays);
   CUDA_OK(cudaGetLastError());
   g_launches.fetch_add(1);
   return SCION_OK;

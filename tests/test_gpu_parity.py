@@ -380,6 +380,12 @@ def test_packed_ray_host_entry_is_identical(built, torch_cuda, world):
         assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), layout
         assert np.array_equal(sa, sb_), layout
         assert dt.closest_hit_host_packed(packed[:0]).shape[0] == 0
+        # origin + direction only (the DSL's default tmax = inf): equal to the padded call on rays whose tmax is inf
+        inf_rays = rays.copy()
+        inf_rays["tmax"] = np.inf
+        c = dt.closest_hit_host(inf_rays)
+        d = dt.closest_hit_host_od(np.ascontiguousarray(sb.pack_rays(inf_rays)[:, :6]))
+        assert np.array_equal(c.view(np.uint8), d.view(np.uint8)), layout
         dt.free()
     d_p = torch.from_numpy(packed.reshape(-1)).to("cuda:0")
     d_r = torch.full((rays.shape[0] * 8,), 5.0, dtype=torch.float32, device="cuda:0")
