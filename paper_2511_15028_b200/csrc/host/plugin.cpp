@@ -122,6 +122,8 @@ const BuilderEntry* dyn_find_builder(const char* layout) {
 
 // throws std::runtime_error / lc::LayoutError; `log` receives the commands and the compilers' output
 void register_layout_plugin(const std::string& name, const std::string& source, const std::string& work_dir_in, std::string& log) {
+  static std::mutex registration;  // registrations are serialised: the name check and the table updates belong together
+  std::lock_guard<std::mutex> one_at_a_time(registration);
   if (name.empty()) throw std::runtime_error("empty layout name");
   for (char c : name)
     if (!(isalnum((unsigned char)c) || c == '-' || c == '_')) throw std::runtime_error("layout names are [A-Za-z0-9_-]+");
