@@ -278,3 +278,67 @@ def test_native_harness_accepts_a_layout_file(built, tmp_path):
     assert r.returncode == 0, r.stderr[-1500:]
     rep = json.loads(r.stdout)
     assert rep["layout"] == "native-q16-swapped" and rep["node_stride"] == 16 and rep["primitives"] == 512
+
+
+def dop_user_layout():
+    """dop14 with the `---` separator removed: one 64-byte array-of-structures record instead of two 32-byte arrays — a
+    layout that is NOT a re-ordering of a shipped one (different buffer shape, no cold segment), same boxes and links"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_2511_15028_b200", "layouts", "dop14.scion")).read()
+    assert "    ---\n" in src
+    return src.replace("    ---\n", "")
+
+
+DOP_NAME = "user-dop14-aos"
+
+
+@pytest.fixture(scope="session")
+def dop_layout(built):
+    if not os.path.exists(os.environ.get("SCION_NVCC", "/usr/local/cuda/bin/nvcc")):
+        pytest.skip("run-time layout plugins need nvcc")
+    if "dop" not in _state:
+        os.makedirs(CACHE, exist_ok=True)
+        _state["dop"] = built.register_layout(DOP_NAME, dop_user_layout(), CACHE)
+    return DOP_NAME
+
+
+def test_dop_user_layout_plan_and_records(built, dop_layout):
+    info = built.layout_info(DOP_NAME)
+    assert info["family"] == 1 and info["node_stride"] == 64 and info["n_segments"] == 1
+    lt = built.Scene.terrain(15, 8).build_sah(32, 4)
+    mine, ref = lt.encode(DOP_NAME), lt.encode("dop14")
+    a = np.frombuffer(bytes([b for b in mine.buffers() if b["name"] == "nodes"][0]["data"]), np.uint8).reshape(-1, 64)
+    rb = [b for b in ref.buffers() if b["name"] == "nodes"][0]
+    raw = np.frombuffer(bytes(rb["data"]), np.uint8)
+    n = lt.nnodes
+    hot = raw[rb["seg_bases"][0]:rb["seg_bases"][0] + 32 * n].reshape(n, 32)
+    cold = raw[rb["seg_bases"][1]:rb["seg_bases"][1] + 32 * n].reshape(n, 32)
+    assert np.array_equal(a[:, :32], hot) and np.array_equal(a[:, 32:], cold)
+
+
+@pytest.mark.gpu
+def test_dop_user_layout_traverses_like_dop14(built, dop_layout):
+    import torch
+    sb = built
+    scene = sb.Scene.terrain(40, 2)
+    lt = scene.build_sah(32, 4)
+    lo, hi = scene.bounds()
+    cam = sb.default_camera(lo, hi, True, 64, 64)
+    rays = np.concatenate([sb.gen_primary_host(cam, 0, 64 * 64), sb.gen_secondary_host(lt.triangles(), 9, 0, 6000)])
+    pts = sb.gen_points_host(lo - 0.2, hi + 0.2, 4, 0, 3000)
+    n, m = rays.shape[0], pts.shape[0]
+    d_rays = torch.from_numpy(rays.view(np.uint8).reshape(-1)).to("cuda:0")
+    d_pts = torch.from_numpy(pts.reshape(-1)).to("cuda:0")
+    out = {}
+    for layout in (DOP_NAME, "dop14"):
+        dt = lt.encode(layout).upload(0)
+        h = torch.full((n * 8,), 0x5A, dtype=torch.uint8, device="cuda:0")
+        st = torch.full((n,), 7, dtype=torch.int32, device="cuda:0")
+        cp = torch.zeros(m * 20, dtype=torch.uint8, device="cuda:0")
+        dt.closest_hit(d_rays.data_ptr(), n, h.data_ptr(), st.data_ptr())
+        dt.closest_point(d_pts.data_ptr(), m, cp.data_ptr())
+        torch.cuda.synchronize()
+        out[layout] = (h, st, cp)
+        dt.free()
+    for a, b in zip(out[DOP_NAME], out["dop14"]):
+        assert torch.equal(a, b)

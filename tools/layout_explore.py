@@ -15,6 +15,7 @@ VARIANTS = [
     ("bvh8-q8-ci-align32", "bvh8-q8-ci", "bvh8_q8_ci", lambda t: t.replace("indirect group Interiors[size = interior_count]", "indirect group Interiors[size = interior_count, align = 32]")),
     ("bvh8-q8-ci-align128", "bvh8-q8-ci", "bvh8_q8_ci", lambda t: t.replace("indirect group Interiors[size = interior_count]", "indirect group Interiors[size = interior_count, align = 128]")),
     ("bvh8-q16-ci-align32", "bvh8-q16-ci", "bvh8_q16_ci", lambda t: t.replace("indirect group Interiors[size = interior_count]", "indirect group Interiors[size = interior_count, align = 32]")),
+    ("dop14-aos", "dop14", "dop14", lambda t: t.replace("    ---\n", "")),
     ("pbrt-q16-align32", "pbrt-q16", "pbrt_q16", lambda t: t.replace("group nodes[size = node_count, align = 16]", "group nodes[size = node_count, align = 32]")),
 ]
 
