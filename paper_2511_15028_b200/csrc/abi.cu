@@ -895,11 +895,12 @@ static int run_query_host(const scion_dtree* ct, bool hit, const void* h_in, uin
   std::lock_guard<std::mutex> lock(t->host_mutex);
   CUDA_OK(cudaSetDevice(t->device));
   const uint64_t in_sz = hit ? (packed_rays ? 4u * (uint64_t)packed_floats : sizeof(scion_ray)) : 12, out_sz = hit ? sizeof(scion_hit) : sizeof(scion_cp);
-  // chunk size: an eighth of the call, between 2^19 and 2^23 queries (every chunk kernel pays ~0.5 ms of
+  // chunk size: an eighth of the call, between 2^17 and 2^23 queries (every chunk kernel pays ~0.5 ms of
   // ramp-up and ragged tail, so small chunks are kernel-bound: 2^28 rays run in 225 / 224 / 185 / 183 ms
-  // with 2^20 / 2^21 / 2^22 / 2^23-query chunks); SCION_HOST_CHUNK_LOG2 overrides
+  // with 2^20 / 2^21 / 2^22 / 2^23-query chunks; a small call wants its copies overlapped all the same: 2^20 rays of C1
+  // run in 0.84 / 0.72 / 0.69 / 0.87 ms with 2^19 / 2^18 / 2^17 / 2^16-query chunks); SCION_HOST_CHUNK_LOG2 overrides
   static const int forced_log2 = [] { const char* e = getenv("SCION_HOST_CHUNK_LOG2"); int l = e ? atoi(e) : 0; return l ? (l < 10 ? 10 : (l > 26 ? 26 : l)) : 0; }();
-  uint64_t kChunk = 1ull << 19;
+  uint64_t kChunk = 1ull << 17;
   if (forced_log2) kChunk = 1ull << forced_log2;
   else while (kChunk < (1ull << 23) && kChunk * 8 < n) kChunk <<= 1;
   constexpr int S = scion_dtree::kSlots;
