@@ -45,7 +45,10 @@ def cmd_check(_):
             plan = sb.layout_plan(l["name"])
             text = sb.emit_cuda(l["name"])
             assert "static void decode(" in text
-            print(f"{l['name']:14s} ok   family={('bvh2', 'dop14', 'bvh8')[l['family']]} node_stride={l['node_stride']} segments={l['n_segments']} slots={len(plan['slots'])}")
+            has_build = bool(sb.lib().scion_layout_has_build(l["name"].encode()))
+            assert has_build == ("static uint64_t build_node(" in text)
+            print(f"{l['name']:22s} ok   family={('bvh2', 'dop14', 'bvh8')[l['family']]} node_stride={l['node_stride']} segments={l['n_segments']} slots={len(plan['slots'])} "
+                  f"constructors={'compiled' if has_build else 'none'}")
         except Exception as e:  # noqa: BLE001
             ok = False
             print(f"{l['name']:14s} FAILED {e}", file=sys.stderr)
